@@ -1,0 +1,223 @@
+/*
+ * gace.h -- C-ABI of the B200-native GACE selectivity probe.
+ *
+ * What it computes: the Measurement Engine's probe (arxiv 2512.19750,
+ * PAPER.md §III-B "Measurement Engine (GPU-based Probing)", lines 54-55, and
+ * §IV-H "Key-Only + Bitmask", lines 250-251): one key-only pass over columnar
+ * int32 / int64 keys, optionally Bernoulli-sampled by a seeded per-row hash,
+ * producing per-predicate match counts, pairwise joint counts (the P(A,B) of
+ * PCS, Eq. 3, lines 73-78) and per-column HyperLogLog registers (the NDV_est
+ * of the drift D, Eq. 1, lines 60-65).  Exact semantics: DESIGN.md
+ * "Semantics" (= SURVEY.md §8(c) steps 1-8) and the readings listed there.
+ *
+ * Conventions (all calls):
+ *  - Every call returns gace_status.  On any non-OK status no output is
+ *    written (all validation happens before any launch); gace_last_error()
+ *    returns a thread-local message.  No C++ exception crosses this ABI.
+ *  - Host pointers are read only during the call.  Device pointers are
+ *    borrowed, never freed.  The library owns all scratch it allocates.
+ *  - No CPU fallback: without a usable CUDA device attach fails with
+ *    GACE_ECUDA.  gace_derive / gace_gate are host-only (no device needed).
+ */
+#ifndef GACE_H_
+#define GACE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GACE_OK = 0,
+    GACE_EINVAL = 1,        /* invalid argument (NULL, range, alignment, index)          */
+    GACE_ENOMEM = 2,        /* device / pinned allocation failed                         */
+    GACE_ECUDA = 3,         /* CUDA runtime error, or no CUDA device                     */
+    GACE_ENCCL = 4,         /* NCCL unavailable or failed                                */
+    GACE_EHANDLE = 5,       /* NULL or already-detached table handle                     */
+    GACE_EUNSUPPORTED = 6   /* legal request outside this build's limits (see below)     */
+} gace_status;
+
+typedef enum { GACE_I32 = 0, GACE_I64 = 1 } gace_dtype;
+
+/* Predicate operators (=, <, <=, >, >=, BETWEEN; reading L9).
+ * Comparison is exact signed int64: v = (int64)x[r] against int64 bounds, also
+ * on int32 columns, so bounds outside the column dtype are legal (L10).        */
+typedef enum {
+    GACE_EQ = 0,            /* v == a                                                    */
+    GACE_LT = 1,            /* v <  a                                                    */
+    GACE_LE = 2,            /* v <= a                                                    */
+    GACE_GT = 3,            /* v >  a                                                    */
+    GACE_GE = 4,            /* v >= a                                                    */
+    GACE_BETWEEN = 5        /* a <= v && v <= b  (inclusive; a > b is the empty predicate) */
+} gace_op;
+
+#define GACE_PRED_NEGATE 1u /* flags bit: logical NOT of the operator (gives !=, NOT BETWEEN) */
+
+/* One candidate predicate, 24 bytes.  `b` is read for BETWEEN only. */
+typedef struct {
+    uint32_t col;           /* column index into the attached table, < ncols             */
+    uint16_t op;            /* gace_op                                                   */
+    uint16_t flags;         /* 0 or GACE_PRED_NEGATE                                     */
+    int64_t a;
+    int64_t b;
+} gace_pred;
+
+/* A pair flagged for a correlation check: joint = #{sampled rows where predicates
+ * i and j both hold} (reading L18: i == j, same-column pairs, duplicates allowed). */
+typedef struct {
+    uint32_t i, j;          /* indices into the predicate batch, < npreds                */
+} gace_pair;
+
+/* Multi-GPU description: rows are sharded contiguously, one
+ * process per GPU.  row_offset = global id of this shard's first row (reading
+ * L7: the sample bit uses global row ids, so results are shard-invariant).
+ * Either nccl_unique_id (128 bytes from ncclGetUniqueId on rank 0, broadcast by
+ * the caller) or an existing nccl_comm (ncclComm_t, not destroyed by detach).  */
+typedef struct {
+    int rank;
+    int nranks;
+    uint64_t row_offset;
+    uint64_t nrows_total;
+    const void *nccl_unique_id;
+    void *nccl_comm;
+} gace_dist;
+
+typedef struct gace_table gace_table;   /* opaque */
+
+/* Limits of this build (GACE_EINVAL beyond the first three, GACE_EUNSUPPORTED beyond
+ * the rest):  ncols <= 64; npreds <= 4096; npairs <= 4096; hll_p == 12; at most 8
+ * distinct probed columns (columns referenced by a predicate or by hll_col_mask)
+ * per gace_probe call; the per-probe plan must fit one CTA's shared memory.     */
+#define GACE_MAX_COLS 64
+#define GACE_MAX_PREDS 4096
+#define GACE_MAX_PAIRS 4096
+#define GACE_MAX_PROBED_COLS 8
+#define GACE_HLL_P 12
+
+/*
+ * Attach a device-resident table.
+ *   col_dev_ptrs[c]  device pointer to nrows_local values of column c, dtype dtypes[c],
+ *                    16-byte aligned (GACE_EINVAL otherwise).  Borrowed: must stay valid
+ *                    and unmodified until detach.  Column-major, one array per column.
+ *   dist             NULL = single GPU, row_offset 0; else gace_dist above (collective:
+ *                    every rank calls attach; NCCL comm created here if an id is given).
+ *   device           CUDA device ordinal.
+ *   cuda_stream      cudaStream_t all work is issued on (NULL = a library-owned stream).
+ * One-time work: a min/max pass per column (the table is immutable while attached).
+ */
+gace_status gace_table_attach(const void *const *col_dev_ptrs, const gace_dtype *dtypes,
+                              uint32_t ncols, uint64_t nrows_local, const gace_dist *dist,
+                              int device, void *cuda_stream, gace_table **out);
+
+/*
+ * Attach a HOST-resident table (§IV-B Exp. A "Key-only = True": the keys cross
+ * PCIe on every probe).  col_host_ptrs[c] are host arrays (pinned for full speed);
+ * every gace_probe streams the probed columns to the device in chunks on a copy
+ * stream, overlapped with the scan of the previous chunk.  Same ownership rules.
+ */
+gace_status gace_table_attach_host(const void *const *col_host_ptrs, const gace_dtype *dtypes,
+                                   uint32_t ncols, uint64_t nrows_local, const gace_dist *dist,
+                                   int device, void *cuda_stream, gace_table **out);
+
+/* Free everything the library allocated for t (never the borrowed columns). */
+gace_status gace_table_detach(gace_table *t);
+
+/*
+ * The probe (north star: counts, joint_counts, hll_regs).
+ *   preds[npreds], pairs[npairs]   host arrays (validated before any launch)
+ *   sample_rate                    in [0,1]; 1 = every row (NaN / out of range: EINVAL)
+ *   seed                           sample seed: keep(r) = u(seed,r) < floor(rate*2^64),
+ *                                  u = (r+1)-th SplitMix64 output (reading L6/L8)
+ *   hll_col_mask                   bit c = HLL over column c (< ncols)
+ *   hll_p                          must be 12 (GACE_EUNSUPPORTED otherwise)
+ * Outputs (host, caller-allocated; merged over all ranks when attached with dist):
+ *   *n_sampled                     number of kept rows
+ *   counts[npreds]                 count[p] = #{kept r : pred_p(x[r])}
+ *   joint_counts[npairs]           may be NULL iff npairs == 0
+ *   hll_regs[popcount(mask)][4096] u8 registers, ascending column order; may be NULL
+ *                                  iff mask == 0 (sampled rows only, reading L4)
+ * Synchronous: returns once the results are in host memory.  One probe in flight per
+ * handle.  Collective over ranks when attached with dist (identical arguments).
+ */
+gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds,
+                       const gace_pair *pairs, uint32_t npairs, double sample_rate,
+                       uint64_t seed, uint64_t hll_col_mask, uint32_t hll_p,
+                       uint64_t *n_sampled, uint64_t *counts, uint64_t *joint_counts,
+                       uint8_t *hll_regs);
+
+/* Test hook: the deterministic sample mask of this shard's rows, bit-packed:
+ * bit (r % 64) of bits[r / 64] = keep(row_offset + r); bits has ceil(nrows_local/64)
+ * words (host).  Device tables only.                                               */
+gace_status gace_sample_mask(gace_table *t, double sample_rate, uint64_t seed, uint64_t *bits);
+
+/*
+ * Derived doubles (host only, Eq. 1-3):
+ *   sel[p]     = counts[p] / n_sampled                   (NaN when n_sampled == 0)
+ *   pcs[q]     = (J/n) / ((A/n) * (B/n))                 (NaN when n == 0 or A*B == 0)
+ *   ndv_est[c] = HLL estimate of regs[c] (raw, linear counting when E <= 2.5m and V > 0)
+ *   drift[c]   = |ndv_hist[c] - ndv_est[c]| / ndv_hist[c] (ndv_hist[c] <= 0: EINVAL)
+ * Any of the output arrays may be NULL (not computed).  regs may be NULL iff
+ * ncols_hll == 0; ndv_hist may be NULL iff drift is NULL.
+ */
+gace_status gace_derive(uint64_t n_sampled, const uint64_t *counts, uint32_t npreds,
+                        const gace_pair *pairs, const uint64_t *joints, uint32_t npairs,
+                        const uint8_t *regs, uint32_t ncols_hll, uint32_t hll_p,
+                        const double *ndv_hist, double *sel, double *pcs, double *ndv_est,
+                        double *drift);
+
+/* Gate thresholds; NULL = the paper's: D >= 0.25 (line 65), |dS| > 0.01 (line 69),
+ * PCS > 1.6 or PCS < 0.7 (line 78). */
+typedef struct {
+    double d_threshold;
+    double sel_err_threshold;
+    double pcs_high;
+    double pcs_low;
+} gace_thresholds;
+
+enum { GACE_SIG_DRIFT = 1, GACE_SIG_SEL_ERROR = 2, GACE_SIG_CORRELATION = 4 };
+
+/*
+ * Risky Gate (§III-A, lines 45-52): fired_mask = OR of
+ *   DRIFT        if any drift[k] >= d_threshold
+ *   SEL_ERROR    if any |s_est[k] - s_probe[k]| > sel_err_threshold
+ *   CORRELATION  if any pcs[k] > pcs_high or pcs[k] < pcs_low
+ * NaN never fires.  per_signal_fired (optional) gets nd + ns + np bytes (0/1) in
+ * that order.  The probe is recommended iff fired_mask != 0.
+ */
+gace_status gace_gate(const double *drift, uint32_t nd, const double *s_est,
+                      const double *s_probe, uint32_t ns, const double *pcs, uint32_t np,
+                      const gace_thresholds *th, uint32_t *fired_mask,
+                      uint8_t *per_signal_fired);
+
+/* Per-stage device times of the last gace_probe on t, in ms (CUDA events on the
+ * table's stream; §IV-B overhead decomposition H2D / kernel / D2H / reduction). */
+typedef struct {
+    double plan_upload_ms;  /* H2D of the predicate plan                               */
+    double h2d_ms;          /* H2D of key columns (host tables; 0 for device tables)   */
+    double scan_ms;         /* probe kernel(s): the HBM pass                           */
+    double finalize_ms;     /* block partials -> counts / joints / registers           */
+    double merge_ms;        /* NCCL all-reduce sum + max (0 on one GPU)                */
+    double d2h_ms;          /* results to host                                         */
+    double total_ms;        /* first to last event                                     */
+    uint64_t scan_launches; /* probe-kernel launches in that call                      */
+    uint64_t bytes_scanned; /* algorithmic bytes: rows x sum of probed column widths   */
+} gace_timing;
+
+gace_status gace_last_timing(const gace_table *t, gace_timing *out);
+
+/* Rank 0 of a multi-GPU job: fill id[128] with a fresh ncclUniqueId to broadcast to
+ * the other ranks (GACE_ENCCL if libnccl.so.2 cannot be loaded). */
+gace_status gace_nccl_unique_id(void *id128);
+
+/* Number of this library's CUDA kernels launched since load (all tables). */
+uint64_t gace_kernel_launches(void);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char *gace_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GACE_H_ */

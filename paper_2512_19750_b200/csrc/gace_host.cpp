@@ -1,0 +1,1133 @@
+// gace_host.cpp -- C-ABI of the GACE selectivity probe (include/gace.h):
+// table handles, the predicate planner, launch orchestration, the NCCL merge
+// and the host-side derive / gate arithmetic.
+//
+// Planner: every predicate becomes a
+// closed int64 interval (plus a negate flag), clipped to the column's value
+// domain; the interval ends give the column's sorted breakpoints T, so each
+// predicate is a contiguous range of buckets bucket(v) = #{t in T : t <= v} and
+// count = (prefix-sum difference over a per-column bucket histogram).  Pairs on
+// one column are interval intersections of those ranges (no per-row work);
+// pairs across two columns share one 2-D histogram per column pair over the
+// sub-buckets of only the pair-relevant predicates.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gace.h"
+#include "gace_kernels.h"
+#include "gace_plan.h"
+
+using namespace gace;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+gace_status fail(gace_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                              \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return fail(GACE_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ------------------------------------------------------------------ NCCL via dlopen
+
+struct NcclUid { char internal[128]; };
+struct Nccl {
+    void *h = nullptr;
+    int (*GetUniqueId)(NcclUid *) = nullptr;
+    int (*CommInitRank)(void **, int, NcclUid, int) = nullptr;
+    int (*AllReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    int (*CommDestroy)(void *) = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+};
+constexpr int kNcclUint8 = 1, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2;
+
+Nccl *nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *nm : names) {
+            n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (n.h) break;
+        }
+        if (!n.h) return;
+        n.GetUniqueId = (int (*)(NcclUid *))dlsym(n.h, "ncclGetUniqueId");
+        n.CommInitRank = (int (*)(void **, int, NcclUid, int))dlsym(n.h, "ncclCommInitRank");
+        n.AllReduce = (int (*)(const void *, void *, size_t, int, int, void *, cudaStream_t))dlsym(n.h, "ncclAllReduce");
+        n.GroupStart = (int (*)())dlsym(n.h, "ncclGroupStart");
+        n.GroupEnd = (int (*)())dlsym(n.h, "ncclGroupEnd");
+        n.CommDestroy = (int (*)(void *))dlsym(n.h, "ncclCommDestroy");
+        n.GetErrorString = (const char *(*)(int))dlsym(n.h, "ncclGetErrorString");
+        if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.GroupStart || !n.GroupEnd || !n.CommDestroy)
+            n.h = nullptr;
+    });
+    return n.h ? &n : nullptr;
+}
+
+// ------------------------------------------------------------------ buffers
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T *as(size_t byte_off = 0) const { return reinterpret_cast<T *>(static_cast<char *>(p) + byte_off); }
+};
+
+struct HostBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(&p, n);
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T *as(size_t byte_off = 0) const { return reinterpret_cast<T *>(static_cast<char *>(p) + byte_off); }
+};
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+}  // namespace
+
+constexpr uint32_t kMagic = 0x47414345u;   // "GACE"
+constexpr int kNumEv = 8;
+
+struct gace_table {
+    uint32_t magic = kMagic;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool host = false;
+    uint32_t ncols = 0;
+    uint64_t nrows = 0;
+    std::vector<const void *> cols;
+    std::vector<int> dtypes;
+    std::vector<int64_t> dlo, dhi;     // value domain per column (measured for device tables)
+    bool has_dist = false;
+    gace_dist dist{};
+    void *comm = nullptr;
+    bool own_comm = false;
+    int sms = 148;
+    DevBuf d_plan, d_acc, d_pre, d_part, d_out, d_nsamp, d_mask, d_stage[2];
+    HostBuf h_plan, h_out;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev[kNumEv]{};
+    cudaEvent_t ev_copied[2]{}, ev_free[2]{}, ev_c0{}, ev_c1{};
+    gace_timing last{};
+    std::mutex mu;
+};
+
+namespace {
+
+// ------------------------------------------------------------------ planner
+
+struct Interval {      // closed int64 interval after clipping to the column domain
+    bool empty = true;
+    int64_t lo = 0, hi = 0;
+};
+
+// PAPER-side semantics (DESIGN.md "Semantics" 4, readings L9/L10): op -> closed interval.
+Interval op_interval(const gace_pred &p) {
+    Interval I;
+    const int64_t a = p.a, b = p.b;
+    I.empty = false;
+    switch (p.op) {
+        case GACE_EQ: I.lo = a; I.hi = a; break;
+        case GACE_LT:
+            if (a == INT64_MIN) I.empty = true; else { I.lo = INT64_MIN; I.hi = a - 1; }
+            break;
+        case GACE_LE: I.lo = INT64_MIN; I.hi = a; break;
+        case GACE_GT:
+            if (a == INT64_MAX) I.empty = true; else { I.lo = a + 1; I.hi = INT64_MAX; }
+            break;
+        case GACE_GE: I.lo = a; I.hi = INT64_MAX; break;
+        default:   // BETWEEN
+            if (a > b) I.empty = true; else { I.lo = a; I.hi = b; }
+    }
+    return I;
+}
+
+Interval clip(Interval I, int64_t dl, int64_t dh) {
+    if (I.empty) return I;
+    I.lo = std::max(I.lo, dl);
+    I.hi = std::min(I.hi, dh);
+    if (I.lo > I.hi) I.empty = true;
+    return I;
+}
+
+void add_breakpoints(const Interval &I, int64_t dl, int64_t dh, std::vector<int64_t> &T) {
+    if (I.empty) return;
+    if (I.lo > dl) T.push_back(I.lo);
+    if (I.hi < dh) T.push_back(I.hi + 1);
+}
+
+uint32_t count_le(const std::vector<int64_t> &T, int64_t x) {
+    return (uint32_t)(std::upper_bound(T.begin(), T.end(), x) - T.begin());
+}
+
+struct SlotPlan {
+    int col = -1;
+    int dtype = 0;
+    bool has_preds = false, has_hll = false;
+    int64_t dl = 0, dh = 0;
+    std::vector<int64_t> T;            // sorted unique breakpoints
+    uint32_t nb = 1;
+    // LUT
+    uint8_t mode = MODE_NOPRED;
+    bool clamp = false;
+    int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
+    uint32_t s1 = 0;
+    std::vector<uint2> l1, l2;         // entries with slot-relative indices (fixed up later)
+    // layout
+    uint32_t lut_idx = 0, l2_idx = 0, hist_idx = 0, hll_off = kNone, bps_off = 0, pre = 0;
+};
+
+// Build the two-level LUT of a slot for level-1 shift s1 over offsets [0, span].
+// Entries hold RELATIVE bucket numbers and RELATIVE L2 indices here.
+void build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
+    std::vector<uint64_t> toff;
+    toff.reserve(S.T.size());
+    for (int64_t t : S.T) toff.push_back((uint64_t)t - (uint64_t)S.base);   // in [1, span]
+    auto le = [&](uint64_t x) { return (uint32_t)(std::upper_bound(toff.begin(), toff.end(), x) - toff.begin()); };
+    S.s1 = s1;
+    S.l1.clear();
+    S.l2.clear();
+    const uint64_t ncells = (span >> s1) + 1;
+    const uint64_t csize = 1ull << s1;
+    for (uint64_t k = 0; k < ncells; ++k) {
+        const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
+        const uint32_t b0 = le(lo), b1 = le(hi);
+        if (b1 - b0 == 0) {
+            S.l1.push_back(make_uint2(b0, kNoThr));
+        } else if (b1 - b0 == 1) {
+            S.l1.push_back(make_uint2(b0, (uint32_t)(toff[b0] - 1)));
+        } else {
+            uint64_t gap = UINT64_MAX;
+            for (uint32_t i = b0 + 1; i < b1; ++i) gap = std::min(gap, toff[i] - toff[i - 1]);
+            uint32_t s2 = 0;
+            while (s2 + 1 < s1 && (2ull << s2) <= gap) ++s2;            // 2^s2 <= gap
+            const uint64_t nsub = ((hi - lo) >> s2) + 1;
+            S.l1.push_back(make_uint2(kL2Flag | (s2 << 24), (uint32_t)S.l2.size()));
+            for (uint64_t j = 0; j < nsub; ++j) {
+                const uint64_t slo = lo + (j << s2), shi = std::min<uint64_t>(slo + (1ull << s2) - 1, hi);
+                const uint32_t c0 = le(slo), c1 = le(shi);
+                S.l2.push_back(make_uint2(c0, c1 == c0 ? kNoThr : (uint32_t)(toff[c0] - 1)));
+            }
+        }
+    }
+}
+
+struct Group {
+    int a, b;                          // slots a < b
+    std::vector<int64_t> TA, TB;       // pair-relevant breakpoints (subsets of T_a, T_b)
+    uint32_t na = 1, nbb = 1;
+    bool direct = false;
+    uint32_t mapA_idx = 0, mapB_idx = 0, grid_rel = 0, sat = 0;
+};
+
+struct Plan {
+    std::vector<SlotPlan> slots;
+    std::vector<int> col2slot;
+    std::vector<Interval> iv;          // per predicate, clipped
+    std::vector<int> pslot;            // per predicate
+    std::vector<Group> groups;
+    std::map<std::pair<int, int>, int> gidx;
+    bool clamp = false;
+    // layout results
+    std::vector<uint8_t> image;        // shared-memory image (tables + maps)
+    uint32_t acc_idx = 0, acc_words = 0, hll_off = 0, hll_bytes = 0, smem_bytes = 0;
+    uint32_t pre_words = 0;
+    std::vector<DirectPair> direct;
+    std::vector<FinJob> jobs;
+    std::vector<FinPred> fpreds;
+    std::vector<FinPair> fpairs;
+    std::vector<int64_t> bps;          // MODE_SEARCH breakpoints, concatenated
+    ProbeParams P{};
+};
+
+constexpr size_t kSmemBudget = kMaxSmem - 1024;   // keep 1 KB for static shared memory
+
+gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
+                      uint32_t nq, uint64_t hll_mask, Plan &pl) {
+    // ---- slots: probed columns in ascending order
+    std::vector<bool> probed(t->ncols, false);
+    for (uint32_t p = 0; p < np; ++p) probed[preds[p].col] = true;
+    for (uint32_t c = 0; c < t->ncols; ++c)
+        if (hll_mask >> c & 1ull) probed[c] = true;
+    pl.col2slot.assign(t->ncols, -1);
+    for (uint32_t c = 0; c < t->ncols; ++c) {
+        if (!probed[c]) continue;
+        if (pl.slots.size() == (size_t)kMaxSlots)
+            return fail(GACE_EUNSUPPORTED, "more than 8 probed columns in one probe");
+        pl.col2slot[c] = (int)pl.slots.size();
+        SlotPlan S;
+        S.col = (int)c;
+        S.dtype = t->dtypes[c];
+        S.dl = t->dlo[c];
+        S.dh = t->dhi[c];
+        S.has_hll = (hll_mask >> c) & 1ull;
+        pl.slots.push_back(S);
+    }
+    // ---- predicates -> clipped intervals -> breakpoints
+    pl.iv.resize(np);
+    pl.pslot.resize(np);
+    for (uint32_t p = 0; p < np; ++p) {
+        const int s = pl.col2slot[preds[p].col];
+        SlotPlan &S = pl.slots[s];
+        pl.pslot[p] = s;
+        S.has_preds = true;
+        pl.iv[p] = clip(op_interval(preds[p]), S.dl, S.dh);
+        add_breakpoints(pl.iv[p], S.dl, S.dh, S.T);
+    }
+    for (auto &S : pl.slots) {
+        std::sort(S.T.begin(), S.T.end());
+        S.T.erase(std::unique(S.T.begin(), S.T.end()), S.T.end());
+        S.nb = (uint32_t)S.T.size() + 1;
+    }
+    // ---- pairs -> groups
+    pl.fpairs.resize(nq);
+    for (uint32_t q = 0; q < nq; ++q) {
+        const int si = pl.pslot[pairs[q].i], sj = pl.pslot[pairs[q].j];
+        if (si == sj) continue;
+        const int a = std::min(si, sj), b = std::max(si, sj);
+        auto key = std::make_pair(a, b);
+        if (!pl.gidx.count(key)) {
+            pl.gidx[key] = (int)pl.groups.size();
+            Group G;
+            G.a = a;
+            G.b = b;
+            pl.groups.push_back(G);
+        }
+        Group &G = pl.groups[pl.gidx[key]];
+        const uint32_t pa = (si == a) ? pairs[q].i : pairs[q].j;
+        const uint32_t pb = (si == a) ? pairs[q].j : pairs[q].i;
+        add_breakpoints(pl.iv[pa], pl.slots[a].dl, pl.slots[a].dh, G.TA);
+        add_breakpoints(pl.iv[pb], pl.slots[b].dl, pl.slots[b].dh, G.TB);
+    }
+    size_t fixed = 0;
+    for (auto &S : pl.slots) {
+        if (S.has_preds) fixed += 4ull * S.nb;
+        if (S.has_hll) fixed += kHllM;
+    }
+    for (auto &G : pl.groups) {
+        std::sort(G.TA.begin(), G.TA.end());
+        G.TA.erase(std::unique(G.TA.begin(), G.TA.end()), G.TA.end());
+        std::sort(G.TB.begin(), G.TB.end());
+        G.TB.erase(std::unique(G.TB.begin(), G.TB.end()), G.TB.end());
+        G.na = (uint32_t)G.TA.size() + 1;
+        G.nbb = (uint32_t)G.TB.size() + 1;
+    }
+    // grids in increasing size while they fit half the budget; the rest evaluate per row
+    {
+        std::vector<int> order(pl.groups.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+        std::sort(order.begin(), order.end(), [&](int x, int y) {
+            return (uint64_t)pl.groups[x].na * pl.groups[x].nbb < (uint64_t)pl.groups[y].na * pl.groups[y].nbb;
+        });
+        size_t used = 0;
+        for (int gi : order) {
+            Group &G = pl.groups[gi];
+            const size_t need = 4ull * ((uint64_t)G.na * G.nbb + pl.slots[G.a].nb + pl.slots[G.b].nb) + 64;
+            if (fixed + used + need <= kSmemBudget / 2) used += need;
+            else G.direct = true;
+        }
+        fixed += used;
+    }
+    size_t ndirect = 0;
+    for (uint32_t q = 0; q < nq; ++q) {
+        const int si = pl.pslot[pairs[q].i], sj = pl.pslot[pairs[q].j];
+        if (si != sj && pl.groups[pl.gidx[std::make_pair(std::min(si, sj), std::max(si, sj))]].direct) ++ndirect;
+    }
+    fixed += 4 * ndirect + 256;
+    if (fixed > kSmemBudget)
+        return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory (" + std::to_string(fixed) + " B)");
+
+    // ---- lookup tables within the remaining budget
+    const size_t lut_budget = kSmemBudget - fixed;
+    for (auto &S : pl.slots) {
+        if (!S.has_preds) continue;
+        S.mode = MODE_LUT;
+        S.clamp = false;
+        if (S.T.empty()) {                       // every value in bucket 0
+            S.base = S.dl;
+            S.clamp = true;
+            S.clamp_lo = S.clamp_hi = S.dl;
+        } else if ((uint64_t)S.dh - (uint64_t)S.dl < (1ull << 32) && !t->host) {
+            S.base = S.dl;                       // domain cover, values never leave it
+        } else if ((uint64_t)S.T.back() - ((uint64_t)S.T.front() - 1) < (1ull << 32)) {
+            S.base = S.T.front() - 1;            // breakpoint-span cover, clamp into it
+            S.clamp = true;
+            S.clamp_lo = S.base;
+            S.clamp_hi = S.T.back();
+        } else {
+            S.mode = MODE_SEARCH;
+        }
+    }
+    // level-1 size target: 16 cells per breakpoint, 64..4096; halve the largest table while over budget
+    std::vector<uint32_t> s1(pl.slots.size(), 0);
+    auto span_of = [](const SlotPlan &S) -> uint64_t {
+        return S.clamp ? (uint64_t)S.clamp_hi - (uint64_t)S.clamp_lo : (uint64_t)S.dh - (uint64_t)S.dl;
+    };
+    for (size_t i = 0; i < pl.slots.size(); ++i) {
+        SlotPlan &S = pl.slots[i];
+        if (S.mode != MODE_LUT) continue;
+        uint64_t target = 64;
+        while (target < 4096 && target < 16ull * S.T.size()) target <<= 1;
+        const uint64_t span = span_of(S);
+        uint32_t sh = 0;
+        while (sh < 31 && (span >> sh) + 1 > target) ++sh;
+        s1[i] = sh;
+        build_lut(S, span, sh);
+    }
+    for (int iter = 0; iter < 256; ++iter) {
+        size_t tot = 0;
+        int worst = -1;
+        size_t worst_sz = 0;
+        for (size_t i = 0; i < pl.slots.size(); ++i) {
+            const SlotPlan &S = pl.slots[i];
+            if (S.mode != MODE_LUT) continue;
+            const size_t sz = 8 * (S.l1.size() + S.l2.size()) + 32;
+            tot += sz;
+            if (sz > worst_sz) { worst_sz = sz; worst = (int)i; }
+        }
+        if (tot <= lut_budget || worst < 0) break;
+        SlotPlan &S = pl.slots[worst];
+        // a coarser level 1 halves it; when level 2 dominates (dense breakpoints) coarsening
+        // does not help, so that column falls back to a binary search in global memory
+        if (s1[worst] >= 31 || S.l1.size() <= 64 || S.l2.size() > S.l1.size()) {
+            S.mode = MODE_SEARCH;
+            S.l1.clear();
+            S.l2.clear();
+            continue;
+        }
+        build_lut(S, span_of(S), ++s1[worst]);
+    }
+
+    // ---- layout: image [L1/L2 tables][group maps] | acc [hists][grids][direct] | hll
+    uint32_t u2 = 0;   // image cursor in uint2 units
+    for (auto &S : pl.slots) {
+        if (S.mode != MODE_LUT) continue;
+        S.lut_idx = u2;
+        u2 += (uint32_t)S.l1.size();
+        S.l2_idx = u2;
+        u2 += (uint32_t)S.l2.size();
+    }
+    uint32_t w = u2 * 2;   // u32 cursor
+    w = (w + 3) & ~3u;
+    for (auto &G : pl.groups) {
+        if (G.direct) continue;
+        G.mapA_idx = w;
+        w += pl.slots[G.a].nb;
+        G.mapB_idx = w;
+        w += pl.slots[G.b].nb;
+    }
+    w = (w + 3) & ~3u;
+    const uint32_t image_words = w;
+    pl.acc_idx = w;
+    for (auto &S : pl.slots) {
+        if (!S.has_preds) continue;
+        S.hist_idx = w;
+        w += S.nb;
+    }
+    for (auto &G : pl.groups) {
+        if (G.direct) continue;
+        G.grid_rel = w - pl.acc_idx;
+        w += G.na * G.nbb;
+    }
+    const uint32_t direct_idx = w;
+    w += (uint32_t)ndirect;
+    w = (w + 3) & ~3u;
+    pl.acc_words = w - pl.acc_idx;
+    pl.hll_off = w * 4;
+    uint32_t nh = 0;
+    for (auto &S : pl.slots) {
+        if (!S.has_hll) continue;
+        S.hll_off = pl.hll_off + nh * kHllM;
+        ++nh;
+    }
+    pl.hll_bytes = nh * kHllM;
+    pl.smem_bytes = (uint32_t)align16(pl.hll_off + pl.hll_bytes);
+    if (pl.smem_bytes > kSmemBudget)
+        return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
+
+    // ---- fill the image (absolute shared-memory indices)
+    pl.image.assign((size_t)image_words * 4, 0);
+    uint2 *img2 = reinterpret_cast<uint2 *>(pl.image.data());
+    uint32_t *img32 = reinterpret_cast<uint32_t *>(pl.image.data());
+    for (auto &S : pl.slots) {
+        if (S.mode != MODE_LUT) continue;
+        for (size_t k = 0; k < S.l1.size(); ++k) {
+            uint2 e = S.l1[k];
+            if (e.x & kL2Flag) e.y += S.l2_idx;
+            else e.x += S.hist_idx;
+            img2[S.lut_idx + k] = e;
+        }
+        for (size_t k = 0; k < S.l2.size(); ++k) {
+            uint2 e = S.l2[k];
+            e.x += S.hist_idx;
+            img2[S.l2_idx + k] = e;
+        }
+    }
+    for (auto &G : pl.groups) {
+        if (G.direct) continue;
+        const SlotPlan &A = pl.slots[G.a], &B = pl.slots[G.b];
+        for (uint32_t r = 0; r < A.nb; ++r) {
+            const uint32_t sub = r == 0 ? 0 : count_le(G.TA, A.T[r - 1]);
+            img32[G.mapA_idx + r] = pl.acc_idx + G.grid_rel + sub * G.nbb;
+        }
+        for (uint32_t r = 0; r < B.nb; ++r) img32[G.mapB_idx + r] = r == 0 ? 0 : count_le(G.TB, B.T[r - 1]);
+    }
+
+    // ---- finalize plan
+    uint32_t pre = 0;
+    for (auto &S : pl.slots) {
+        if (!S.has_preds) continue;
+        S.pre = pre;
+        pl.jobs.push_back(FinJob{JOB_HIST, S.hist_idx - pl.acc_idx, pre, 0, S.nb});
+        pre += S.nb + 1;
+    }
+    for (auto &G : pl.groups) {
+        if (G.direct) continue;
+        G.sat = pre;
+        pl.jobs.push_back(FinJob{JOB_SAT, G.grid_rel, pre, G.na, G.nbb});
+        pre += (G.na + 1) * (G.nbb + 1);
+    }
+    pl.pre_words = pre;
+    auto bucket_iv = [&](uint32_t p, const std::vector<int64_t> &T, uint32_t &lo, uint32_t &hi) {
+        if (pl.iv[p].empty) { lo = 1; hi = 0; return; }
+        lo = count_le(T, pl.iv[p].lo);
+        hi = count_le(T, pl.iv[p].hi);
+    };
+    pl.fpreds.resize(np);
+    for (uint32_t p = 0; p < np; ++p) {
+        const SlotPlan &S = pl.slots[pl.pslot[p]];
+        FinPred F{};
+        F.pre = S.pre;
+        bucket_iv(p, S.T, F.lo, F.hi);
+        F.neg = (preds[p].flags & GACE_PRED_NEGATE) ? 1 : 0;
+        pl.fpreds[p] = F;
+    }
+    uint32_t dcur = 0;
+    for (uint32_t q = 0; q < nq; ++q) {
+        const uint32_t i = pairs[q].i, j = pairs[q].j;
+        const int si = pl.pslot[i], sj = pl.pslot[j];
+        FinPair F{};
+        if (si == sj) {
+            F.kind = PAIR_SAME;
+            F.pre = pl.slots[si].pre;
+            bucket_iv(i, pl.slots[si].T, F.li, F.hi);
+            bucket_iv(j, pl.slots[sj].T, F.lj, F.hj);
+            F.negi = (preds[i].flags & GACE_PRED_NEGATE) ? 1 : 0;
+            F.negj = (preds[j].flags & GACE_PRED_NEGATE) ? 1 : 0;
+        } else {
+            const Group &G = pl.groups[pl.gidx[std::make_pair(std::min(si, sj), std::max(si, sj))]];
+            const uint32_t pa = (si == G.a) ? i : j, pb = (si == G.a) ? j : i;
+            const uint32_t na_ = (preds[pa].flags & GACE_PRED_NEGATE) ? 1 : 0;
+            const uint32_t nb_ = (preds[pb].flags & GACE_PRED_NEGATE) ? 1 : 0;
+            if (G.direct) {
+                DirectPair D{};
+                uint32_t lo, hi;
+                bucket_iv(pa, pl.slots[G.a].T, lo, hi);
+                D.la = lo + pl.slots[G.a].hist_idx;
+                D.ha = hi + pl.slots[G.a].hist_idx;
+                bucket_iv(pb, pl.slots[G.b].T, lo, hi);
+                D.lb = lo + pl.slots[G.b].hist_idx;
+                D.hb = hi + pl.slots[G.b].hist_idx;
+                D.sa = (uint8_t)G.a;
+                D.sb = (uint8_t)G.b;
+                D.nega = (uint8_t)na_;
+                D.negb = (uint8_t)nb_;
+                D.acc_idx = direct_idx + dcur;
+                pl.direct.push_back(D);
+                F.kind = PAIR_DIRECT;
+                F.pre = direct_idx + dcur - pl.acc_idx;
+                ++dcur;
+            } else {
+                F.kind = PAIR_GRID;
+                F.pre = G.sat;
+                F.na = G.na;
+                F.nb = G.nbb;
+                bucket_iv(pa, G.TA, F.li, F.hi);
+                bucket_iv(pb, G.TB, F.lj, F.hj);
+                F.negi = na_;
+                F.negj = nb_;
+            }
+        }
+        pl.fpairs[q] = F;
+    }
+
+    // ---- kernel parameters (pointers filled in at launch)
+    ProbeParams &P = pl.P;
+    memset(&P, 0, sizeof(P));
+    P.nslots = (uint32_t)pl.slots.size();
+    for (int i = 0; i < kMaxSlots * kMaxSlots; ++i) P.combo[i] = -1;
+    uint32_t bps = 0;
+    for (size_t i = 0; i < pl.slots.size(); ++i) {
+        SlotPlan &S = pl.slots[i];
+        SlotParams &Q = P.slot[i];
+        Q.dtype = (uint8_t)S.dtype;
+        Q.mode = S.has_preds ? S.mode : (uint8_t)MODE_NOPRED;
+        Q.has_hll = S.has_hll ? 1 : 0;
+        Q.hll_off = S.hll_off;
+        Q.hist_idx = S.hist_idx;
+        Q.base = S.base;
+        Q.s1 = S.s1;
+        Q.cell_mask = S.s1 >= 32 ? 0xFFFFFFFFu : (uint32_t)((1ull << S.s1) - 1);
+        Q.lut_idx = S.lut_idx;
+        Q.l2_idx = S.l2_idx;
+        if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
+        else { Q.clamp_lo = INT64_MIN; Q.clamp_hi = INT64_MAX; }
+        if (S.has_preds && S.mode == MODE_LUT && S.clamp) {
+            Q.clamp_lo = S.clamp_lo;
+            Q.clamp_hi = S.clamp_hi;
+            pl.clamp = true;
+        }
+        if (S.has_preds && S.mode == MODE_SEARCH) {
+            S.bps_off = bps;
+            Q.nbp = (uint32_t)S.T.size();
+            for (int64_t x : S.T) pl.bps.push_back(x);
+            bps += (uint32_t)S.T.size();
+        }
+    }
+    for (size_t g = 0; g < pl.groups.size(); ++g) {
+        const Group &G = pl.groups[g];
+        if (G.direct) continue;
+        P.grp[g].a = (uint8_t)G.a;
+        P.grp[g].b = (uint8_t)G.b;
+        P.grp[g].mapA_adj = (int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx;
+        P.grp[g].mapB_adj = (int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx;
+        P.combo[G.a * kMaxSlots + G.b] = (int8_t)g;
+    }
+    P.ndirect = (uint32_t)pl.direct.size();
+    P.image_u4 = image_words / 4;
+    P.acc_idx = pl.acc_idx;
+    P.acc_words = pl.acc_words;
+    P.hll_off = pl.hll_off;
+    P.hll_bytes = pl.hll_bytes;
+    P.smem_bytes = pl.smem_bytes;
+    return GACE_OK;
+}
+
+// ------------------------------------------------------------------ validation helpers
+
+int popcount64(uint64_t x) { return __builtin_popcountll(x); }
+
+gace_status check_table(const gace_table *t) {
+    if (!t || t->magic != kMagic) return fail(GACE_EHANDLE, "invalid or detached table handle");
+    return GACE_OK;
+}
+
+gace_status validate_batch(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
+                           uint32_t nq, double rate, uint64_t hll_mask, uint32_t hll_p) {
+    if (np > GACE_MAX_PREDS) return fail(GACE_EINVAL, "npreds > 4096");
+    if (nq > GACE_MAX_PAIRS) return fail(GACE_EINVAL, "npairs > 4096");
+    if (np && !preds) return fail(GACE_EINVAL, "preds is NULL");
+    if (nq && !pairs) return fail(GACE_EINVAL, "pairs is NULL");
+    if (!(rate >= 0.0 && rate <= 1.0)) return fail(GACE_EINVAL, "sample_rate must be in [0, 1]");
+    if (t->ncols < 64 && (hll_mask >> t->ncols)) return fail(GACE_EINVAL, "hll_col_mask names a column >= ncols");
+    for (uint32_t p = 0; p < np; ++p) {
+        if (preds[p].col >= t->ncols) return fail(GACE_EINVAL, "predicate column out of range");
+        if (preds[p].op > GACE_BETWEEN) return fail(GACE_EINVAL, "unknown predicate op");
+        if (preds[p].flags & ~GACE_PRED_NEGATE) return fail(GACE_EINVAL, "unknown predicate flags");
+    }
+    for (uint32_t q = 0; q < nq; ++q)
+        if (pairs[q].i >= np || pairs[q].j >= np) return fail(GACE_EINVAL, "pair index out of range");
+    if (hll_p != GACE_HLL_P) return fail(GACE_EUNSUPPORTED, "hll_p must be 12");
+    return GACE_OK;
+}
+
+uint64_t threshold_of(double rate) { return rate >= 1.0 ? ~0ull : (uint64_t)std::ldexp(rate, 64); }
+
+gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uint32_t ncols, uint64_t nrows,
+                          const gace_dist *dist, int device, void *stream, bool host, gace_table **out) {
+    if (!out) return fail(GACE_EINVAL, "out is NULL");
+    if (!ptrs || !dtypes) return fail(GACE_EINVAL, "column pointers / dtypes are NULL");
+    if (ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "ncols must be in [1, 64]");
+    for (uint32_t c = 0; c < ncols; ++c) {
+        if (dtypes[c] != GACE_I32 && dtypes[c] != GACE_I64) return fail(GACE_EINVAL, "unknown dtype");
+        if (!ptrs[c] && nrows) return fail(GACE_EINVAL, "NULL column pointer");
+        if (!host && ((uintptr_t)ptrs[c] & 15)) return fail(GACE_EINVAL, "column pointer not 16-byte aligned");
+    }
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+            return fail(GACE_EINVAL, "bad rank / nranks");
+        if (dist->nranks > 1 && !dist->nccl_unique_id && !dist->nccl_comm)
+            return fail(GACE_EINVAL, "multi-rank attach needs an NCCL unique id or comm");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(GACE_ECUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) return fail(GACE_EINVAL, "bad device ordinal");
+    CUDA_TRY(cudaSetDevice(device));
+    gace_table *t = new gace_table();
+    t->device = device;
+    t->host = host;
+    t->ncols = ncols;
+    t->nrows = nrows;
+    t->cols.assign(ptrs, ptrs + ncols);
+    for (uint32_t c = 0; c < ncols; ++c) t->dtypes.push_back((int)dtypes[c]);
+    cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
+    auto bail = [&](gace_status s) {
+        gace_table_detach(t);
+        return s;
+    };
+    if (stream) {
+        t->stream = (cudaStream_t)stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(GACE_ECUDA, "stream create failed"));
+        t->own_stream = true;
+    }
+    for (int i = 0; i < kNumEv; ++i)
+        if (cudaEventCreate(&t->ev[i]) != cudaSuccess) return bail(fail(GACE_ECUDA, "event create failed"));
+    // value domains
+    t->dlo.resize(ncols);
+    t->dhi.resize(ncols);
+    for (uint32_t c = 0; c < ncols; ++c) {
+        t->dlo[c] = dtypes[c] == GACE_I32 ? INT32_MIN : INT64_MIN;
+        t->dhi[c] = dtypes[c] == GACE_I32 ? INT32_MAX : INT64_MAX;
+    }
+    if (!host && nrows) {
+        DevBuf mm;
+        if (mm.ensure(16 * ncols) != cudaSuccess) return bail(fail(GACE_ENOMEM, "minmax scratch"));
+        std::vector<long long> init(2 * ncols);
+        for (uint32_t c = 0; c < ncols; ++c) { init[2 * c] = LLONG_MAX; init[2 * c + 1] = LLONG_MIN; }
+        cudaMemcpyAsync(mm.p, init.data(), 16 * ncols, cudaMemcpyHostToDevice, t->stream);
+        for (uint32_t c = 0; c < ncols; ++c) {
+            if (launch_minmax(ptrs[c], dtypes[c], nrows, mm.as<long long>(16 * c), t->sms, t->stream) != cudaSuccess) {
+                mm.release();
+                return bail(fail(GACE_ECUDA, "minmax launch failed"));
+            }
+            ++g_launches;
+        }
+        cudaMemcpyAsync(init.data(), mm.p, 16 * ncols, cudaMemcpyDeviceToHost, t->stream);
+        cudaError_t e = cudaStreamSynchronize(t->stream);
+        mm.release();
+        if (e != cudaSuccess) return bail(fail(GACE_ECUDA, std::string("attach scan: ") + cudaGetErrorString(e)));
+        for (uint32_t c = 0; c < ncols; ++c) { t->dlo[c] = init[2 * c]; t->dhi[c] = init[2 * c + 1]; }
+    }
+    if (host) {
+        if (cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(GACE_ECUDA, "copy stream create failed"));
+        for (int b = 0; b < 2; ++b) {
+            if (cudaEventCreateWithFlags(&t->ev_copied[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&t->ev_free[b], cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(GACE_ECUDA, "event create failed"));
+        }
+        if (cudaEventCreate(&t->ev_c0) != cudaSuccess || cudaEventCreate(&t->ev_c1) != cudaSuccess)
+            return bail(fail(GACE_ECUDA, "event create failed"));
+    }
+    if (dist) {
+        t->has_dist = true;
+        t->dist = *dist;
+        t->dist.nccl_unique_id = nullptr;
+        if (dist->nranks > 1) {
+            if (dist->nccl_comm) {
+                t->comm = dist->nccl_comm;
+            } else {
+                Nccl *n = nccl();
+                if (!n) return bail(fail(GACE_ENCCL, "libnccl.so.2 not loadable"));
+                NcclUid id;
+                memcpy(&id, dist->nccl_unique_id, sizeof(id));
+                int r = n->CommInitRank(&t->comm, dist->nranks, id, dist->rank);
+                if (r != 0) return bail(fail(GACE_ENCCL, std::string("ncclCommInitRank: ") + (n->GetErrorString ? n->GetErrorString(r) : "")));
+                t->own_comm = true;
+            }
+        }
+    }
+    *out = t;
+    return GACE_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+
+extern "C" {
+
+const char *gace_last_error(void) { return g_err.c_str(); }
+
+uint64_t gace_kernel_launches(void) { return g_launches.load(); }
+
+gace_status gace_nccl_unique_id(void *id128) {
+    if (!id128) return fail(GACE_EINVAL, "id is NULL");
+    Nccl *n = nccl();
+    if (!n) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
+    NcclUid id;
+    int r = n->GetUniqueId(&id);
+    if (r != 0) return fail(GACE_ENCCL, "ncclGetUniqueId failed");
+    memcpy(id128, &id, sizeof(id));
+    return GACE_OK;
+}
+
+gace_status gace_table_attach(const void *const *col_dev_ptrs, const gace_dtype *dtypes, uint32_t ncols,
+                              uint64_t nrows_local, const gace_dist *dist, int device, void *cuda_stream,
+                              gace_table **out) {
+    return attach_common(col_dev_ptrs, dtypes, ncols, nrows_local, dist, device, cuda_stream, false, out);
+}
+
+gace_status gace_table_attach_host(const void *const *col_host_ptrs, const gace_dtype *dtypes, uint32_t ncols,
+                                   uint64_t nrows_local, const gace_dist *dist, int device, void *cuda_stream,
+                                   gace_table **out) {
+    return attach_common(col_host_ptrs, dtypes, ncols, nrows_local, dist, device, cuda_stream, true, out);
+}
+
+gace_status gace_table_detach(gace_table *t) {
+    if (!t || t->magic != kMagic) return fail(GACE_EHANDLE, "invalid or detached table handle");
+    cudaSetDevice(t->device);
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    if (t->copy_stream) cudaStreamSynchronize(t->copy_stream);
+    if (t->own_comm && t->comm) {
+        Nccl *n = nccl();
+        if (n) n->CommDestroy(t->comm);
+    }
+    for (auto &e : t->ev) if (e) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b) {
+        if (t->ev_copied[b]) cudaEventDestroy(t->ev_copied[b]);
+        if (t->ev_free[b]) cudaEventDestroy(t->ev_free[b]);
+        t->d_stage[b].release();
+    }
+    if (t->ev_c0) cudaEventDestroy(t->ev_c0);
+    if (t->ev_c1) cudaEventDestroy(t->ev_c1);
+    t->d_plan.release(); t->d_acc.release(); t->d_pre.release(); t->d_part.release();
+    t->d_out.release(); t->d_nsamp.release(); t->d_mask.release();
+    t->h_plan.release(); t->h_out.release();
+    if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
+    if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
+    t->magic = 0;
+    delete t;
+    return GACE_OK;
+}
+
+gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, const gace_pair *pairs,
+                       uint32_t npairs, double sample_rate, uint64_t seed, uint64_t hll_col_mask, uint32_t hll_p,
+                       uint64_t *n_sampled, uint64_t *counts, uint64_t *joint_counts, uint8_t *hll_regs) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(t->mu);
+    st = validate_batch(t, preds, npreds, pairs, npairs, sample_rate, hll_col_mask, hll_p);
+    if (st) return st;
+    const int nh = popcount64(hll_col_mask);
+    if (!n_sampled) return fail(GACE_EINVAL, "n_sampled is NULL");
+    if (npreds && !counts) return fail(GACE_EINVAL, "counts is NULL");
+    if (npairs && !joint_counts) return fail(GACE_EINVAL, "joint_counts is NULL");
+    if (nh && !hll_regs) return fail(GACE_EINVAL, "hll_regs is NULL");
+
+    Plan pl;
+    st = make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, pl);
+    if (st) return st;
+    CUDA_TRY(cudaSetDevice(t->device));
+
+    // ---- one pinned blob -> one H2D copy: image | direct | jobs | fpreds | fpairs | bps
+    size_t off = 0;
+    const size_t o_img = off; off = align16(off + pl.image.size());
+    const size_t o_dir = off; off = align16(off + pl.direct.size() * sizeof(DirectPair));
+    const size_t o_job = off; off = align16(off + pl.jobs.size() * sizeof(FinJob));
+    const size_t o_fp = off; off = align16(off + pl.fpreds.size() * sizeof(FinPred));
+    const size_t o_fq = off; off = align16(off + pl.fpairs.size() * sizeof(FinPair));
+    const size_t o_bps = off; off = align16(off + pl.bps.size() * sizeof(int64_t));
+    const size_t blob = std::max<size_t>(off, 16);
+    CUDA_TRY(cudaStreamSynchronize(t->stream));   // previous call fully done with the staging buffers
+    if (t->h_plan.ensure(blob) != cudaSuccess || t->d_plan.ensure(blob) != cudaSuccess)
+        return fail(GACE_ENOMEM, "plan buffers");
+    char *hb = t->h_plan.as<char>();
+    memcpy(hb + o_img, pl.image.data(), pl.image.size());
+    if (!pl.direct.empty()) memcpy(hb + o_dir, pl.direct.data(), pl.direct.size() * sizeof(DirectPair));
+    if (!pl.jobs.empty()) memcpy(hb + o_job, pl.jobs.data(), pl.jobs.size() * sizeof(FinJob));
+    if (!pl.fpreds.empty()) memcpy(hb + o_fp, pl.fpreds.data(), pl.fpreds.size() * sizeof(FinPred));
+    if (!pl.fpairs.empty()) memcpy(hb + o_fq, pl.fpairs.data(), pl.fpairs.size() * sizeof(FinPair));
+    if (!pl.bps.empty()) memcpy(hb + o_bps, pl.bps.data(), pl.bps.size() * sizeof(int64_t));
+
+    const int grid = t->sms;
+    const size_t acc_bytes = std::max<size_t>(8ull * pl.acc_words, 8);
+    const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
+    const size_t out_words = 1 + npreds + npairs;
+    const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
+    if (t->d_acc.ensure(acc_bytes) != cudaSuccess || t->d_pre.ensure(std::max<size_t>(8ull * pl.pre_words, 8)) != cudaSuccess ||
+        t->d_part.ensure(part_bytes) != cudaSuccess || t->d_out.ensure(out_bytes) != cudaSuccess ||
+        t->d_nsamp.ensure(8) != cudaSuccess || t->h_out.ensure(out_bytes) != cudaSuccess)
+        return fail(GACE_ENOMEM, "probe scratch");
+
+    cudaStream_t s = t->stream;
+    CUDA_TRY(cudaEventRecord(t->ev[0], s));
+    CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, blob, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(t->d_acc.p, 0, acc_bytes, s));
+    CUDA_TRY(cudaMemsetAsync(t->d_nsamp.p, 0, 8, s));
+    CUDA_TRY(cudaEventRecord(t->ev[1], s));
+
+    ProbeParams P = pl.P;
+    P.image = t->d_plan.as<const uint4>(o_img);
+    P.direct = t->d_plan.as<const DirectPair>(o_dir);
+    for (size_t i = 0; i < pl.slots.size(); ++i)
+        if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
+    P.g_acc = t->d_acc.as<unsigned long long>();
+    P.g_hll_part = t->d_part.as<uint8_t>();
+    P.g_nsamp = t->d_nsamp.as<unsigned long long>();
+    P.thr = threshold_of(sample_rate);
+    P.seed = seed;
+    P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
+    const bool sample = sample_rate < 1.0;
+    const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
+    uint64_t bytes_per_row = 0;
+    for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
+
+    // rows per launch: keep every CTA's u32 bins below 2^31
+    const uint64_t max_rows = (uint64_t)grid * kThreads * (1ull << 19);
+    uint64_t launches = 0;
+    double h2d_ms = 0;
+    if (t->nrows == 0) {
+        CUDA_TRY(cudaMemsetAsync(t->d_part.p, 0, part_bytes, s));
+    } else if (!t->host) {
+        for (uint64_t r0 = 0; r0 < t->nrows; r0 += max_rows) {
+            const uint64_t n = std::min(max_rows, t->nrows - r0);
+            for (size_t i = 0; i < pl.slots.size(); ++i) {
+                const size_t w = pl.slots[i].dtype == GACE_I32 ? 4 : 8;
+                P.slot[i].ptr = static_cast<const char *>(t->cols[pl.slots[i].col]) + r0 * w;
+            }
+            P.nrows = n;
+            P.row0 = row_offset + r0;
+            P.part_merge = launches ? 1u : 0u;
+            CUDA_TRY(launch_probe(P, pl.clamp, sample, grid, s));
+            ++launches;
+        }
+    } else {
+        // host table: double-buffered H2D of the probed columns, overlapped with the scan
+        const uint64_t chunk = std::min<uint64_t>((t->nrows + 3) & ~3ull, 1ull << 24);
+        const size_t stage_bytes = align16(chunk * bytes_per_row) + 16 * pl.slots.size();
+        if (t->d_stage[0].ensure(stage_bytes) != cudaSuccess || t->d_stage[1].ensure(stage_bytes) != cudaSuccess)
+            return fail(GACE_ENOMEM, "host-table staging");
+        CUDA_TRY(cudaEventRecord(t->ev_free[0], s));
+        CUDA_TRY(cudaEventRecord(t->ev_free[1], s));
+        CUDA_TRY(cudaStreamWaitEvent(t->copy_stream, t->ev[1], 0));
+        CUDA_TRY(cudaEventRecord(t->ev_c0, t->copy_stream));
+        uint64_t k = 0;
+        for (uint64_t r0 = 0; r0 < t->nrows; r0 += chunk, ++k) {
+            const int b = (int)(k & 1);
+            const uint64_t n = std::min(chunk, t->nrows - r0);
+            CUDA_TRY(cudaStreamWaitEvent(t->copy_stream, t->ev_free[b], 0));
+            size_t so = 0;
+            for (size_t i = 0; i < pl.slots.size(); ++i) {
+                const size_t w = pl.slots[i].dtype == GACE_I32 ? 4 : 8;
+                char *dst = t->d_stage[b].as<char>(so);
+                CUDA_TRY(cudaMemcpyAsync(dst, static_cast<const char *>(t->cols[pl.slots[i].col]) + r0 * w, n * w,
+                                         cudaMemcpyHostToDevice, t->copy_stream));
+                P.slot[i].ptr = dst;
+                so = align16(so + chunk * w);
+            }
+            CUDA_TRY(cudaEventRecord(t->ev_copied[b], t->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(s, t->ev_copied[b], 0));
+            P.nrows = n;
+            P.row0 = row_offset + r0;
+            P.part_merge = launches ? 1u : 0u;
+            CUDA_TRY(launch_probe(P, pl.clamp, sample, grid, s));
+            ++launches;
+            CUDA_TRY(cudaEventRecord(t->ev_free[b], s));
+        }
+        CUDA_TRY(cudaEventRecord(t->ev_c1, t->copy_stream));
+    }
+    g_launches += launches;
+    CUDA_TRY(cudaEventRecord(t->ev[2], s));
+
+    FinParams F{};
+    F.jobs = t->d_plan.as<const FinJob>(o_job);
+    F.njobs = (uint32_t)pl.jobs.size();
+    F.hll_bytes = pl.hll_bytes;
+    F.nparts = (t->nrows == 0) ? 1 : (uint32_t)grid;
+    F.hll_blocks = pl.hll_bytes ? std::min<uint32_t>(std::max<uint32_t>(pl.hll_bytes / 4096, 1) * 4, 64) : 0;
+    F.g_acc = t->d_acc.as<const unsigned long long>();
+    F.g_pre = t->d_pre.as<unsigned long long>();
+    F.g_hll_part = t->d_part.as<const uint8_t>();
+    F.g_nsamp = t->d_nsamp.as<const unsigned long long>();
+    F.preds = t->d_plan.as<const FinPred>(o_fp);
+    F.npreds = npreds;
+    F.pairs = t->d_plan.as<const FinPair>(o_fq);
+    F.npairs = npairs;
+    F.out = t->d_out.as<unsigned long long>();
+    F.out_regs = t->d_out.as<uint8_t>(align16(8 * out_words));
+    CUDA_TRY(launch_finalize(F, s));
+    g_launches += (F.njobs + F.hll_blocks ? 2 : 1);
+    CUDA_TRY(cudaEventRecord(t->ev[3], s));
+
+    if (t->has_dist && t->dist.nranks > 1) {
+        Nccl *n = nccl();
+        if (!n) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
+        n->GroupStart();
+        int r1 = n->AllReduce(F.out, F.out, out_words, kNcclUint64, kNcclSum, t->comm, s);
+        int r2 = pl.hll_bytes ? n->AllReduce(F.out_regs, F.out_regs, pl.hll_bytes, kNcclUint8, kNcclMax, t->comm, s) : 0;
+        int r3 = n->GroupEnd();
+        if (r1 || r2 || r3) return fail(GACE_ENCCL, "ncclAllReduce failed");
+    }
+    CUDA_TRY(cudaEventRecord(t->ev[4], s));
+    CUDA_TRY(cudaMemcpyAsync(t->h_out.p, t->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(t->ev[5], s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+
+    const uint64_t *ho = t->h_out.as<uint64_t>();
+    *n_sampled = ho[0];
+    if (npreds) memcpy(counts, ho + 1, 8ull * npreds);
+    if (npairs) memcpy(joint_counts, ho + 1 + npreds, 8ull * npairs);
+    if (nh) memcpy(hll_regs, t->h_out.as<uint8_t>(align16(8 * out_words)), pl.hll_bytes);
+
+    gace_timing &T = t->last;
+    float ms;
+    cudaEventElapsedTime(&ms, t->ev[0], t->ev[1]); T.plan_upload_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[1], t->ev[2]); T.scan_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[2], t->ev[3]); T.finalize_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[3], t->ev[4]); T.merge_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[4], t->ev[5]); T.d2h_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[0], t->ev[5]); T.total_ms = ms;
+    if (t->host && t->nrows) {
+        cudaEventElapsedTime(&ms, t->ev_c0, t->ev_c1);
+        h2d_ms = ms;
+    }
+    T.h2d_ms = h2d_ms;
+    T.scan_launches = launches;
+    T.bytes_scanned = t->nrows * bytes_per_row;
+    return GACE_OK;
+}
+
+gace_status gace_sample_mask(gace_table *t, double sample_rate, uint64_t seed, uint64_t *bits) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(t->mu);
+    if (!(sample_rate >= 0.0 && sample_rate <= 1.0)) return fail(GACE_EINVAL, "sample_rate must be in [0, 1]");
+    if (!bits && t->nrows) return fail(GACE_EINVAL, "bits is NULL");
+    const uint64_t words = (t->nrows + 63) / 64;
+    if (!words) return GACE_OK;
+    CUDA_TRY(cudaSetDevice(t->device));
+    if (t->d_mask.ensure(8 * words) != cudaSuccess) return fail(GACE_ENOMEM, "mask buffer");
+    const uint64_t row0 = t->has_dist ? t->dist.row_offset : 0;
+    CUDA_TRY(launch_sample_mask(t->nrows, row0, seed, threshold_of(sample_rate), sample_rate >= 1.0,
+                                t->d_mask.as<unsigned long long>(), t->stream));
+    ++g_launches;
+    CUDA_TRY(cudaMemcpyAsync(bits, t->d_mask.p, 8 * words, cudaMemcpyDeviceToHost, t->stream));
+    CUDA_TRY(cudaStreamSynchronize(t->stream));
+    return GACE_OK;
+}
+
+gace_status gace_last_timing(const gace_table *t, gace_timing *out) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    if (!out) return fail(GACE_EINVAL, "out is NULL");
+    *out = t->last;
+    return GACE_OK;
+}
+
+// ---------------------------------------------------------------- derive / gate (host doubles)
+
+static double hll_estimate(const uint8_t *R, uint32_t m) {
+    double z = 0.0;
+    uint32_t v = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+        z += std::ldexp(1.0, -(int)R[j]);
+        v += R[j] == 0;
+    }
+    const double md = (double)m;
+    const double alpha = 0.7213 / (1.0 + 1.079 / md);
+    const double e = alpha * md * md / z;
+    if (e <= 2.5 * md && v > 0) return md * std::log(md / (double)v);
+    return e;
+}
+
+gace_status gace_derive(uint64_t n, const uint64_t *counts, uint32_t npreds, const gace_pair *pairs,
+                        const uint64_t *joints, uint32_t npairs, const uint8_t *regs, uint32_t ncols_hll,
+                        uint32_t hll_p, const double *ndv_hist, double *sel, double *pcs, double *ndv_est,
+                        double *drift) {
+    if ((npreds && !counts && (sel || pcs)) || (npairs && (!pairs || !joints) && pcs))
+        return fail(GACE_EINVAL, "NULL input array");
+    if (ncols_hll && !regs && (ndv_est || drift)) return fail(GACE_EINVAL, "regs is NULL");
+    if (drift && ncols_hll && !ndv_hist) return fail(GACE_EINVAL, "ndv_hist is NULL");
+    if (ncols_hll && (ndv_est || drift) && hll_p != GACE_HLL_P) return fail(GACE_EUNSUPPORTED, "hll_p must be 12");
+    if (pcs)
+        for (uint32_t q = 0; q < npairs; ++q)
+            if (pairs[q].i >= npreds || pairs[q].j >= npreds) return fail(GACE_EINVAL, "pair index out of range");
+    if (drift)
+        for (uint32_t c = 0; c < ncols_hll; ++c)
+            if (!(ndv_hist[c] > 0)) return fail(GACE_EINVAL, "ndv_hist must be > 0");
+    const double nan = std::nan("");
+    const double fn = (double)n;
+    if (sel)
+        for (uint32_t p = 0; p < npreds; ++p) sel[p] = n ? (double)counts[p] / fn : nan;
+    if (pcs)
+        for (uint32_t q = 0; q < npairs; ++q) {
+            const uint64_t a = counts[pairs[q].i], b = counts[pairs[q].j];
+            if (!n || !a || !b) { pcs[q] = nan; continue; }
+            const double pa = (double)a / fn, pb = (double)b / fn, pj = (double)joints[q] / fn;
+            pcs[q] = pj / (pa * pb);
+        }
+    for (uint32_t c = 0; c < ncols_hll && (ndv_est || drift); ++c) {
+        const double e = hll_estimate(regs + (size_t)c * kHllM, kHllM);
+        if (ndv_est) ndv_est[c] = e;
+        if (drift) drift[c] = std::fabs(ndv_hist[c] - e) / ndv_hist[c];
+    }
+    return GACE_OK;
+}
+
+gace_status gace_gate(const double *drift, uint32_t nd, const double *s_est, const double *s_probe, uint32_t ns,
+                      const double *pcs, uint32_t np, const gace_thresholds *th, uint32_t *fired_mask,
+                      uint8_t *per_signal_fired) {
+    if (!fired_mask) return fail(GACE_EINVAL, "fired_mask is NULL");
+    if ((nd && !drift) || (ns && (!s_est || !s_probe)) || (np && !pcs)) return fail(GACE_EINVAL, "NULL signal array");
+    const gace_thresholds def = {0.25, 0.01, 1.6, 0.7};
+    const gace_thresholds &T = th ? *th : def;
+    uint32_t mask = 0, k = 0;
+    for (uint32_t i = 0; i < nd; ++i, ++k) {
+        const bool f = drift[i] >= T.d_threshold;                            // NaN: false
+        if (f) mask |= GACE_SIG_DRIFT;
+        if (per_signal_fired) per_signal_fired[k] = f;
+    }
+    for (uint32_t i = 0; i < ns; ++i, ++k) {
+        const bool f = std::fabs(s_est[i] - s_probe[i]) > T.sel_err_threshold;
+        if (f) mask |= GACE_SIG_SEL_ERROR;
+        if (per_signal_fired) per_signal_fired[k] = f;
+    }
+    for (uint32_t i = 0; i < np; ++i, ++k) {
+        const bool f = pcs[i] > T.pcs_high || pcs[i] < T.pcs_low;
+        if (f) mask |= GACE_SIG_CORRELATION;
+        if (per_signal_fired) per_signal_fired[k] = f;
+    }
+    *fired_mask = mask;
+    return GACE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,517 @@
+// gace_kernels.cu -- sm_100a kernels of the GACE selectivity probe.
+//
+// Hot path: probe_kernel streams every probed key
+// column once from HBM with 128-bit non-allocating loads, draws the Bernoulli
+// sample bit from a counter-based SplitMix64 of the global row id, resolves each
+// value's bucket with a shared-memory lookup table, and accumulates
+//   * a per-column u32 bucket histogram   (-> counts by prefix differences),
+//   * a per-column-pair 2-D sub-bucket grid (-> joint counts by rectangle sums),
+//   * u8 HyperLogLog registers            (fmix32 / mix64 hash, read-check-CAS max),
+// all in shared memory.  One CTA per SM, grid-stride over row quads.  At the
+// end each CTA adds its nonzero bins into global u64 accumulators and writes
+// its HLL registers as a per-CTA partial.  fin_prefix / fin_output turn the
+// accumulators into the packed result [n_sampled, counts, joints] + registers.
+// No tensor cores: this is an HBM-bound integer scan.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gace_kernels.h"
+#include "gace_plan.h"
+
+namespace gace {
+
+#define GACE_GAMMA 0x9E3779B97F4A7C15ULL
+
+// SplitMix64 finaliser (sample bit; int64 HLL hash).  DESIGN.md "Semantics" 1, 6.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// MurmurHash3 fmix32 (int32 HLL hash).  DESIGN.md "Semantics" 6.
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6BU;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35U;
+    h ^= h >> 16;
+    return h;
+}
+
+__device__ __forceinline__ int4 ld_stream(const void *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+extern __shared__ uint4 g_smem[];
+
+// Raise register byte idx to r (registers only grow; updates are rare after warm-up).
+__device__ __forceinline__ void hll_raise(uint8_t *R, uint32_t idx, uint32_t r) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(R + (idx & ~3u));
+    const uint32_t sh = (idx & 3u) * 8u;
+    uint32_t old = *reinterpret_cast<volatile uint32_t *>(w);
+    while (true) {
+        if (((old >> sh) & 0xFFu) >= r) return;
+        const uint32_t nw = (old & ~(0xFFu << sh)) | (r << sh);
+        const uint32_t prev = atomicCAS(w, old, nw);
+        if (prev == old) return;
+        old = prev;
+    }
+}
+
+__device__ __forceinline__ void hll_i32(const SlotParams &S, int32_t x) {
+    uint8_t *R = reinterpret_cast<uint8_t *>(g_smem) + S.hll_off;
+    const uint32_t h = fmix32(static_cast<uint32_t>(x));
+    const uint32_t idx = h >> (32 - kHllP);
+    const uint32_t r = __clz((h << kHllP) | (1u << (kHllP - 1))) + 1;   // <= 32-p+1
+    if (r > R[idx]) hll_raise(R, idx, r);
+}
+
+__device__ __forceinline__ void hll_i64(const SlotParams &S, int64_t x) {
+    uint8_t *R = reinterpret_cast<uint8_t *>(g_smem) + S.hll_off;
+    const uint64_t h = mix64(static_cast<uint64_t>(x) + GACE_GAMMA);
+    const uint32_t idx = static_cast<uint32_t>(h >> (64 - kHllP));
+    const uint32_t r = __clzll((h << kHllP) | (1ull << (kHllP - 1))) + 1;  // <= 64-p+1
+    if (r > R[idx]) hll_raise(R, idx, r);
+}
+
+// #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback).
+__device__ __forceinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, int64_t v) {
+    uint32_t lo = 0;
+    while (n > 0) {
+        const uint32_t half = n >> 1;
+        const bool right = __ldg(bps + lo + half) <= v;
+        lo = right ? lo + half + 1 : lo;
+        n = right ? n - half - 1 : half;
+    }
+    return lo;
+}
+
+// Absolute shared-memory index of the histogram bucket of offset u.
+__device__ __forceinline__ uint32_t lut_bucket(const SlotParams &S, uint32_t u) {
+    const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
+    uint2 e = T[S.lut_idx + (u >> S.s1)];
+    if (e.x & kL2Flag) e = T[e.y + ((u & S.cell_mask) >> ((e.x >> 24) & 31u))];
+    return (e.x & kBaseMask) + (u > e.y ? 1u : 0u);
+}
+
+template <bool CLAMP>
+__device__ __forceinline__ uint32_t bucket_i32(const SlotParams &S, int32_t x) {
+    if (S.mode == MODE_SEARCH) return S.hist_idx + search_bucket(S.bps, S.nbp, x);
+    if (CLAMP) x = min(max(x, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
+    return lut_bucket(S, static_cast<uint32_t>(x) - static_cast<uint32_t>(S.base));
+}
+
+template <bool CLAMP>
+__device__ __forceinline__ uint32_t bucket_i64(const SlotParams &S, int64_t x) {
+    if (S.mode == MODE_SEARCH) return S.hist_idx + search_bucket(S.bps, S.nbp, x);
+    if (CLAMP) x = min(max(x, S.clamp_lo), S.clamp_hi);
+    return lut_bucket(S, static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base)));
+}
+
+// One column slot over one row quad: load, bucket, HLL, histogram.
+// FULL: all four rows valid and kept.  Otherwise `keep` has one bit per row and
+// rows past the end (k >= nvalid) are never loaded.
+template <bool CLAMP, bool FULL>
+__device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint32_t nvalid,
+                                          uint32_t keep, uint32_t (&bk)[4]) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    if (S.dtype == 0) {
+        int32_t v[4];
+        const int32_t *p = static_cast<const int32_t *>(S.ptr) + q * 4;
+        if (FULL || nvalid == 4) {
+            const int4 t = ld_stream(p);
+            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = (k < (int)nvalid) ? __ldg(p + k) : 0;
+        }
+        if (S.mode != MODE_NOPRED) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk[k] = bucket_i32<CLAMP>(S, v[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[k], 1u);
+        }
+        if (S.has_hll) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (FULL || ((keep >> k) & 1u)) hll_i32(S, v[k]);
+        }
+    } else {
+        int64_t v[4];
+        const int64_t *p = static_cast<const int64_t *>(S.ptr) + q * 4;
+        if (FULL || nvalid == 4) {
+            const int4 t0 = ld_stream(p);
+            const int4 t1 = ld_stream(p + 2);
+            v[0] = (static_cast<int64_t>(t0.y) << 32) | static_cast<uint32_t>(t0.x);
+            v[1] = (static_cast<int64_t>(t0.w) << 32) | static_cast<uint32_t>(t0.z);
+            v[2] = (static_cast<int64_t>(t1.y) << 32) | static_cast<uint32_t>(t1.x);
+            v[3] = (static_cast<int64_t>(t1.w) << 32) | static_cast<uint32_t>(t1.z);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = (k < (int)nvalid) ? __ldg(reinterpret_cast<const long long *>(p) + k) : 0;
+        }
+        if (S.mode != MODE_NOPRED) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk[k] = bucket_i64<CLAMP>(S, v[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[k], 1u);
+        }
+        if (S.has_hll) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (FULL || ((keep >> k) & 1u)) hll_i64(S, v[k]);
+        }
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&bk)[NC][4], uint32_t s, int k) {
+    uint32_t r = bk[0][k];
+#pragma unroll
+    for (int c = 1; c < NC; ++c) r = (s == (uint32_t)c) ? bk[c][k] : r;
+    return r;
+}
+
+template <int NC, bool CLAMP, bool FULL>
+__device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint32_t nvalid, uint32_t keep) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    uint32_t bk[NC][4];
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (s < (int)P.nslots) slot_quad<CLAMP, FULL>(P.slot[s], q, nvalid, keep, bk[s]);
+    }
+    // joint counts: one 2-D grid bin per row and column pair (a, b)
+#pragma unroll
+    for (int a = 0; a < NC; ++a) {
+#pragma unroll
+        for (int b = a + 1; b < NC; ++b) {
+            const int g = P.combo[a * kMaxSlots + b];
+            if (g >= 0) {
+                const int ma = P.grp[g].mapA_adj;
+                const int mb = P.grp[g].mapB_adj;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (FULL || ((keep >> k) & 1u)) {
+                        const uint32_t ia = sm32[ma + (int)bk[a][k]];
+                        const uint32_t ib = sm32[mb + (int)bk[b][k]];
+                        atomicAdd(sm32 + ia + ib, 1u);
+                    }
+                }
+            }
+        }
+    }
+    // fallback: cross-column pairs whose grid did not fit, evaluated per row
+    for (uint32_t d = 0; d < P.ndirect; ++d) {
+        const DirectPair D = P.direct[d];
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ba = pick<NC>(bk, D.sa, k);
+            const uint32_t bb = pick<NC>(bk, D.sb, k);
+            const uint32_t ina = ((ba >= D.la) & (ba <= D.ha)) ^ D.nega;
+            const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
+            c += ((keep >> k) & 1u) & ina & inb;
+        }
+        const uint32_t m = __activemask();
+        const uint32_t tot = __reduce_add_sync(m, c);
+        if ((threadIdx.x & 31) == (uint32_t)(__ffs(m) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
+    }
+}
+
+template <int NC, bool CLAMP, bool SAMPLE>
+__global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constant__ ProbeParams P) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    // tables -> shared memory; accumulators and registers -> 0
+    for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) g_smem[i] = __ldg(P.image + i);
+    for (uint32_t i = P.image_u4 + threadIdx.x; i < P.smem_bytes / 16; i += blockDim.x)
+        g_smem[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+
+    const uint64_t nq = (P.nrows + 3) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t kept = 0;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+        const uint64_t rem = P.nrows - q * 4;
+        const uint32_t nvalid = rem >= 4 ? 4u : (uint32_t)rem;
+        uint32_t keep = (1u << nvalid) - 1u;
+        if (SAMPLE) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t g = P.row0 + q * 4 + k;
+                m |= (mix64(P.seed + (g + 1) * GACE_GAMMA) < P.thr ? 1u : 0u) << k;
+            }
+            keep &= m;
+            if (keep == 0) continue;
+        }
+        kept += __popc(keep);
+        if (keep == 0xFu) row_quad<NC, CLAMP, true>(P, q, 4, keep);
+        else row_quad<NC, CLAMP, false>(P, q, nvalid, keep);
+    }
+    __syncthreads();
+
+    // CTA partials -> global
+    for (uint32_t i = threadIdx.x; i < P.acc_words; i += blockDim.x) {
+        const uint32_t v = sm32[P.acc_idx + i];
+        if (v) atomicAdd(P.g_acc + i, (unsigned long long)v);
+    }
+    if (P.hll_bytes) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(g_smem) + P.hll_off);
+        uint4 *dst = reinterpret_cast<uint4 *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes);
+        for (uint32_t i = threadIdx.x; i < P.hll_bytes / 16; i += blockDim.x) {
+            uint4 v = src[i];
+            if (P.part_merge) {      // later launch of a chunked probe: max-merge into the partial
+                const uint4 o = dst[i];
+                v.x = __vmaxu4(v.x, o.x); v.y = __vmaxu4(v.y, o.y);
+                v.z = __vmaxu4(v.z, o.z); v.w = __vmaxu4(v.w, o.w);
+            }
+            dst[i] = v;
+        }
+    }
+    kept = __reduce_add_sync(0xFFFFFFFFu, kept);
+    if ((threadIdx.x & 31) == 0 && kept) atomicAdd(P.g_nsamp, (unsigned long long)kept);
+}
+
+// ------------------------------------------------------------------ finalize
+
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
+                                                                   unsigned long long *total) {
+    __shared__ unsigned long long warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) / 32;
+        unsigned long long s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) warp_sums[lane] = s;     // inclusive
+    }
+    __syncthreads();
+    const unsigned long long before = (wid ? warp_sums[wid - 1] : 0) + x - v;
+    *total = warp_sums[(blockDim.x + 31) / 32 - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
+    if (blockIdx.x < F.njobs) {
+        const FinJob J = F.jobs[blockIdx.x];
+        const unsigned long long *src = F.g_acc + J.src;
+        unsigned long long *dst = F.g_pre + J.dst;
+        if (J.kind == JOB_HIST) {
+            const uint32_t n = J.nb;
+            const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+            const uint32_t beg = min(n, threadIdx.x * per), end = min(n, beg + per);
+            unsigned long long s = 0;
+            for (uint32_t i = beg; i < end; ++i) s += src[i];
+            unsigned long long total;
+            unsigned long long run = block_exclusive_scan(s, &total);
+            for (uint32_t i = beg; i < end; ++i) {
+                dst[i] = run;
+                run += src[i];
+            }
+            if (threadIdx.x == 0) dst[n] = total;
+        } else {   // JOB_SAT: summed-area table with a zero border, row stride nb + 1
+            const uint32_t na = J.na, nb = J.nb, st = nb + 1;
+            for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) dst[j] = 0;
+            for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
+                unsigned long long run = 0;
+                dst[(size_t)(i + 1) * st] = 0;
+                for (uint32_t j = 0; j < nb; ++j) {
+                    run += src[(size_t)i * nb + j];
+                    dst[(size_t)(i + 1) * st + j + 1] = run;
+                }
+            }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < nb; j += blockDim.x) {
+                unsigned long long run = 0;
+                for (uint32_t i = 0; i < na; ++i) {
+                    run += dst[(size_t)(i + 1) * st + j + 1];
+                    dst[(size_t)(i + 1) * st + j + 1] = run;
+                }
+            }
+        }
+    } else {   // HLL: byte-wise max over the per-CTA partials
+        const uint32_t words = F.hll_bytes / 4;
+        const uint32_t b = blockIdx.x - F.njobs;
+        const uint32_t per = (words + F.hll_blocks - 1) / F.hll_blocks;
+        const uint32_t beg = b * per, end = min(words, beg + per);
+        const uint32_t *part = reinterpret_cast<const uint32_t *>(F.g_hll_part);
+        for (uint32_t w = beg + threadIdx.x; w < end; w += blockDim.x) {
+            uint32_t m = 0;
+            for (uint32_t c = 0; c < F.nparts; ++c) m = __vmaxu4(m, part[(size_t)c * words + w]);
+            reinterpret_cast<uint32_t *>(F.out_regs)[w] = m;
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long iv(const unsigned long long *pre, uint32_t lo, uint32_t hi) {
+    return lo <= hi ? pre[hi + 1] - pre[lo] : 0ull;
+}
+
+__device__ __forceinline__ unsigned long long rect(const unsigned long long *S, uint32_t st, uint32_t r0,
+                                                   uint32_t r1, uint32_t c0, uint32_t c1) {
+    if (r0 > r1 || c0 > c1) return 0ull;
+    return S[(size_t)(r1 + 1) * st + c1 + 1] - S[(size_t)r0 * st + c1 + 1] - S[(size_t)(r1 + 1) * st + c0] +
+           S[(size_t)r0 * st + c0];
+}
+
+// joint of (p_i xor neg_i) and (p_j xor neg_j) from c_i = |p_i|, c_j = |p_j|, c_ij = |p_i and p_j|
+__device__ __forceinline__ unsigned long long combine(unsigned long long n, unsigned long long ci,
+                                                      unsigned long long cj, unsigned long long cij,
+                                                      uint32_t ni, uint32_t nj) {
+    if (!ni && !nj) return cij;
+    if (ni && !nj) return cj - cij;
+    if (!ni && nj) return ci - cij;
+    return n - ci - cj + cij;
+}
+
+__global__ void fin_output(const FinParams F) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long n = *F.g_nsamp;
+    if (t == 0) F.out[0] = n;
+    if (t >= 1 && t <= F.npreds) {
+        const FinPred p = F.preds[t - 1];
+        const unsigned long long c = iv(F.g_pre + p.pre, p.lo, p.hi);
+        F.out[t] = p.neg ? n - c : c;
+    } else if (t > F.npreds && t <= F.npreds + F.npairs) {
+        const FinPair q = F.pairs[t - 1 - F.npreds];
+        unsigned long long r;
+        if (q.kind == PAIR_DIRECT) {
+            r = F.g_acc[q.pre];
+        } else if (q.kind == PAIR_SAME) {
+            const unsigned long long *pre = F.g_pre + q.pre;
+            const uint32_t lo = max(q.li, q.lj), hi = min(q.hi, q.hj);
+            r = combine(n, iv(pre, q.li, q.hi), iv(pre, q.lj, q.hj), iv(pre, lo, hi), q.negi, q.negj);
+        } else {
+            const unsigned long long *S = F.g_pre + q.pre;
+            const uint32_t st = q.nb + 1;
+            const unsigned long long ci = rect(S, st, q.li, q.hi, 0, q.nb - 1);
+            const unsigned long long cj = rect(S, st, 0, q.na - 1, q.lj, q.hj);
+            const unsigned long long cij = rect(S, st, q.li, q.hi, q.lj, q.hj);
+            r = combine(n, ci, cj, cij, q.negi, q.negj);
+        }
+        F.out[t] = r;
+    }
+}
+
+// ------------------------------------------------------------------ attach / test hook
+
+__global__ void minmax_kernel(const void *col, int dtype, uint64_t n, long long *mm) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const long long v = dtype == 0 ? (long long)__ldg(static_cast<const int32_t *>(col) + i)
+                                       : __ldg(static_cast<const long long *>(col) + i);
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+
+__global__ void sample_mask_kernel(uint64_t nrows, uint64_t row0, uint64_t seed, uint64_t thr,
+                                   uint32_t all, unsigned long long *bits) {
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w * 64 >= nrows) return;
+    unsigned long long m = 0;
+    for (int b = 0; b < 64; ++b) {
+        const uint64_t r = w * 64 + b;
+        if (r >= nrows) break;
+        const uint64_t g = row0 + r;
+        if (all || mix64(seed + (g + 1) * GACE_GAMMA) < thr) m |= 1ull << b;
+    }
+    bits[w] = m;
+}
+
+// ------------------------------------------------------------------ launchers
+
+template <int NC, bool CLAMP, bool SAMPLE>
+static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
+    auto k = probe_kernel<NC, CLAMP, SAMPLE>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    k<<<grid, kThreads, P.smem_bytes, s>>>(P);
+    return cudaGetLastError();
+}
+
+template <int NC>
+static cudaError_t launch_nc(const ProbeParams &P, bool clamp, bool sample, int grid, cudaStream_t s) {
+    if (clamp) return sample ? launch_t<NC, true, true>(P, grid, s) : launch_t<NC, true, false>(P, grid, s);
+    return sample ? launch_t<NC, false, true>(P, grid, s) : launch_t<NC, false, false>(P, grid, s);
+}
+
+cudaError_t launch_probe(const ProbeParams &P, bool clamp, bool sample, int grid, cudaStream_t s) {
+    const uint32_t n = P.nslots;
+    if (n <= 1) return launch_nc<1>(P, clamp, sample, grid, s);
+    if (n <= 2) return launch_nc<2>(P, clamp, sample, grid, s);
+    if (n <= 4) return launch_nc<4>(P, clamp, sample, grid, s);
+    return launch_nc<8>(P, clamp, sample, grid, s);
+}
+
+cudaError_t launch_finalize(const FinParams &F, cudaStream_t s) {
+    const uint32_t blocks = F.njobs + F.hll_blocks;
+    if (blocks) {
+        fin_prefix<<<blocks, 1024, 0, s>>>(F);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const uint32_t outs = 1 + F.npreds + F.npairs;
+    fin_output<<<(outs + 255) / 256, 256, 0, s>>>(F);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_minmax(const void *col, int dtype, uint64_t n, long long *mm, int sms, cudaStream_t s) {
+    const uint64_t want = (n + 255) / 256;
+    const int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
+    minmax_kernel<<<grid, 256, 0, s>>>(col, dtype, n, mm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_mask(uint64_t nrows, uint64_t row0, uint64_t seed, uint64_t thr, bool all,
+                               unsigned long long *bits, cudaStream_t s) {
+    const uint64_t words = (nrows + 63) / 64;
+    if (!words) return cudaSuccess;
+    sample_mask_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(nrows, row0, seed, thr, all, bits);
+    return cudaGetLastError();
+}
+
+int probe_kernel_regs(int nc, bool clamp, bool sample) {
+    cudaFuncAttributes a;
+    cudaError_t e;
+    if (nc <= 4) e = cudaFuncGetAttributes(&a, clamp ? (sample ? probe_kernel<4, true, true> : probe_kernel<4, true, false>)
+                                                      : (sample ? probe_kernel<4, false, true> : probe_kernel<4, false, false>));
+    else e = cudaFuncGetAttributes(&a, clamp ? (sample ? probe_kernel<8, true, true> : probe_kernel<8, true, false>)
+                                             : (sample ? probe_kernel<8, false, true> : probe_kernel<8, false, false>));
+    return e == cudaSuccess ? a.numRegs : -1;
+}
+
+}  // namespace gace

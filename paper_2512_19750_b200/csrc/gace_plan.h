@@ -1,0 +1,138 @@
+// gace_plan.h -- internal plan layout shared by the host planner (gace_host.cpp)
+// and the sm_100a kernels (gace_kernels.cu).  Not part of the C-ABI.
+//
+// The planner turns a predicate batch into, per probed column ("slot"):
+//   * the sorted breakpoints T of all its predicates (interval ends lo and hi+1,
+//     clipped to the column's value domain), so that every predicate is a
+//     contiguous bucket range of  bucket(v) = #{t in T : t <= v};
+//   * a two-level lookup table over the offset u = v - base that resolves
+//     bucket(v) with one shared-memory load and one compare;
+//   * a u32 shared-memory histogram over the buckets (counts are prefix sums);
+// and, per pair of probed columns carrying cross-column pairs ("group"), a 2-D
+// histogram over the sub-buckets of only the pair-relevant predicates (joints are
+// rectangle sums).  HLL registers live in shared memory as u8[4096] per column.
+#pragma once
+#include <stdint.h>
+
+namespace gace {
+
+constexpr int kMaxSlots = 8;           // GACE_MAX_PROBED_COLS
+constexpr int kMaxGroups = 28;         // unordered slot pairs
+constexpr int kHllP = 12;
+constexpr int kHllM = 1 << kHllP;
+constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM)
+constexpr uint32_t kNoThr = 0xFFFFFFFFu;
+constexpr uint32_t kL2Flag = 0x80000000u;
+constexpr uint32_t kBaseMask = 0x00FFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+enum SlotMode : uint8_t { MODE_LUT = 0, MODE_SEARCH = 1, MODE_NOPRED = 2 };
+
+// LUT entry (8 bytes).  Direct entry: x = absolute u32 index of the cell's first
+// bucket in shared memory (bits 0..23), y = threshold: bucket += (u > y).
+// Level-2 pointer: x = kL2Flag | s2 << 24, y = index of the first L2 entry.
+struct SlotParams {
+    const void *ptr;        // device column base for this launch
+    const int64_t *bps;     // MODE_SEARCH: sorted breakpoints (device)
+    int64_t base;           // u = (uint32)(v - base)
+    int64_t clamp_lo;       // CLAMP kernels: v = min(max(v, clamp_lo), clamp_hi)
+    int64_t clamp_hi;
+    uint32_t nbp;           // MODE_SEARCH: number of breakpoints
+    uint32_t s1;            // level-1 cell = u >> s1
+    uint32_t cell_mask;     // (1 << s1) - 1
+    uint32_t lut_idx;       // level-1 table: uint2 index into shared memory
+    uint32_t l2_idx;        // level-2 table: uint2 index into shared memory
+    uint32_t hist_idx;      // u32 index of bucket 0 of this column's histogram
+    uint32_t hll_off;       // byte offset of this column's u8[4096] registers, or kNone
+    uint8_t dtype;          // 0 = int32, 1 = int64
+    uint8_t mode;           // SlotMode
+    uint8_t has_hll;
+    uint8_t pad;
+};
+
+struct GroupParams {
+    int32_t mapA_adj;       // u32 index of mapA minus hist_idx of slot a (indexed by absolute bucket)
+    int32_t mapB_adj;
+    uint8_t a, b;           // slots, a < b
+    uint8_t pad[2];
+};
+
+// Cross-column pair evaluated per row (fallback when a group's 2-D grid does not fit).
+struct DirectPair {
+    uint32_t la, ha;        // absolute bucket interval of predicate on slot sa (la > ha: empty)
+    uint32_t lb, hb;
+    uint8_t sa, sb, nega, negb;
+    uint32_t acc_idx;       // u32 index of its counter in shared memory
+};
+
+struct ProbeParams {
+    SlotParams slot[kMaxSlots];
+    GroupParams grp[kMaxGroups];
+    int8_t combo[kMaxSlots * kMaxSlots];   // group of slots (a, b), a < b, or -1
+    uint32_t nslots;
+    uint32_t ndirect;
+    const DirectPair *direct;              // device
+    const uint4 *image;                    // device: tables copied into shared memory
+    uint32_t image_u4;                     // image size in 16-byte units
+    uint32_t acc_idx;                      // u32 index where the zeroed accumulators start
+    uint32_t acc_words;                    // number of u32 accumulators
+    uint32_t hll_off;                      // byte offset of the HLL register block
+    uint32_t hll_bytes;                    // nh * 4096
+    uint32_t smem_bytes;                   // total dynamic shared memory
+    unsigned long long *g_acc;             // u64[acc_words], summed over CTAs (and launches)
+    uint8_t *g_hll_part;                   // [part_slot][hll_bytes] per-CTA register partials
+    unsigned long long *g_nsamp;
+    uint64_t nrows;                        // rows in this launch
+    uint64_t row0;                         // global id of the launch's first row
+    uint64_t thr;                          // floor(rate * 2^64)
+    uint64_t seed;
+    uint32_t sample_all;                   // rate == 1
+    uint32_t part_merge;                   // 1: max-merge into existing per-CTA partials (later chunk launches)
+};
+
+// ---------------------------------------------------------------- finalize
+
+enum FinJobKind : uint32_t { JOB_HIST = 0, JOB_SAT = 1 };
+
+struct FinJob {
+    uint32_t kind;
+    uint32_t src;           // index into g_acc
+    uint32_t dst;           // index into g_pre
+    uint32_t na, nb;        // HIST: nb buckets (na unused); SAT: na x nb grid
+};
+
+enum FinPairKind : uint32_t { PAIR_SAME = 0, PAIR_GRID = 1, PAIR_DIRECT = 2 };
+
+struct FinPred {
+    uint32_t pre;           // g_pre index of the column's exclusive prefix (nb + 1 values)
+    uint32_t lo, hi;        // bucket interval (lo > hi: empty)
+    uint32_t neg;
+};
+
+struct FinPair {
+    uint32_t kind;
+    uint32_t pre;           // SAME: 1-D prefix; GRID: SAT (row stride nb + 1); DIRECT: g_acc index
+    uint32_t na, nb;        // GRID: grid extent
+    uint32_t li, hi, lj, hj;// SAME: bucket intervals; GRID: i on the A side, j on the B side
+    uint32_t negi, negj;
+};
+
+struct FinParams {
+    const FinJob *jobs;
+    uint32_t njobs;
+    uint32_t hll_bytes;
+    uint32_t nparts;        // number of per-CTA HLL partials
+    uint32_t hll_blocks;
+    const unsigned long long *g_acc;
+    unsigned long long *g_pre;
+    const uint8_t *g_hll_part;
+    const unsigned long long *g_nsamp;
+    const FinPred *preds;
+    uint32_t npreds;
+    const FinPair *pairs;
+    uint32_t npairs;
+    unsigned long long *out;    // [1 + npreds + npairs]: n_sampled, counts, joints
+    uint8_t *out_regs;          // [hll_bytes]
+};
+
+}  // namespace gace

@@ -1,0 +1,290 @@
+"""Thin ctypes binding over libgace.so (include/gace.h) -- argument marshalling only.
+
+Every step of the probe runs in the library's sm_100a kernels; this module
+only converts torch / numpy buffers into pointers and copies results into
+numpy arrays.  If libgace.so is missing it raises; there is no CPU fallback.
+
+Names follow the C-ABI: ``table_attach`` / ``table_attach_host`` ->
+``Table``; ``Table.probe`` (gace_probe); ``Table.sample_mask``;
+``derive`` (gace_derive); ``gate`` (gace_gate).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgace.so")
+
+GACE_OK, GACE_EINVAL, GACE_ENOMEM, GACE_ECUDA, GACE_ENCCL, GACE_EHANDLE, GACE_EUNSUPPORTED = range(7)
+STATUS_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "EHANDLE", "EUNSUPPORTED"]
+I32, I64 = 0, 1
+EQ, LT, LE, GT, GE, BETWEEN = range(6)
+NEGATE = 1
+SIG_DRIFT, SIG_SEL_ERROR, SIG_CORRELATION = 1, 2, 4
+HLL_P = 12
+HLL_M = 1 << HLL_P
+
+PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
+PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
+
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe",
+           "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
+           "gace_kernel_launches", "gace_last_error"]
+
+
+class GaceError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 7 else status}: {msg}")
+        self.status = status
+
+
+class _Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("row_offset", ctypes.c_uint64),
+                ("nrows_total", ctypes.c_uint64), ("nccl_unique_id", ctypes.c_void_p),
+                ("nccl_comm", ctypes.c_void_p)]
+
+
+class _Thresholds(ctypes.Structure):
+    _fields_ = [("d_threshold", ctypes.c_double), ("sel_err_threshold", ctypes.c_double),
+                ("pcs_high", ctypes.c_double), ("pcs_low", ctypes.c_double)]
+
+
+class _Timing(ctypes.Structure):
+    _fields_ = [("plan_upload_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
+                ("finalize_ms", ctypes.c_double), ("merge_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("scan_launches", ctypes.c_uint64),
+                ("bytes_scanned", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libgace.so (built in-tree by paper_2512_19750_b200.build); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2512_19750_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u32, u64, i32, dbl = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+    L.gace_table_attach.argtypes = [vp, vp, u32, u64, vp, i32, vp, ctypes.POINTER(vp)]
+    L.gace_table_attach_host.argtypes = [vp, vp, u32, u64, vp, i32, vp, ctypes.POINTER(vp)]
+    L.gace_table_detach.argtypes = [vp]
+    L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
+    L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
+    L.gace_derive.argtypes = [u64, vp, u32, vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp]
+    L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
+    L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
+    L.gace_nccl_unique_id.argtypes = [vp]
+    for f in EXPORTS:
+        if f not in ("gace_kernel_launches", "gace_last_error"):
+            getattr(L, f).restype = ctypes.c_int
+    L.gace_kernel_launches.restype = u64
+    L.gace_kernel_launches.argtypes = []
+    L.gace_last_error.restype = ctypes.c_char_p
+    L.gace_last_error.argtypes = []
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != GACE_OK:
+        raise GaceError(status, lib().gace_last_error().decode())
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None or a.size == 0 else a.ctypes.data
+
+
+def as_preds(preds) -> np.ndarray:
+    a = np.ascontiguousarray(preds)
+    return a if a.dtype == PRED_DTYPE else a.astype(PRED_DTYPE)
+
+
+def as_pairs(pairs) -> np.ndarray:
+    if pairs is None or len(pairs) == 0:
+        return np.zeros(0, dtype=PAIR_DTYPE)
+    a = np.ascontiguousarray(pairs)
+    return a if a.dtype == PAIR_DTYPE else a.astype(PAIR_DTYPE)
+
+
+def kernel_launches() -> int:
+    return int(lib().gace_kernel_launches())
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().gace_nccl_unique_id(buf))
+    return buf.raw
+
+
+@dataclass
+class ProbeResult:
+    n_sampled: int
+    counts: np.ndarray        # u64[P]
+    joints: np.ndarray        # u64[Q]
+    regs: np.ndarray          # u8[H, 4096], ascending column order
+
+
+@dataclass
+class DistInfo:
+    rank: int
+    nranks: int
+    row_offset: int
+    nrows_total: int
+    unique_id: bytes | None = None
+    comm: int | None = None
+
+
+def _dtype_code(dt) -> int:
+    s = str(dt)
+    if s.endswith("int32"):
+        return I32
+    if s.endswith("int64"):
+        return I64
+    raise GaceError(GACE_EINVAL, f"unsupported column dtype {dt}")
+
+
+class Table:
+    """A table attached to the library.  ``columns``: CUDA torch tensors (device
+    table, zero-copy) or, with ``host=True``, CPU tensors / numpy arrays (host table:
+    every probe streams the probed keys over PCIe)."""
+
+    def __init__(self, columns: Sequence, host: bool = False, dist: DistInfo | None = None,
+                 device: int | None = None, stream=None):
+        L = lib()
+        self._cols = list(columns)
+        if not self._cols:
+            raise GaceError(GACE_EINVAL, "no columns")
+        nrows = len(self._cols[0])
+        ptrs, codes = [], []
+        for c in self._cols:
+            if len(c) != nrows:
+                raise GaceError(GACE_EINVAL, "columns differ in length")
+            codes.append(_dtype_code(c.dtype))
+            if isinstance(c, np.ndarray):
+                if not host:
+                    raise GaceError(GACE_EINVAL, "numpy columns need host=True")
+                ptrs.append(c.ctypes.data)
+            else:
+                if not c.is_contiguous():
+                    raise GaceError(GACE_EINVAL, "columns must be contiguous")
+                if host != (not c.is_cuda):
+                    raise GaceError(GACE_EINVAL, "device tables take CUDA tensors, host tables CPU tensors")
+                ptrs.append(c.data_ptr())
+                if device is None and c.is_cuda:
+                    device = c.device.index
+        self.nrows = nrows
+        self.ncols = len(self._cols)
+        self.host = host
+        arr_p = (ctypes.c_void_p * self.ncols)(*ptrs)
+        arr_t = (ctypes.c_int * self.ncols)(*codes)
+        d = None
+        self._uid = None
+        if dist is not None:
+            self._uid = ctypes.create_string_buffer(dist.unique_id, 128) if dist.unique_id else None
+            d = _Dist(dist.rank, dist.nranks, dist.row_offset, dist.nrows_total,
+                      ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None, dist.comm)
+        self.row_offset = dist.row_offset if dist else 0
+        s = None
+        if stream is not None:
+            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        h = ctypes.c_void_p()
+        fn = L.gace_table_attach_host if host else L.gace_table_attach
+        _check(fn(arr_p, arr_t, self.ncols, nrows, ctypes.byref(d) if d is not None else None,
+                  0 if device is None else device, s, ctypes.byref(h)))
+        self._h = h
+
+    def probe(self, preds, pairs=None, sample_rate: float = 1.0, seed: int = 0,
+              hll_cols: Sequence[int] = (), hll_p: int = HLL_P) -> ProbeResult:
+        P = as_preds(preds)
+        Q = as_pairs(pairs)
+        mask = 0
+        for c in hll_cols:
+            mask |= 1 << int(c)
+        nh = bin(mask).count("1")
+        counts = np.zeros(max(len(P), 1), dtype=np.uint64)
+        joints = np.zeros(max(len(Q), 1), dtype=np.uint64)
+        regs = np.zeros((max(nh, 1), HLL_M), dtype=np.uint8)
+        n = ctypes.c_uint64()
+        _check(lib().gace_probe(self._h, _ptr(P), len(P), _ptr(Q), len(Q), float(sample_rate),
+                                int(seed) & ((1 << 64) - 1), mask, hll_p, ctypes.byref(n),
+                                counts.ctypes.data, joints.ctypes.data, regs.ctypes.data))
+        return ProbeResult(int(n.value), counts[:len(P)], joints[:len(Q)], regs[:nh])
+
+    def sample_mask(self, sample_rate: float, seed: int) -> np.ndarray:
+        bits = np.zeros(max(1, (self.nrows + 63) // 64), dtype=np.uint64)
+        _check(lib().gace_sample_mask(self._h, float(sample_rate), int(seed) & ((1 << 64) - 1),
+                                      bits.ctypes.data))
+        return bits[:(self.nrows + 63) // 64]
+
+    def last_timing(self) -> dict:
+        t = _Timing()
+        _check(lib().gace_last_timing(self._h, ctypes.byref(t)))
+        return {f: getattr(t, f) for f, _ in _Timing._fields_}
+
+    def detach(self):
+        if self._h is not None and self._h.value:
+            _check(lib().gace_table_detach(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.detach()
+        except Exception:
+            pass
+
+
+def table_attach(columns, dist: DistInfo | None = None, stream=None) -> Table:
+    return Table(columns, host=False, dist=dist, stream=stream)
+
+
+def table_attach_host(columns, dist: DistInfo | None = None, device: int = 0, stream=None) -> Table:
+    return Table(columns, host=True, dist=dist, device=device, stream=stream)
+
+
+def derive(n_sampled: int, counts, pairs, joints, regs, ndv_hist=None):
+    """gace_derive: (sel[P], pcs[Q], ndv_est[H], drift[H]) as float64 arrays."""
+    counts = np.ascontiguousarray(counts, dtype=np.uint64)
+    Q = as_pairs(pairs)
+    joints = np.ascontiguousarray(joints, dtype=np.uint64)
+    regs = np.ascontiguousarray(regs, dtype=np.uint8).reshape(-1, HLL_M) if regs is not None and len(regs) \
+        else np.zeros((0, HLL_M), np.uint8)
+    H = regs.shape[0]
+    sel = np.zeros(max(len(counts), 1))
+    pcs = np.zeros(max(len(Q), 1))
+    ndv = np.zeros(max(H, 1))
+    drift = np.zeros(max(H, 1))
+    hist = None if ndv_hist is None else np.ascontiguousarray(ndv_hist, dtype=np.float64)
+    _check(lib().gace_derive(n_sampled, _ptr(counts), len(counts), _ptr(Q), _ptr(joints), len(Q),
+                             _ptr(regs), H, HLL_P, _ptr(hist), sel.ctypes.data, pcs.ctypes.data,
+                             ndv.ctypes.data, drift.ctypes.data if hist is not None else None))
+    return sel[:len(counts)], pcs[:len(Q)], ndv[:H], (drift[:H] if hist is not None else None)
+
+
+def gate(drift=(), s_est=(), s_probe=(), pcs=(), thresholds: dict | None = None):
+    """gace_gate: (fired_mask, per-signal bool array in the order drift, sel, pcs)."""
+    d = np.ascontiguousarray(drift, dtype=np.float64)
+    se = np.ascontiguousarray(s_est, dtype=np.float64)
+    sp = np.ascontiguousarray(s_probe, dtype=np.float64)
+    pc = np.ascontiguousarray(pcs, dtype=np.float64)
+    if len(se) != len(sp):
+        raise GaceError(GACE_EINVAL, "s_est and s_probe differ in length")
+    th = None
+    if thresholds is not None:
+        t = {"d": 0.25, "sel_err": 0.01, "pcs_high": 1.6, "pcs_low": 0.7}
+        t.update(thresholds)
+        th = _Thresholds(t["d"], t["sel_err"], t["pcs_high"], t["pcs_low"])
+    per = np.zeros(max(len(d) + len(se) + len(pc), 1), dtype=np.uint8)
+    mask = ctypes.c_uint32()
+    _check(lib().gace_gate(_ptr(d), len(d), _ptr(se), _ptr(sp), len(se), _ptr(pc), len(pc),
+                           ctypes.byref(th) if th is not None else None, ctypes.byref(mask),
+                           per.ctypes.data))
+    return int(mask.value), per[:len(d) + len(se) + len(pc)].astype(bool)

@@ -1,0 +1,86 @@
+"""The C-ABI boundary on CPU: libgace.so loads and exports every symbol
+include/gace.h declares; host-only calls (derive, gate) agree with the oracle;
+device calls fail loudly without a GPU; the product never imports the oracle."""
+import ast
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2512_19750_b200 import build, gace
+    build.build()
+    gace.lib()
+    return gace
+
+
+def test_exports_match_header(G):
+    hdr = open(os.path.join(ROOT, "include", "gace.h")).read()
+    declared = set(re.findall(r"^\s*(?:gace_status|uint64_t|const char \*)\s*(gace_\w+)\s*\(", hdr, re.M))
+    assert declared == set(G.EXPORTS)
+    L = G.lib()
+    for name in declared:
+        assert hasattr(L, name)
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2512_19750_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert not any(a.name.split(".")[0] == "oracle" for a in node.names)
+                    if isinstance(node, ast.ImportFrom):
+                        assert (node.module or "").split(".")[0] != "oracle"
+            if f.endswith((".cu", ".cpp", ".h")):
+                assert "oracle" not in open(os.path.join(dirpath, f)).read().lower()
+
+
+def test_attach_without_gpu_fails_loudly(G):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    col = np.zeros(16, dtype=np.int32)
+    with pytest.raises(G.GaceError) as e:
+        G.Table([col], host=True)
+    assert e.value.status == G.GACE_ECUDA
+
+
+def test_gate_matches_oracle(G, oracle):
+    g = np.random.default_rng(0)
+    for _ in range(200):
+        d = list(g.choice([0.0, 0.1, 0.25, 0.2499999, 0.3, float("nan"), 1.0], size=3))
+        se = list(g.random(2))
+        sp = [x + g.choice([0.0, 0.01, -0.02, 0.005]) for x in se]
+        pc = list(g.choice([1.6, 0.7, 1.0, 1.61, 0.69, float("nan"), 5.0], size=2))
+        mask, per = G.gate(d, se, sp, pc)
+        omask, oper = oracle.gate(d, se, sp, pc)
+        assert mask == omask and list(per) == oper
+    assert G.gate([0.2], thresholds={"d": 0.15})[0] == G.SIG_DRIFT
+
+
+def test_derive_matches_oracle(G, oracle):
+    import synth
+    w = synth.get("C4", 40000)
+    t = [x.numpy() for x in w.table()]
+    n, c, j, regs = oracle.probe(t, w.preds, w.pairs, rate=0.9, seed=3, hll_cols=w.hll_cols)
+    sel, pcs, ndv, drift = G.derive(n, c, w.pairs, j, regs, w.ndv_hist)
+    osel, opcs, ondv, odrift = oracle.derive(n, c, w.pairs, j, regs, w.ndv_hist)
+
+    def close(a, b):
+        return (math.isnan(a) and math.isnan(b)) or abs(a - b) <= 1e-12 * max(abs(a), abs(b))
+    for a, b in zip(list(sel) + list(pcs) + list(ndv) + list(drift), osel + opcs + ondv + odrift):
+        assert close(float(a), float(b))
+    # degenerate: n = 0, zero marginals
+    sel, pcs, _, _ = G.derive(0, [0, 0], [(0, 1)], [0], None)
+    assert math.isnan(sel[0]) and math.isnan(pcs[0])
+    with pytest.raises(G.GaceError):
+        G.derive(5, [1], [], [], np.zeros((1, 4096), np.uint8), [0.0])

@@ -1,0 +1,82 @@
+"""World-size-2 gloo run of the multi-GPU dataflow on CPU.
+
+Each rank takes its contiguous shard [floor(gN/G), floor((g+1)N/G)), runs the
+per-shard probe with its global row offset, and the two ranks merge with one
+all-reduce(sum) over [n_sampled, counts, joints] and one all-reduce(max) over
+the HLL registers -- the exchange the product does with NCCL.  The merged
+result must equal the single-process whole-table probe bit for bit.  The
+shard arithmetic and the unique-id broadcast are the product's host helpers
+(paper_2512_19750_b200.dist), exercised here without a GPU.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, nrows, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from oracle import reference as R
+        from paper_2512_19750_b200 import dist as gdist
+        w = synth.get(name, nrows)
+        r0, r1 = gdist.shard_range(rank, world, w.nrows)
+        cols = [x.numpy() for x in w.table(r0, r1)]
+        n, c, j, regs = R.probe(cols, w.preds, w.pairs, rate=0.7, seed=31,
+                                hll_cols=w.hll_cols, row_offset=r0)
+        sums = torch.tensor(np.concatenate([[n], c, j]).astype(np.int64))
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        mx = torch.tensor(regs.astype(np.int32))
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        uid = gdist.broadcast_unique_id(bytes(range(128)) if rank == 0 else None)
+        if rank == 0:
+            q.put((sums.numpy(), mx.numpy(), uid))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,nrows", [("C1", 10007), ("C5", 6001)])
+def test_two_rank_merge_equals_whole(oracle, name, nrows):
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, nrows, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    sums, mx, uid = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = synth.get(name, nrows)
+    n, c, j, regs = oracle.probe([x.numpy() for x in w.table()], w.preds, w.pairs, rate=0.7,
+                                 seed=31, hll_cols=w.hll_cols)
+    assert sums[0] == n
+    assert np.array_equal(sums[1:1 + len(c)], c.astype(np.int64))
+    assert np.array_equal(sums[1 + len(c):], j.astype(np.int64))
+    assert np.array_equal(mx, regs.astype(np.int32))
+    assert uid == bytes(range(128))
+
+
+def test_shard_ranges_cover():
+    from paper_2512_19750_b200 import dist as gdist
+    for N in (0, 1, 7, 600_037_902):
+        for G in (1, 2, 3, 4, 8):
+            rs = [gdist.shard_range(g, G, N) for g in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == N
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(e - s for s, e in rs) - min(e - s for s, e in rs) <= 1

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element.
+
+Counts, joint counts, HLL registers, n_sampled and the sample mask must be
+bit-exact (BASELINE.json north_star).  Inputs are the seeded synthetic
+workloads (synth/) at sizes the oracle finishes in seconds that still span
+many CTAs, row quads and a ragged tail, plus edge cases.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+I32MIN, I32MAX = -(2 ** 31), 2 ** 31 - 1
+I64MIN, I64MAX = -(2 ** 63), 2 ** 63 - 1
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2512_19750_b200 import build, gace
+    build.build()
+    gace.lib()
+    assert torch.cuda.is_available()
+    return gace
+
+
+def _gpu_probe(G, cols_np, preds, pairs, rate, seed, hll_cols, row_offset=0, host=False):
+    if host:
+        cols = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in cols_np]
+    else:
+        cols = [torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in cols_np]
+    dist = G.DistInfo(0, 1, row_offset, row_offset + len(cols_np[0])) if row_offset else None
+    t = G.Table(cols, host=host, dist=dist, device=0)
+    try:
+        return t.probe(preds, pairs, rate, seed, hll_cols)
+    finally:
+        t.detach()
+
+
+def _assert_same(got, want):
+    n, c, j, r = want
+    assert got.n_sampled == n
+    np.testing.assert_array_equal(got.counts, c)
+    np.testing.assert_array_equal(got.joints, j)
+    assert got.regs.shape == r.shape
+    np.testing.assert_array_equal(got.regs, r)
+
+
+def _check(G, oracle, cols, preds, pairs=None, rate=1.0, seed=0, hll_cols=(), row_offset=0, host=False):
+    want = oracle.probe(cols, preds, pairs, rate=rate, seed=seed, hll_cols=hll_cols, row_offset=row_offset)
+    got = _gpu_probe(G, cols, preds, pairs, rate, seed, hll_cols, row_offset, host)
+    _assert_same(got, want)
+    return got
+
+
+# ------------------------------------------------------------------ workload shapes
+
+@pytest.mark.parametrize("name,nrows,rate", [
+    ("C1", 100_003, 1.0), ("C1", 65_537, 0.37),
+    ("C2", 200_001, 0.01), ("C2", 50_000, 0.5),
+    ("C3", 300_002, 1.0), ("C3B", 100_001, 1.0),
+    ("C4", 100_003, 1.0), ("C4", 40_000, 0.2),
+    ("C5", 120_001, 1.0), ("C5_i64", 60_007, 1.0), ("C5", 50_000, 0.05),
+])
+def test_workloads(G, oracle, name, nrows, rate):
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, w.sample_seed + 17, w.hll_cols)
+
+
+@pytest.mark.parametrize("name", ["C1", "C5"])
+def test_host_table_path(G, oracle, name):
+    w = synth.get(name, 70_001)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, 1.0, 0, w.hll_cols, host=True)
+    _check(G, oracle, cols, w.preds, w.pairs, 0.3, 9, w.hll_cols, host=True)
+
+
+def test_shard_offsets_and_merge(G, oracle):
+    w = synth.get("C5", 90_000)
+    cols = [x.numpy() for x in w.table()]
+    whole = oracle.probe(cols, w.preds, w.pairs, rate=0.6, seed=5, hll_cols=w.hll_cols)
+    cuts = [0, 4, 30_001, 61_113, 90_000]
+    parts = []
+    for s, e in zip(cuts, cuts[1:]):
+        part = [c[s:e] for c in cols]
+        parts.append(_check(G, oracle, part, w.preds, w.pairs, 0.6, 5, w.hll_cols, row_offset=s))
+    assert sum(p.n_sampled for p in parts) == whole[0]
+    np.testing.assert_array_equal(sum(p.counts for p in parts), whole[1])
+    np.testing.assert_array_equal(sum(p.joints for p in parts), whole[2])
+    np.testing.assert_array_equal(np.maximum.reduce([p.regs for p in parts]), whole[3])
+
+
+# ------------------------------------------------------------------ edge cases
+
+def _boundary_preds(col, vals):
+    rows = []
+    for op in range(5):
+        for a in vals:
+            for fl in (0, 1):
+                rows.append((col, op, fl, a, 0))
+    for a in vals[::2]:
+        for b in vals[1::2]:
+            rows.append((col, 5, 0, a, b))
+            rows.append((col, 5, 1, a, b))
+    return np.array(rows, dtype=synth.PRED_DTYPE)
+
+
+@pytest.mark.parametrize("nrows", [0, 1, 3, 4, 5, 31, 32, 33, 4095, 4097, 148 * 1024 * 4 + 3])
+def test_ragged_sizes(G, oracle, nrows):
+    g = np.random.default_rng(nrows)
+    c0 = g.integers(-5, 5, size=nrows).astype(np.int32)
+    c1 = g.integers(I32MIN, I32MAX, size=nrows, endpoint=True).astype(np.int32)
+    vals = [I64MIN, I32MIN - 1, I32MIN, -3, -1, 0, 2, 4, I32MAX, I32MAX + 1, I64MAX]
+    P = np.concatenate([_boundary_preds(0, vals), _boundary_preds(1, [I32MIN, -7, 0, 10 ** 9, I32MAX])])
+    Q = np.array([(0, 1), (5, 200), (3, 3), (100, 7)], dtype=synth.PAIR_DTYPE)
+    for rate in (1.0, 0.5):
+        _check(G, oracle, [c0, c1], P, Q, rate, 3, [0, 1])
+
+
+def test_all_equal_column_max_contention(G, oracle):
+    n = 2_000_003
+    c = np.full(n, 7, dtype=np.int32)
+    P = np.array([(0, 0, 0, 7, 0), (0, 1, 0, 7, 0), (0, 5, 0, 0, 10), (0, 0, 1, 7, 0)], dtype=synth.PRED_DTYPE)
+    _check(G, oracle, [c, c.copy()], np.concatenate([P, P.copy().astype(synth.PRED_DTYPE)]),
+           np.array([(0, 4), (1, 6)], dtype=synth.PAIR_DTYPE), 1.0, 0, [0])
+
+
+@pytest.mark.parametrize("rate", [0.0, 2.0 ** -60, 0.01, 0.5, 1.0 - 2.0 ** -53, 1.0])
+def test_sample_rates_and_mask(G, oracle, rate):
+    w = synth.get("C1", 50_001)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, 42, w.hll_cols)
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols], dist=G.DistInfo(0, 1, 12345, 10 ** 9))
+    try:
+        np.testing.assert_array_equal(t.sample_mask(rate, 42), oracle.sample_mask(50_001, rate, 42, 12345))
+    finally:
+        t.detach()
+
+
+def test_int64_wide_domain_search_mode(G, oracle):
+    g = np.random.default_rng(1)
+    n = 100_000
+    c = g.integers(I64MIN, I64MAX, size=n, dtype=np.int64, endpoint=True)
+    c[:10] = [I64MIN, I64MAX, 0, -1, 1, I64MIN + 1, I64MAX - 1, 5, 5, 5]
+    small = g.integers(-1000, 1000, size=n).astype(np.int64) * (1 << 40)
+    vals = [I64MIN, I64MIN + 1, -(1 << 62), -1, 0, 1, 5, 1 << 62, I64MAX - 1, I64MAX]
+    P = np.concatenate([_boundary_preds(0, vals), _boundary_preds(1, [-(1 << 50), 0, 7 << 40, 1 << 52])])
+    Q = np.array([(0, 150), (10, 11), (3, 140)], dtype=synth.PAIR_DTYPE)
+    _check(G, oracle, [c, small], P, Q, 1.0, 0, [0, 1])
+    _check(G, oracle, [c, small], P, Q, 0.4, 8, [0, 1], host=True)
+
+
+def test_many_predicates_one_column(G, oracle):
+    g = np.random.default_rng(2)
+    n = 300_000
+    c = g.integers(0, 1 << 20, size=n).astype(np.int32)
+    lo = g.integers(0, 1 << 20, size=4096)
+    w = g.integers(0, 5000, size=4096)
+    ops = g.integers(0, 6, size=4096)
+    P = np.zeros(4096, dtype=synth.PRED_DTYPE)
+    P["col"] = 0
+    P["op"] = ops
+    P["flags"] = g.integers(0, 2, size=4096)
+    P["a"] = lo
+    P["b"] = lo + w
+    Q = np.stack([g.integers(0, 4096, size=4096), g.integers(0, 4096, size=4096)], 1)
+    Q = np.array([tuple(x) for x in Q], dtype=synth.PAIR_DTYPE)
+    _check(G, oracle, [c], P, Q, 1.0, 0, [0])
+
+
+def test_direct_pair_fallback(G, oracle):
+    # many distinct predicates on both sides of one column pair: the 2-D grid does
+    # not fit shared memory and the pairs are evaluated per row instead
+    g = np.random.default_rng(3)
+    n = 200_000
+    a = g.integers(0, 100_000, size=n).astype(np.int32)
+    b = g.integers(0, 100_000, size=n).astype(np.int32)
+    k = 600
+    P = np.zeros(2 * k, dtype=synth.PRED_DTYPE)
+    P["col"][k:] = 1
+    P["op"] = 5
+    P["a"] = g.integers(0, 100_000, size=2 * k)
+    P["b"] = P["a"] + g.integers(0, 20_000, size=2 * k)
+    P["flags"] = g.integers(0, 2, size=2 * k)
+    Q = np.array([(i, k + (i * 7) % k) for i in range(k)], dtype=synth.PAIR_DTYPE)
+    _check(G, oracle, [a, b], P, Q, 1.0, 0, [])
+    _check(G, oracle, [a, b], P, Q, 0.5, 1, [0])
+
+
+def test_eight_columns_every_group(G, oracle):
+    g = np.random.default_rng(4)
+    n = 80_001
+    cols = [g.integers(-50 * (c + 1), 50 * (c + 1), size=n).astype(np.int32 if c % 3 else np.int64)
+            for c in range(9)]
+    rows = []
+    for c in range(8):
+        for _ in range(6):
+            x = int(g.integers(-60 * (c + 1), 60 * (c + 1)))
+            rows.append((c, int(g.integers(0, 6)), int(g.integers(0, 2)), x, x + int(g.integers(0, 40))))
+    P = np.array(rows, dtype=synth.PRED_DTYPE)
+    Q = np.array([(int(i), int(j)) for i, j in zip(g.integers(0, 48, 200), g.integers(0, 48, 200))],
+                 dtype=synth.PAIR_DTYPE)
+    _check(G, oracle, cols, P, Q, 1.0, 0, [0, 3, 7])
+    _check(G, oracle, cols, P, Q, 0.7, 2, [1, 2, 4, 5, 6])
+
+
+def test_hll_only_and_nine_columns_rejected(G, oracle):
+    g = np.random.default_rng(5)
+    cols = [g.integers(-10 ** 6, 10 ** 6, size=10_000).astype(np.int32) for _ in range(9)]
+    _check(G, oracle, cols, np.zeros(0, dtype=synth.PRED_DTYPE), None, 1.0, 0, list(range(8)))
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols])
+    try:
+        with pytest.raises(G.GaceError) as e:
+            t.probe(np.zeros(0, dtype=synth.PRED_DTYPE), None, 1.0, 0, list(range(9)))
+        assert e.value.status == G.GACE_EUNSUPPORTED
+        with pytest.raises(G.GaceError) as e:
+            t.probe(np.zeros(0, dtype=synth.PRED_DTYPE), None, float("nan"), 0, [0])
+        assert e.value.status == G.GACE_EINVAL
+        with pytest.raises(G.GaceError):
+            t.probe(np.array([(9, 0, 0, 0, 0)], dtype=synth.PRED_DTYPE))
+    finally:
+        t.detach()
+
+
+def test_randomised_sweep(G, oracle):
+    """>= 1000 randomised small requests (SPEC.md S:543 style)."""
+    g = np.random.default_rng(6)
+    n = 20_011
+    base = [g.integers(-30, 30, size=n).astype(np.int32), g.integers(0, 1000, size=n).astype(np.int32),
+            (g.integers(-5, 5, size=n) * (1 << 33)).astype(np.int64)]
+    t = G.Table([torch.from_numpy(c).cuda() for c in base])
+    try:
+        for trial in range(1000):
+            np_ = int(g.integers(1, 12))
+            rows = []
+            for _ in range(np_):
+                c = int(g.integers(0, 3))
+                scale = [1, 30, 1 << 33][c]
+                x = int(g.integers(-35, 35)) * scale
+                rows.append((c, int(g.integers(0, 6)), int(g.integers(0, 2)), x, x + int(g.integers(-2, 20)) * scale))
+            P = np.array(rows, dtype=synth.PRED_DTYPE)
+            Q = np.array([(int(g.integers(0, np_)), int(g.integers(0, np_))) for _ in range(int(g.integers(0, 6)))],
+                         dtype=synth.PAIR_DTYPE)
+            rate = float(g.choice([1.0, 0.5, 0.05]))
+            hll = [int(c) for c in g.choice(3, size=int(g.integers(0, 3)), replace=False)]
+            got = t.probe(P, Q, rate, trial, hll)
+            want = oracle.probe(base, P, Q, rate=rate, seed=trial, hll_cols=hll)
+            _assert_same(got, want)
+    finally:
+        t.detach()
+
+
+def test_derived_values_end_to_end(G, oracle):
+    w = synth.get("C4", 100_000)
+    cols = [x.numpy() for x in w.table()]
+    got = _gpu_probe(G, cols, w.preds, w.pairs, 1.0, 0, w.hll_cols)
+    sel, pcs, ndv, drift = G.derive(got.n_sampled, got.counts, w.pairs, got.joints, got.regs, w.ndv_hist)
+    osel, opcs, ondv, odrift = oracle.derive(got.n_sampled, got.counts, w.pairs, got.joints, got.regs, w.ndv_hist)
+    np.testing.assert_allclose(sel, osel, rtol=1e-12)
+    np.testing.assert_allclose(pcs, opcs, rtol=1e-12)
+    np.testing.assert_allclose(ndv, ondv, rtol=1e-12)
+    np.testing.assert_allclose(drift, odrift, rtol=1e-12)
