@@ -210,6 +210,20 @@ gace_status gace_last_timing(const gace_table *t, gace_timing *out);
  * the other ranks (GACE_ENCCL if libnccl.so.2 cannot be loaded). */
 gace_status gace_nccl_unique_id(void *id128);
 
+/* Test hook (host only; no device needed): plan a predicate batch for a table with
+ * value domains [dlo[c], dhi[c]] (host = 0: device table; 1: host table) and resolve
+ * values[n] of column `col` through the planned lookup table with the kernel's own
+ * lookup code (csrc/gace_plan.h lut_lookup), bounds-checked.  out[k] = bucket of
+ * values[k] relative to the column's bucket 0 (= #{breakpoints <= v}); *mode = 0 lookup
+ * table, 1 binary search; the column's sorted breakpoints go to bps[cap], *nbp = count.
+ * GACE_EUNSUPPORTED "internal: ..." reports a plan that would read out of range.     */
+gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
+                               const int64_t *dhi, int host, const gace_pred *preds,
+                               uint32_t npreds, const gace_pair *pairs, uint32_t npairs,
+                               uint64_t hll_mask, uint32_t col, const int64_t *values, uint64_t n,
+                               uint32_t *out, uint32_t *mode, int64_t *bps, uint32_t cap,
+                               uint32_t *nbp);
+
 /* Number of this library's CUDA kernels launched since load (all tables). */
 uint64_t gace_kernel_launches(void);
 

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -219,13 +220,23 @@ struct SlotPlan {
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
     std::vector<uint2> l1, l2;         // entries with slot-relative indices (fixed up later)
+    std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
     // layout
-    uint32_t lut_idx = 0, l2_idx = 0, hist_idx = 0, hll_off = kNone, bps_off = 0, pre = 0;
+    uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_idx = 0, hll_off = kNone, bps_off = 0, pre = 0;
 };
 
-// Build the two-level LUT of a slot for level-1 shift s1 over offsets [0, span].
-// Entries hold RELATIVE bucket numbers and RELATIVE L2 indices here.
-void build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
+uint32_t ceil_log2(uint64_t x) {
+    uint32_t r = 0;
+    while ((1ull << r) < x) ++r;
+    return r;
+}
+
+// Build the lookup table of a slot for level-1 shift s1 over offsets u in [0, span]
+// (entry formats: gace_plan.h).  Entries hold RELATIVE bucket numbers and RELATIVE
+// sub-table / list indices here; make_plan adds the slot's shared-memory offsets.
+// A cell with <= 8 breakpoints is a leaf (direct or list); a denser cell points to a
+// block of uniform sub-cells, built recursively (shift strictly decreases).
+bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     std::vector<uint64_t> toff;
     toff.reserve(S.T.size());
     for (int64_t t : S.T) toff.push_back((uint64_t)t - (uint64_t)S.base);   // in [1, span]
@@ -233,30 +244,49 @@ void build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     S.s1 = s1;
     S.l1.clear();
     S.l2.clear();
+    S.lst.clear();
+    bool ok = true;
+    // entry for offsets [lo, hi] of a cell of size 2^s
+    std::function<uint2(uint64_t, uint64_t, uint32_t)> node = [&](uint64_t lo, uint64_t hi, uint32_t s) -> uint2 {
+        const uint32_t b0 = le(lo), b1 = le(hi), cnt = b1 - b0;   // breakpoints in (lo, hi]
+        if (cnt == 0) return make_uint2(b0, kNoThr);
+        if (cnt == 1) return make_uint2(b0, (uint32_t)(toff[b0] - 1));
+        if (cnt <= 8 || s == 0) {
+            uint2 e = make_uint2(kSpecial | kList | (cnt << 24) | b0, (uint32_t)S.lst.size());
+            for (uint32_t i = b0; i < b1; ++i) S.lst.push_back((uint32_t)toff[i]);
+            return e;
+        }
+        // sub-cells at the minimum breakpoint gap when affordable (then each holds <= 1),
+        // else about two sub-cells per breakpoint
+        uint64_t gap = UINT64_MAX;
+        for (uint32_t i = b0 + 1; i < b1; ++i) gap = std::min(gap, toff[i] - toff[i - 1]);
+        uint32_t sc = 0;
+        while (sc + 1 < s && (2ull << sc) <= gap) ++sc;          // 2^sc <= gap, sc < s
+        if (((hi - lo) >> sc) + 1 > 4ull * cnt + 16) {
+            const uint32_t want = ceil_log2(cnt) + 1;
+            sc = s > want ? s - want : 0;
+        }
+        const uint64_t nsub = ((hi - lo) >> sc) + 1;
+        if (S.l2.size() + nsub > (1u << 22)) { ok = false; return make_uint2(b0, kNoThr); }
+        const uint32_t first = (uint32_t)S.l2.size();
+        S.l2.resize(first + nsub);
+        for (uint64_t j = 0; j < nsub; ++j) {
+            const uint64_t slo = lo + (j << sc), shi = std::min<uint64_t>(slo + (1ull << sc) - 1, hi);
+            const uint2 e = node(slo, shi, sc);
+            S.l2[first + j] = e;
+        }
+        return make_uint2(kSpecial | (sc << 24), first);
+    };
     const uint64_t ncells = (span >> s1) + 1;
     const uint64_t csize = 1ull << s1;
-    for (uint64_t k = 0; k < ncells; ++k) {
+    for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
-        const uint32_t b0 = le(lo), b1 = le(hi);
-        if (b1 - b0 == 0) {
-            S.l1.push_back(make_uint2(b0, kNoThr));
-        } else if (b1 - b0 == 1) {
-            S.l1.push_back(make_uint2(b0, (uint32_t)(toff[b0] - 1)));
-        } else {
-            uint64_t gap = UINT64_MAX;
-            for (uint32_t i = b0 + 1; i < b1; ++i) gap = std::min(gap, toff[i] - toff[i - 1]);
-            uint32_t s2 = 0;
-            while (s2 + 1 < s1 && (2ull << s2) <= gap) ++s2;            // 2^s2 <= gap
-            const uint64_t nsub = ((hi - lo) >> s2) + 1;
-            S.l1.push_back(make_uint2(kL2Flag | (s2 << 24), (uint32_t)S.l2.size()));
-            for (uint64_t j = 0; j < nsub; ++j) {
-                const uint64_t slo = lo + (j << s2), shi = std::min<uint64_t>(slo + (1ull << s2) - 1, hi);
-                const uint32_t c0 = le(slo), c1 = le(shi);
-                S.l2.push_back(make_uint2(c0, c1 == c0 ? kNoThr : (uint32_t)(toff[c0] - 1)));
-            }
-        }
+        S.l1.push_back(node(lo, hi, s1));
     }
+    return ok;
 }
+
+size_t lut_bytes(const SlotPlan &S) { return 8 * (S.l1.size() + S.l2.size()) + 4 * S.lst.size() + 32; }
 
 struct Group {
     int a, b;                          // slots a < b
@@ -404,10 +434,17 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             S.mode = MODE_SEARCH;
         }
     }
-    // level-1 size target: 16 cells per breakpoint, 64..4096; halve the largest table while over budget
+    // level-1 size target: 16 cells per breakpoint, 64..4096; coarsen the largest table while over budget
     std::vector<uint32_t> s1(pl.slots.size(), 0);
     auto span_of = [](const SlotPlan &S) -> uint64_t {
         return S.clamp ? (uint64_t)S.clamp_hi - (uint64_t)S.clamp_lo : (uint64_t)S.dh - (uint64_t)S.dl;
+    };
+    auto to_search = [](SlotPlan &S) {
+        S.mode = MODE_SEARCH;
+        S.clamp = false;
+        S.l1.clear();
+        S.l2.clear();
+        S.lst.clear();
     };
     for (size_t i = 0; i < pl.slots.size(); ++i) {
         SlotPlan &S = pl.slots[i];
@@ -418,7 +455,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         uint32_t sh = 0;
         while (sh < 31 && (span >> sh) + 1 > target) ++sh;
         s1[i] = sh;
-        build_lut(S, span, sh);
+        if (!build_lut(S, span, sh)) to_search(S);
     }
     for (int iter = 0; iter < 256; ++iter) {
         size_t tot = 0;
@@ -427,33 +464,33 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         for (size_t i = 0; i < pl.slots.size(); ++i) {
             const SlotPlan &S = pl.slots[i];
             if (S.mode != MODE_LUT) continue;
-            const size_t sz = 8 * (S.l1.size() + S.l2.size()) + 32;
+            const size_t sz = lut_bytes(S);
             tot += sz;
             if (sz > worst_sz) { worst_sz = sz; worst = (int)i; }
         }
         if (tot <= lut_budget || worst < 0) break;
         SlotPlan &S = pl.slots[worst];
-        // a coarser level 1 halves it; when level 2 dominates (dense breakpoints) coarsening
-        // does not help, so that column falls back to a binary search in global memory
-        if (s1[worst] >= 31 || S.l1.size() <= 64 || S.l2.size() > S.l1.size()) {
-            S.mode = MODE_SEARCH;
-            S.l1.clear();
-            S.l2.clear();
+        // a coarser level 1 roughly halves it; when level 2 / lists dominate (dense
+        // breakpoints) that column falls back to a binary search in global memory
+        if (s1[worst] >= 31 || S.l1.size() <= 64 || 8 * S.l2.size() + 4 * S.lst.size() > 8 * S.l1.size()) {
+            to_search(S);
             continue;
         }
-        build_lut(S, span_of(S), ++s1[worst]);
+        if (!build_lut(S, span_of(S), ++s1[worst])) to_search(S);
     }
 
-    // ---- layout: image [L1/L2 tables][group maps] | acc [hists][grids][direct] | hll
-    uint32_t u2 = 0;   // image cursor in uint2 units
+    // ---- layout: image [per slot: L1 | L2 | lists][group maps] | acc [hists][grids][direct] | hll
+    uint32_t w = 0;    // u32 cursor
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        S.lut_idx = u2;
-        u2 += (uint32_t)S.l1.size();
-        S.l2_idx = u2;
-        u2 += (uint32_t)S.l2.size();
+        w = (w + 1) & ~1u;
+        S.lut_idx = w / 2;
+        w += 2 * (uint32_t)S.l1.size();
+        S.l2_idx = w / 2;
+        w += 2 * (uint32_t)S.l2.size();
+        S.lst_idx = w;
+        w += (uint32_t)S.lst.size();
     }
-    uint32_t w = u2 * 2;   // u32 cursor
     w = (w + 3) & ~3u;
     for (auto &G : pl.groups) {
         if (G.direct) continue;
@@ -490,24 +527,23 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     pl.smem_bytes = (uint32_t)align16(pl.hll_off + pl.hll_bytes);
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
+    if (w > kBaseMask) return fail(GACE_EUNSUPPORTED, "probe plan too large for 24-bit bucket indices");
 
     // ---- fill the image (absolute shared-memory indices)
     pl.image.assign((size_t)image_words * 4, 0);
     uint2 *img2 = reinterpret_cast<uint2 *>(pl.image.data());
     uint32_t *img32 = reinterpret_cast<uint32_t *>(pl.image.data());
+    auto fix = [&](uint2 e, const SlotPlan &S) {
+        if (!(e.x & kSpecial)) { e.x += S.hist_idx; return e; }
+        if (e.x & kList) { e.x += S.hist_idx; e.y += S.lst_idx; return e; }
+        e.y += S.l2_idx;
+        return e;
+    };
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        for (size_t k = 0; k < S.l1.size(); ++k) {
-            uint2 e = S.l1[k];
-            if (e.x & kL2Flag) e.y += S.l2_idx;
-            else e.x += S.hist_idx;
-            img2[S.lut_idx + k] = e;
-        }
-        for (size_t k = 0; k < S.l2.size(); ++k) {
-            uint2 e = S.l2[k];
-            e.x += S.hist_idx;
-            img2[S.l2_idx + k] = e;
-        }
+        for (size_t k = 0; k < S.l1.size(); ++k) img2[S.lut_idx + k] = fix(S.l1[k], S);
+        for (size_t k = 0; k < S.l2.size(); ++k) img2[S.l2_idx + k] = fix(S.l2[k], S);
+        for (size_t k = 0; k < S.lst.size(); ++k) img32[S.lst_idx + k] = S.lst[k];
     }
     for (auto &G : pl.groups) {
         if (G.direct) continue;
@@ -1131,3 +1167,77 @@ gace_status gace_gate(const double *drift, uint32_t nd, const double *s_est, con
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- planner test hook
+
+namespace {
+struct CheckedTables {
+    const std::vector<uint8_t> *img;
+    mutable bool oob = false;
+    uint2 u2(uint32_t i) const {
+        if ((size_t)i * 8 + 8 > img->size()) { oob = true; return make_uint2(0, kNoThr); }
+        return reinterpret_cast<const uint2 *>(img->data())[i];
+    }
+    uint32_t u32(uint32_t i) const {
+        if ((size_t)i * 4 + 4 > img->size()) { oob = true; return 0; }
+        return reinterpret_cast<const uint32_t *>(img->data())[i];
+    }
+};
+}  // namespace
+
+extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
+                                          const int64_t *dhi, int host, const gace_pred *preds, uint32_t npreds,
+                                          const gace_pair *pairs, uint32_t npairs, uint64_t hll_mask, uint32_t col,
+                                          const int64_t *values, uint64_t n, uint32_t *out, uint32_t *mode,
+                                          int64_t *bps, uint32_t cap, uint32_t *nbp) {
+    if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS || col >= ncols || (n && (!values || !out)))
+        return fail(GACE_EINVAL, "bad arguments");
+    gace_table t;
+    t.ncols = ncols;
+    t.host = host != 0;
+    for (uint32_t c = 0; c < ncols; ++c) {
+        t.dtypes.push_back((int)dtypes[c]);
+        t.dlo.push_back(dlo[c]);
+        t.dhi.push_back(dhi[c]);
+    }
+    gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, 1.0, hll_mask, GACE_HLL_P);
+    if (st) return st;
+    Plan pl;
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    if (st) return st;
+    const int s = pl.col2slot[col];
+    if (s < 0 || !pl.slots[s].has_preds) return fail(GACE_EINVAL, "column has no predicates");
+    const SlotPlan &S = pl.slots[s];
+    const SlotParams &Q = pl.P.slot[s];
+    if (mode) *mode = Q.mode;
+    if (nbp) *nbp = (uint32_t)S.T.size();
+    for (uint32_t i = 0; bps && i < S.T.size() && i < cap; ++i) bps[i] = S.T[i];
+    // static layout checks: every map entry of every grid lands inside the accumulators
+    for (const Group &G : pl.groups) {
+        if (G.direct) continue;
+        const uint32_t *m32 = reinterpret_cast<const uint32_t *>(pl.image.data());
+        uint32_t ma = 0, mb = 0;
+        for (uint32_t r = 0; r < pl.slots[G.a].nb; ++r) ma = std::max(ma, m32[G.mapA_idx + r]);
+        for (uint32_t r = 0; r < pl.slots[G.b].nb; ++r) mb = std::max(mb, m32[G.mapB_idx + r]);
+        if (ma + mb >= pl.acc_idx + pl.acc_words) return fail(GACE_EUNSUPPORTED, "internal: grid map out of range");
+    }
+    CheckedTables M{&pl.image};
+    for (uint64_t k = 0; k < n; ++k) {
+        uint32_t b;
+        if (Q.mode == MODE_SEARCH) {
+            b = S.hist_idx + count_le(S.T, values[k]);
+        } else if (Q.dtype == GACE_I32) {
+            int32_t x = (int32_t)values[k];
+            if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
+            b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)x - (uint32_t)Q.base);
+        } else {
+            int64_t x = values[k];
+            if (pl.clamp) x = std::min(std::max(x, Q.clamp_lo), Q.clamp_hi);
+            b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
+        }
+        if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
+        if (b < S.hist_idx || b >= S.hist_idx + S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
+        out[k] = b - S.hist_idx;
+    }
+    return GACE_OK;
+}

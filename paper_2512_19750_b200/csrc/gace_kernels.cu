@@ -91,12 +91,14 @@ __device__ __forceinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n
     return lo;
 }
 
+struct SmemTables {
+    __device__ __forceinline__ uint2 u2(uint32_t i) const { return reinterpret_cast<const uint2 *>(g_smem)[i]; }
+    __device__ __forceinline__ uint32_t u32(uint32_t i) const { return reinterpret_cast<const uint32_t *>(g_smem)[i]; }
+};
+
 // Absolute shared-memory index of the histogram bucket of offset u.
 __device__ __forceinline__ uint32_t lut_bucket(const SlotParams &S, uint32_t u) {
-    const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
-    uint2 e = T[S.lut_idx + (u >> S.s1)];
-    if (e.x & kL2Flag) e = T[e.y + ((u & S.cell_mask) >> ((e.x >> 24) & 31u))];
-    return (e.x & kBaseMask) + (u > e.y ? 1u : 0u);
+    return lut_lookup(SmemTables{}, S.lut_idx, S.s1, u);
 }
 
 template <bool CLAMP>

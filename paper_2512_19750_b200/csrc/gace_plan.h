@@ -12,6 +12,7 @@
 // histogram over the sub-buckets of only the pair-relevant predicates (joints are
 // rectangle sums).  HLL registers live in shared memory as u8[4096] per column.
 #pragma once
+#include <cuda_runtime.h>   // uint2 / uint4
 #include <stdint.h>
 
 namespace gace {
@@ -22,15 +23,47 @@ constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
 constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM)
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
-constexpr uint32_t kL2Flag = 0x80000000u;
+constexpr uint32_t kSpecial = 0x80000000u;  // entry is a level-2 pointer or a list
+constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list
 constexpr uint32_t kBaseMask = 0x00FFFFFFu;
+constexpr uint32_t kListMax = 63;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+#if defined(__CUDACC__)
+#define GACE_HD __host__ __device__ __forceinline__
+#else
+#define GACE_HD inline
+#endif
+
+// Absolute bucket index of offset u.  `M` reads the table image: M.u2(i) / M.u32(i)
+// (shared memory in the kernel; a bounds-checked copy in gace_debug_buckets).
+template <class Mem>
+GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
+    uint32_t s = s1;
+    uint2 e = M.u2(lut_idx + (u >> s));
+    while ((e.x & (kSpecial | kList)) == kSpecial) {        // sub-cell block (nested)
+        const uint32_t sc = (e.x >> 24) & 63u;
+        e = M.u2(e.y + ((u & ((1u << s) - 1u)) >> sc));
+        s = sc;
+    }
+    if (e.x & kList) {
+        uint32_t b = e.x & kBaseMask;
+        const uint32_t n = (e.x >> 24) & 63u;
+        for (uint32_t i = 0; i < n; ++i) b += (u >= M.u32(e.y + i)) ? 1u : 0u;
+        return b;
+    }
+    return (e.x & kBaseMask) + (u > e.y ? 1u : 0u);
+}
 
 enum SlotMode : uint8_t { MODE_LUT = 0, MODE_SEARCH = 1, MODE_NOPRED = 2 };
 
-// LUT entry (8 bytes).  Direct entry: x = absolute u32 index of the cell's first
-// bucket in shared memory (bits 0..23), y = threshold: bucket += (u > y).
-// Level-2 pointer: x = kL2Flag | s2 << 24, y = index of the first L2 entry.
+// LUT entry (8 bytes), over the offset u = v - base of one column:
+//   direct : x = absolute u32 index of the cell's first bucket (bits 0..23),
+//            y = threshold, bucket = x + (u > y)        (at most one breakpoint in the cell)
+//   nested : x = kSpecial | sc << 24, y = uint2 index of a block of sub-cells of size
+//            2^sc; sub-entry = T2[y + ((u mod cell size) >> sc)] (any of the three kinds)
+//   list   : x = kSpecial | kList | n << 24 | first bucket, y = u32 index of n sorted
+//            breakpoint offsets t, bucket = first + #{t : u >= t}
 struct SlotParams {
     const void *ptr;        // device column base for this launch
     const int64_t *bps;     // MODE_SEARCH: sorted breakpoints (device)

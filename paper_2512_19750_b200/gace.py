@@ -34,7 +34,7 @@ PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
 EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
-           "gace_kernel_launches", "gace_last_error"]
+           "gace_debug_buckets", "gace_kernel_launches", "gace_last_error"]
 
 
 class GaceError(RuntimeError):
@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
     L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
     L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
     L.gace_nccl_unique_id.argtypes = [vp]
+    L.gace_debug_buckets.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, u32, vp, u64, vp,
+                                     ctypes.POINTER(u32), vp, u32, ctypes.POINTER(u32)]
     for f in EXPORTS:
         if f not in ("gace_kernel_launches", "gace_last_error"):
             getattr(L, f).restype = ctypes.c_int
@@ -113,6 +115,29 @@ def as_pairs(pairs) -> np.ndarray:
         return np.zeros(0, dtype=PAIR_DTYPE)
     a = np.ascontiguousarray(pairs)
     return a if a.dtype == PAIR_DTYPE else a.astype(PAIR_DTYPE)
+
+
+def debug_buckets(dtypes, dlo, dhi, host: bool, preds, pairs, hll_cols, col: int, values):
+    """Planner test hook (host only): bucket of each value of `col` through the planned
+    lookup table, using the kernel's lookup code.  Returns (buckets u32, mode, breakpoints)."""
+    P = as_preds(preds)
+    Q = as_pairs(pairs)
+    mask = 0
+    for c in hll_cols:
+        mask |= 1 << int(c)
+    n = len(dtypes)
+    dt = np.ascontiguousarray(dtypes, dtype=np.int32)
+    lo = np.ascontiguousarray(dlo, dtype=np.int64)
+    hi = np.ascontiguousarray(dhi, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    out = np.zeros(max(len(v), 1), dtype=np.uint32)
+    bps = np.zeros(2 * len(P) + 2, dtype=np.int64)
+    mode = ctypes.c_uint32()
+    nbp = ctypes.c_uint32()
+    _check(lib().gace_debug_buckets(n, dt.ctypes.data, lo.ctypes.data, hi.ctypes.data, int(host), _ptr(P), len(P),
+                                    _ptr(Q), len(Q), mask, col, _ptr(v), len(v), out.ctypes.data,
+                                    ctypes.byref(mode), bps.ctypes.data, len(bps), ctypes.byref(nbp)))
+    return out[:len(v)], int(mode.value), bps[:nbp.value]
 
 
 def kernel_launches() -> int:
