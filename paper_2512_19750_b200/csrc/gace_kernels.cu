@@ -116,8 +116,9 @@ __device__ __forceinline__ uint32_t bucket_i64(const SlotParams &S, int64_t x) {
 }
 
 // One column slot over one row quad: load, bucket, HLL, histogram.
-// FULL: all four rows valid and kept.  Otherwise `keep` has one bit per row and
-// rows past the end (k >= nvalid) are never loaded.
+// FULL: all four rows valid and kept.  Otherwise `keep` has one bit per row; rows
+// past the end (k >= nvalid) are never loaded -- they repeat row 0's key, so their
+// (unused) bucket lookups stay inside the column's value domain.
 template <bool CLAMP, bool FULL>
 __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint32_t nvalid,
                                           uint32_t keep, uint32_t (&bk)[4]) {
@@ -130,7 +131,7 @@ __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint3
             v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = (k < (int)nvalid) ? __ldg(p + k) : 0;
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(p + (k < (int)nvalid ? k : 0));   // pad with a real key
         }
         if (S.mode != MODE_NOPRED) {
 #pragma unroll
@@ -156,7 +157,8 @@ __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint3
             v[3] = (static_cast<int64_t>(t1.w) << 32) | static_cast<uint32_t>(t1.z);
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = (k < (int)nvalid) ? __ldg(reinterpret_cast<const long long *>(p) + k) : 0;
+            for (int k = 0; k < 4; ++k)   // pad with a real key: buckets of padding rows stay in range
+                v[k] = __ldg(reinterpret_cast<const long long *>(p) + (k < (int)nvalid ? k : 0));
         }
         if (S.mode != MODE_NOPRED) {
 #pragma unroll
