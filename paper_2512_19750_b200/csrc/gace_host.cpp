@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -222,7 +223,7 @@ struct SlotPlan {
     std::vector<uint2> l1, l2;         // entries with slot-relative indices (fixed up later)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
     // layout
-    uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_idx = 0, hll_off = kNone, bps_off = 0, pre = 0;
+    uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_idx = 0, hll_idx = kNone, bps_off = 0, pre = 0;
 };
 
 uint32_t ceil_log2(uint64_t x) {
@@ -378,7 +379,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     size_t fixed = 0;
     for (auto &S : pl.slots) {
         if (S.has_preds) fixed += 4ull * S.nb;
-        if (S.has_hll) fixed += kHllM;
+        if (S.has_hll) fixed += 4 * kHllM;
     }
     for (auto &G : pl.groups) {
         std::sort(G.TA.begin(), G.TA.end());
@@ -520,11 +521,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     uint32_t nh = 0;
     for (auto &S : pl.slots) {
         if (!S.has_hll) continue;
-        S.hll_off = pl.hll_off + nh * kHllM;
+        S.hll_idx = w + nh * kHllM;
         ++nh;
     }
     pl.hll_bytes = nh * kHllM;
-    pl.smem_bytes = (uint32_t)align16(pl.hll_off + pl.hll_bytes);
+    pl.smem_bytes = (uint32_t)align16(pl.hll_off + 4 * pl.hll_bytes);
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
     if (w > kBaseMask) return fail(GACE_EUNSUPPORTED, "probe plan too large for 24-bit bucket indices");
@@ -645,7 +646,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.dtype = (uint8_t)S.dtype;
         Q.mode = S.has_preds ? S.mode : (uint8_t)MODE_NOPRED;
         Q.has_hll = S.has_hll ? 1 : 0;
-        Q.hll_off = S.hll_off;
+        Q.hll_idx = S.hll_idx;
         Q.hist_idx = S.hist_idx;
         Q.base = S.base;
         Q.s1 = S.s1;
@@ -942,6 +943,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
+    if (const char *ab = getenv("GACE_ABLATE")) P.dbg = (uint32_t)strtoul(ab, nullptr, 0);   // design experiments only
     const bool sample = sample_rate < 1.0;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
     uint64_t bytes_per_row = 0;

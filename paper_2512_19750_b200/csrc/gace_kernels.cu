@@ -49,34 +49,40 @@ __device__ __forceinline__ int4 ld_stream(const void *p) {
 
 extern __shared__ uint4 g_smem[];
 
-// Raise register byte idx to r (registers only grow; updates are rare after warm-up).
-__device__ __forceinline__ void hll_raise(uint8_t *R, uint32_t idx, uint32_t r) {
-    uint32_t *w = reinterpret_cast<uint32_t *>(R + (idx & ~3u));
-    const uint32_t sh = (idx & 3u) * 8u;
-    uint32_t old = *reinterpret_cast<volatile uint32_t *>(w);
-    while (true) {
-        if (((old >> sh) & 0xFFu) >= r) return;
-        const uint32_t nw = (old & ~(0xFFu << sh)) | (r << sh);
-        const uint32_t prev = atomicCAS(w, old, nw);
-        if (prev == old) return;
-        old = prev;
-    }
+// HLL registers live in shared memory as u32 (native ATOMS.MAX; registers only grow).
+// `lmin` is a lower bound on every register of the column in this CTA (refreshed now
+// and then); a value with rank <= lmin cannot raise any register and skips the
+// shared-memory check entirely -- after warm-up that is nearly every value.
+__device__ __forceinline__ void hll_update(const SlotParams &S, uint32_t idx, uint32_t r, uint32_t lmin,
+                                           uint32_t dbg) {
+    if (r <= lmin) return;
+    uint32_t *R = reinterpret_cast<uint32_t *>(g_smem) + S.hll_idx;
+    if (r > R[idx] && !(dbg & 1)) atomicMax(R + idx, r);
 }
 
-__device__ __forceinline__ void hll_i32(const SlotParams &S, int32_t x) {
-    uint8_t *R = reinterpret_cast<uint8_t *>(g_smem) + S.hll_off;
+__device__ __forceinline__ void hll_i32(const SlotParams &S, int32_t x, uint32_t lmin, uint32_t dbg) {
     const uint32_t h = fmix32(static_cast<uint32_t>(x));
-    const uint32_t idx = h >> (32 - kHllP);
     const uint32_t r = __clz((h << kHllP) | (1u << (kHllP - 1))) + 1;   // <= 32-p+1
-    if (r > R[idx]) hll_raise(R, idx, r);
+    hll_update(S, h >> (32 - kHllP), r, lmin, dbg);
 }
 
-__device__ __forceinline__ void hll_i64(const SlotParams &S, int64_t x) {
-    uint8_t *R = reinterpret_cast<uint8_t *>(g_smem) + S.hll_off;
+__device__ __forceinline__ void hll_i64(const SlotParams &S, int64_t x, uint32_t lmin, uint32_t dbg) {
     const uint64_t h = mix64(static_cast<uint64_t>(x) + GACE_GAMMA);
-    const uint32_t idx = static_cast<uint32_t>(h >> (64 - kHllP));
     const uint32_t r = __clzll((h << kHllP) | (1ull << (kHllP - 1))) + 1;  // <= 64-p+1
-    if (r > R[idx]) hll_raise(R, idx, r);
+    hll_update(S, static_cast<uint32_t>(h >> (64 - kHllP)), r, lmin, dbg);
+}
+
+// Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
+__device__ __forceinline__ uint32_t hll_min(const SlotParams &S) {
+    const uint4 *R = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(g_smem) + S.hll_idx);
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t m = 0xFFFFFFFFu;
+#pragma unroll 8
+    for (int i = 0; i < kHllM / 4 / 32; ++i) {
+        const uint4 v = R[i * 32 + lane];
+        m = min(m, min(min(v.x, v.y), min(v.z, v.w)));
+    }
+    return __reduce_min_sync(0xFFFFFFFFu, m);
 }
 
 // #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback).
@@ -121,7 +127,7 @@ __device__ __forceinline__ uint32_t bucket_i64(const SlotParams &S, int64_t x) {
 // (unused) bucket lookups stay inside the column's value domain.
 template <bool CLAMP, bool FULL>
 __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint32_t nvalid,
-                                          uint32_t keep, uint32_t (&bk)[4]) {
+                                          uint32_t keep, uint32_t (&bk)[4], uint32_t lmin, uint32_t dbg) {
     uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
     if (S.dtype == 0) {
         int32_t v[4];
@@ -138,12 +144,12 @@ __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint3
             for (int k = 0; k < 4; ++k) bk[k] = bucket_i32<CLAMP>(S, v[k]);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[k], 1u);
+                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
         }
-        if (S.has_hll) {
+        if (S.has_hll && !(dbg & 8)) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) hll_i32(S, v[k]);
+                if (FULL || ((keep >> k) & 1u)) hll_i32(S, v[k], lmin, dbg);
         }
     } else {
         int64_t v[4];
@@ -165,12 +171,12 @@ __device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint3
             for (int k = 0; k < 4; ++k) bk[k] = bucket_i64<CLAMP>(S, v[k]);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[k], 1u);
+                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
         }
-        if (S.has_hll) {
+        if (S.has_hll && !(dbg & 8)) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) hll_i64(S, v[k]);
+                if (FULL || ((keep >> k) & 1u)) hll_i64(S, v[k], lmin, dbg);
         }
     }
 }
@@ -184,12 +190,13 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&bk)[NC][4], uint32_t s
 }
 
 template <int NC, bool CLAMP, bool FULL>
-__device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint32_t nvalid, uint32_t keep) {
+__device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint32_t nvalid, uint32_t keep,
+                                         const uint32_t (&lmin)[NC]) {
     uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
     uint32_t bk[NC][4];
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
-        if (s < (int)P.nslots) slot_quad<CLAMP, FULL>(P.slot[s], q, nvalid, keep, bk[s]);
+        if (s < (int)P.nslots) slot_quad<CLAMP, FULL>(P.slot[s], q, nvalid, keep, bk[s], lmin[s], P.dbg);
     }
     // joint counts: one 2-D grid bin per row and column pair (a, b)
 #pragma unroll
@@ -202,7 +209,7 @@ __device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint3
                 const int mb = P.grp[g].mapB_adj;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if (FULL || ((keep >> k) & 1u)) {
+                    if ((FULL || ((keep >> k) & 1u)) && !(P.dbg & 4)) {
                         const uint32_t ia = sm32[ma + (int)bk[a][k]];
                         const uint32_t ib = sm32[mb + (int)bk[b][k]];
                         atomicAdd(sm32 + ia + ib, 1u);
@@ -241,7 +248,19 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
     const uint64_t nq = (P.nrows + 3) / 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t kept = 0;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    uint32_t lmin[NC];
+#pragma unroll
+    for (int s = 0; s < NC; ++s) lmin[s] = 0;
+    uint32_t it = 0, next_refresh = 8;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride, ++it) {
+        if (it == next_refresh) {
+            next_refresh = it + min(it, 256u);
+            if (__activemask() == 0xFFFFFFFFu) {
+#pragma unroll
+                for (int s = 0; s < NC; ++s)
+                    if (s < (int)P.nslots && P.slot[s].has_hll) lmin[s] = hll_min(P.slot[s]);
+            }
+        }
         const uint64_t rem = P.nrows - q * 4;
         const uint32_t nvalid = rem >= 4 ? 4u : (uint32_t)rem;
         uint32_t keep = (1u << nvalid) - 1u;
@@ -256,8 +275,8 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
             if (keep == 0) continue;
         }
         kept += __popc(keep);
-        if (keep == 0xFu) row_quad<NC, CLAMP, true>(P, q, 4, keep);
-        else row_quad<NC, CLAMP, false>(P, q, nvalid, keep);
+        if (keep == 0xFu) row_quad<NC, CLAMP, true>(P, q, 4, keep, lmin);
+        else row_quad<NC, CLAMP, false>(P, q, nvalid, keep, lmin);
     }
     __syncthreads();
 
@@ -266,16 +285,13 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
         const uint32_t v = sm32[P.acc_idx + i];
         if (v) atomicAdd(P.g_acc + i, (unsigned long long)v);
     }
-    if (P.hll_bytes) {
+    if (P.hll_bytes) {   // u32 registers -> packed u8 partial of this CTA
         const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(g_smem) + P.hll_off);
-        uint4 *dst = reinterpret_cast<uint4 *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes);
-        for (uint32_t i = threadIdx.x; i < P.hll_bytes / 16; i += blockDim.x) {
-            uint4 v = src[i];
-            if (P.part_merge) {      // later launch of a chunked probe: max-merge into the partial
-                const uint4 o = dst[i];
-                v.x = __vmaxu4(v.x, o.x); v.y = __vmaxu4(v.y, o.y);
-                v.z = __vmaxu4(v.z, o.z); v.w = __vmaxu4(v.w, o.w);
-            }
+        uint32_t *dst = reinterpret_cast<uint32_t *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes);
+        for (uint32_t i = threadIdx.x; i < P.hll_bytes / 4; i += blockDim.x) {
+            const uint4 r = src[i];
+            uint32_t v = r.x | (r.y << 8) | (r.z << 16) | (r.w << 24);
+            if (P.part_merge) v = __vmaxu4(v, dst[i]);   // later launch of a chunked probe
             dst[i] = v;
         }
     }

@@ -76,7 +76,7 @@ struct SlotParams {
     uint32_t lut_idx;       // level-1 table: uint2 index into shared memory
     uint32_t l2_idx;        // level-2 table: uint2 index into shared memory
     uint32_t hist_idx;      // u32 index of bucket 0 of this column's histogram
-    uint32_t hll_off;       // byte offset of this column's u8[4096] registers, or kNone
+    uint32_t hll_idx;       // u32 index of this column's u32[4096] HLL registers, or kNone
     uint8_t dtype;          // 0 = int32, 1 = int64
     uint8_t mode;           // SlotMode
     uint8_t has_hll;
@@ -109,8 +109,8 @@ struct ProbeParams {
     uint32_t image_u4;                     // image size in 16-byte units
     uint32_t acc_idx;                      // u32 index where the zeroed accumulators start
     uint32_t acc_words;                    // number of u32 accumulators
-    uint32_t hll_off;                      // byte offset of the HLL register block
-    uint32_t hll_bytes;                    // nh * 4096
+    uint32_t hll_off;                      // byte offset of the u32 HLL register block (nh * 4096 u32)
+    uint32_t hll_bytes;                    // nh * 4096: bytes of the packed u8 registers output
     uint32_t smem_bytes;                   // total dynamic shared memory
     unsigned long long *g_acc;             // u64[acc_words], summed over CTAs (and launches)
     uint8_t *g_hll_part;                   // [part_slot][hll_bytes] per-CTA register partials
@@ -121,6 +121,8 @@ struct ProbeParams {
     uint64_t seed;
     uint32_t sample_all;                   // rate == 1
     uint32_t part_merge;                   // 1: max-merge into existing per-CTA partials (later chunk launches)
+    uint32_t dbg;                          // ablation bits (env GACE_ABLATE; 0 in production):
+                                           // 1 no HLL raise, 2 no histogram adds, 4 no grid adds, 8 no HLL
 };
 
 // ---------------------------------------------------------------- finalize
