@@ -389,7 +389,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         G.na = (uint32_t)G.TA.size() + 1;
         G.nbb = (uint32_t)G.TB.size() + 1;
     }
-    // grids in increasing size while they fit half the budget; the rest evaluate per row
+    // grids in increasing size while they fit (keeping 4 KB per column with predicates for
+    // its lookup table); the groups left over are evaluated per row ("direct")
+    size_t lut_reserve = 0;
+    for (auto &S : pl.slots) lut_reserve += S.has_preds ? 4096 : 0;
     {
         std::vector<int> order(pl.groups.size());
         for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
@@ -400,7 +403,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         for (int gi : order) {
             Group &G = pl.groups[gi];
             const size_t need = 4ull * ((uint64_t)G.na * G.nbb + pl.slots[G.a].nb + pl.slots[G.b].nb) + 64;
-            if (fixed + used + need <= kSmemBudget / 2) used += need;
+            if (fixed + used + need + lut_reserve <= kSmemBudget) used += need;
             else G.direct = true;
         }
         fixed += used;
@@ -585,7 +588,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         F.neg = (preds[p].flags & GACE_PRED_NEGATE) ? 1 : 0;
         pl.fpreds[p] = F;
     }
-    uint32_t dcur = 0;
+    struct DEnt { uint32_t g, q; DirectPair D; };
+    std::vector<DEnt> dlist;
     for (uint32_t q = 0; q < nq; ++q) {
         const uint32_t i = pairs[q].i, j = pairs[q].j;
         const int si = pl.pslot[i], sj = pl.pslot[j];
@@ -611,15 +615,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                 bucket_iv(pb, pl.slots[G.b].T, lo, hi);
                 D.lb = lo + pl.slots[G.b].hist_idx;
                 D.hb = hi + pl.slots[G.b].hist_idx;
-                D.sa = (uint8_t)G.a;
-                D.sb = (uint8_t)G.b;
-                D.nega = (uint8_t)na_;
-                D.negb = (uint8_t)nb_;
-                D.acc_idx = direct_idx + dcur;
-                pl.direct.push_back(D);
+                D.nega = na_;
+                D.negb = nb_;
+                dlist.push_back({(uint32_t)pl.gidx[std::make_pair(G.a, G.b)], q, D});
                 F.kind = PAIR_DIRECT;
-                F.pre = direct_idx + dcur - pl.acc_idx;
-                ++dcur;
             } else {
                 F.kind = PAIR_GRID;
                 F.pre = G.sat;
@@ -632,6 +631,17 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             }
         }
         pl.fpairs[q] = F;
+    }
+    // direct pairs grouped by column pair; each counter's slot = its position
+    std::stable_sort(dlist.begin(), dlist.end(), [](const DEnt &x, const DEnt &y) { return x.g < y.g; });
+    std::vector<uint32_t> dbeg(pl.groups.size(), 0), dend(pl.groups.size(), 0);
+    for (uint32_t k = 0; k < dlist.size(); ++k) {
+        DEnt &E = dlist[k];
+        E.D.acc_idx = direct_idx + k;
+        pl.fpairs[E.q].pre = direct_idx + k - pl.acc_idx;
+        if (dend[E.g] == 0) dbeg[E.g] = k;
+        dend[E.g] = k + 1;
+        pl.direct.push_back(E.D);
     }
 
     // ---- kernel parameters (pointers filled in at launch)
@@ -669,11 +679,15 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     }
     for (size_t g = 0; g < pl.groups.size(); ++g) {
         const Group &G = pl.groups[g];
-        if (G.direct) continue;
         P.grp[g].a = (uint8_t)G.a;
         P.grp[g].b = (uint8_t)G.b;
-        P.grp[g].mapA_adj = (int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx;
-        P.grp[g].mapB_adj = (int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx;
+        P.grp[g].dbeg = (uint16_t)dbeg[g];
+        P.grp[g].dend = (uint16_t)dend[g];
+        P.grp[g].has_grid = G.direct ? 0 : 1;
+        if (!G.direct) {
+            P.grp[g].mapA_adj = (int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx;
+            P.grp[g].mapB_adj = (int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx;
+        }
         P.combo[G.a * kMaxSlots + G.b] = (int8_t)g;
     }
     P.ndirect = (uint32_t)pl.direct.size();
@@ -945,6 +959,9 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
     if (const char *ab = getenv("GACE_ABLATE")) P.dbg = (uint32_t)strtoul(ab, nullptr, 0);   // design experiments only
     const bool sample = sample_rate < 1.0;
+    P.clamp = pl.clamp ? 1u : 0u;
+    bool i64 = false;
+    for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
     uint64_t bytes_per_row = 0;
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
@@ -965,7 +982,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
             P.nrows = n;
             P.row0 = row_offset + r0;
             P.part_merge = launches ? 1u : 0u;
-            CUDA_TRY(launch_probe(P, pl.clamp, sample, grid, s));
+            CUDA_TRY(launch_probe(P, sample, i64, grid, s));
             ++launches;
         }
     } else {
@@ -997,7 +1014,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
             P.nrows = n;
             P.row0 = row_offset + r0;
             P.part_merge = launches ? 1u : 0u;
-            CUDA_TRY(launch_probe(P, pl.clamp, sample, grid, s));
+            CUDA_TRY(launch_probe(P, sample, i64, grid, s));
             ++launches;
             CUDA_TRY(cudaEventRecord(t->ev_free[b], s));
         }

@@ -107,106 +107,111 @@ __device__ __forceinline__ uint32_t lut_bucket(const SlotParams &S, uint32_t u) 
     return lut_lookup(SmemTables{}, S.lut_idx, S.s1, u);
 }
 
-template <bool CLAMP>
-__device__ __forceinline__ uint32_t bucket_i32(const SlotParams &S, int32_t x) {
+__device__ __forceinline__ uint32_t bucket_i32(const SlotParams &S, int32_t x, bool clamp) {
     if (S.mode == MODE_SEARCH) return S.hist_idx + search_bucket(S.bps, S.nbp, x);
-    if (CLAMP) x = min(max(x, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
+    if (clamp) x = min(max(x, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
     return lut_bucket(S, static_cast<uint32_t>(x) - static_cast<uint32_t>(S.base));
 }
 
-template <bool CLAMP>
-__device__ __forceinline__ uint32_t bucket_i64(const SlotParams &S, int64_t x) {
+__device__ __forceinline__ uint32_t bucket_i64(const SlotParams &S, int64_t x, bool clamp) {
     if (S.mode == MODE_SEARCH) return S.hist_idx + search_bucket(S.bps, S.nbp, x);
-    if (CLAMP) x = min(max(x, S.clamp_lo), S.clamp_hi);
+    if (clamp) x = min(max(x, S.clamp_lo), S.clamp_hi);
     return lut_bucket(S, static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base)));
 }
 
-// One column slot over one row quad: load, bucket, HLL, histogram.
-// FULL: all four rows valid and kept.  Otherwise `keep` has one bit per row; rows
-// past the end (k >= nvalid) are never loaded -- they repeat row 0's key, so their
-// (unused) bucket lookups stay inside the column's value domain.
-template <bool CLAMP, bool FULL>
-__device__ __forceinline__ void slot_quad(const SlotParams &S, uint64_t q, uint32_t nvalid,
-                                          uint32_t keep, uint32_t (&bk)[4], uint32_t lmin, uint32_t dbg) {
-    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
-    if (S.dtype == 0) {
-        int32_t v[4];
-        const int32_t *p = static_cast<const int32_t *>(S.ptr) + q * 4;
-        if (FULL || nvalid == 4) {
-            const int4 t = ld_stream(p);
-            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = __ldg(p + (k < (int)nvalid ? k : 0));   // pad with a real key
-        }
-        if (S.mode != MODE_NOPRED) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bk[k] = bucket_i32<CLAMP>(S, v[k]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
-        }
-        if (S.has_hll && !(dbg & 8)) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) hll_i32(S, v[k], lmin, dbg);
-        }
-    } else {
-        int64_t v[4];
-        const int64_t *p = static_cast<const int64_t *>(S.ptr) + q * 4;
-        if (FULL || nvalid == 4) {
-            const int4 t0 = ld_stream(p);
-            const int4 t1 = ld_stream(p + 2);
-            v[0] = (static_cast<int64_t>(t0.y) << 32) | static_cast<uint32_t>(t0.x);
-            v[1] = (static_cast<int64_t>(t0.w) << 32) | static_cast<uint32_t>(t0.z);
-            v[2] = (static_cast<int64_t>(t1.y) << 32) | static_cast<uint32_t>(t1.x);
-            v[3] = (static_cast<int64_t>(t1.w) << 32) | static_cast<uint32_t>(t1.z);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)   // pad with a real key: buckets of padding rows stay in range
-                v[k] = __ldg(reinterpret_cast<const long long *>(p) + (k < (int)nvalid ? k : 0));
-        }
-        if (S.mode != MODE_NOPRED) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bk[k] = bucket_i64<CLAMP>(S, v[k]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
-        }
-        if (S.has_hll && !(dbg & 8)) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (FULL || ((keep >> k) & 1u)) hll_i64(S, v[k], lmin, dbg);
-        }
-    }
+__device__ __forceinline__ bool keep_row(const ProbeParams &P, uint64_t g) {
+    return mix64(P.seed + (g + 1) * GACE_GAMMA) < P.thr;
 }
 
-template <int NC>
-__device__ __forceinline__ uint32_t pick(const uint32_t (&bk)[NC][4], uint32_t s, int k) {
-    uint32_t r = bk[0][k];
-#pragma unroll
-    for (int c = 1; c < NC; ++c) r = (s == (uint32_t)c) ? bk[c][k] : r;
-    return r;
-}
+// Register-resident 16-byte chunks of one "unit" (U row quads) of every slot: the
+// main loop prefetches the next unit's chunks while it processes this one.
+template <int NC, int U, bool I64>
+struct Unit {
+    int4 r[NC][U][I64 ? 2 : 1];
+};
 
-template <int NC, bool CLAMP, bool FULL>
-__device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint32_t nvalid, uint32_t keep,
-                                         const uint32_t (&lmin)[NC]) {
-    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
-    uint32_t bk[NC][4];
+template <int NC, int U, bool I64>
+__device__ __forceinline__ void load_unit(const ProbeParams &P, uint64_t u, Unit<NC, U, I64> &X) {
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
-        if (s < (int)P.nslots) slot_quad<CLAMP, FULL>(P.slot[s], q, nvalid, keep, bk[s], lmin[s], P.dbg);
+        if (s >= (int)P.nslots) continue;
+        const char *base = static_cast<const char *>(P.slot[s].ptr);
+        if (!I64 || P.slot[s].dtype == 0) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) X.r[s][j][0] = ld_stream(base + (u * U + j) * 16);
+        } else {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                X.r[s][j][0] = ld_stream(base + (u * U + j) * 32);
+                X.r[s][j][I64 ? 1 : 0] = ld_stream(base + (u * U + j) * 32 + 16);
+            }
+        }
     }
-    // joint counts: one 2-D grid bin per row and column pair (a, b)
+}
+
+// One slot over one row quad whose keys are in registers: bucket, histogram, HLL.
+// keep: one bit per row (0xF when all four rows are kept).
+template <bool I64, bool FULL>
+__device__ __forceinline__ void slot_quad(const ProbeParams &P, const SlotParams &S, const int4 (&r)[I64 ? 2 : 1],
+                                          uint32_t keep, uint32_t (&bk)[4], uint32_t lmin) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    const bool clamp = P.clamp;
+    const uint32_t dbg = P.dbg;
+    if (!I64 || S.dtype == 0) {
+        const int32_t v[4] = {r[0].x, r[0].y, r[0].z, r[0].w};
+        if (S.mode != MODE_NOPRED) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk[k] = bucket_i32(S, v[k], clamp);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
+        }
+        if (S.has_hll && !(dbg & 8)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // a key equal to the previous kept row's key cannot change a register
+                const bool dup = FULL && k > 0 && v[k] == v[k - 1];
+                if ((FULL || ((keep >> k) & 1u)) && !dup) hll_i32(S, v[k], lmin, dbg);
+            }
+        }
+    } else {
+        const int64_t v[4] = {
+            (static_cast<int64_t>(r[0].y) << 32) | static_cast<uint32_t>(r[0].x),
+            (static_cast<int64_t>(r[0].w) << 32) | static_cast<uint32_t>(r[0].z),
+            (static_cast<int64_t>(r[I64 ? 1 : 0].y) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].x),
+            (static_cast<int64_t>(r[I64 ? 1 : 0].w) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].z)};
+        if (S.mode != MODE_NOPRED) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk[k] = bucket_i64(S, v[k], clamp);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
+        }
+        if (S.has_hll && !(dbg & 8)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool dup = FULL && k > 0 && v[k] == v[k - 1];
+                if ((FULL || ((keep >> k) & 1u)) && !dup) hll_i64(S, v[k], lmin, dbg);
+            }
+        }
+    }
+}
+
+// Pair counts of one row quad: one 2-D grid bin per row and column pair (a, b), and
+// per-row evaluation of the pairs of column pairs whose grid did not fit ("direct").
+template <int NC, bool FULL>
+__device__ __forceinline__ void pairs_quad(const ProbeParams &P, const uint32_t (&bk)[NC][4], uint32_t keep) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
 #pragma unroll
     for (int a = 0; a < NC; ++a) {
 #pragma unroll
         for (int b = a + 1; b < NC; ++b) {
             const int g = P.combo[a * kMaxSlots + b];
-            if (g >= 0) {
-                const int ma = P.grp[g].mapA_adj;
-                const int mb = P.grp[g].mapB_adj;
+            if (g < 0) continue;
+            const GroupParams &G = P.grp[g];
+            if (G.has_grid) {
+                const int ma = G.mapA_adj;
+                const int mb = G.mapB_adj;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if ((FULL || ((keep >> k) & 1u)) && !(P.dbg & 4)) {
@@ -216,28 +221,43 @@ __device__ __forceinline__ void row_quad(const ProbeParams &P, uint64_t q, uint3
                     }
                 }
             }
-        }
-    }
-    // fallback: cross-column pairs whose grid did not fit, evaluated per row
-    for (uint32_t d = 0; d < P.ndirect; ++d) {
-        const DirectPair D = P.direct[d];
-        uint32_t c = 0;
+            for (uint32_t d = G.dbeg; d < G.dend; ++d) {
+                const DirectPair D = P.direct[d];
+                uint32_t c = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t ba = pick<NC>(bk, D.sa, k);
-            const uint32_t bb = pick<NC>(bk, D.sb, k);
-            const uint32_t ina = ((ba >= D.la) & (ba <= D.ha)) ^ D.nega;
-            const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
-            c += ((keep >> k) & 1u) & ina & inb;
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t ina = ((bk[a][k] >= D.la) & (bk[a][k] <= D.ha)) ^ D.nega;
+                    const uint32_t inb = ((bk[b][k] >= D.lb) & (bk[b][k] <= D.hb)) ^ D.negb;
+                    c += ((keep >> k) & 1u) & ina & inb;
+                }
+                const uint32_t m = __activemask();
+                const uint32_t tot = __reduce_add_sync(m, c);
+                if ((threadIdx.x & 31) == (uint32_t)(__ffs(m) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
+            }
         }
-        const uint32_t m = __activemask();
-        const uint32_t tot = __reduce_add_sync(m, c);
-        if ((threadIdx.x & 31) == (uint32_t)(__ffs(m) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
     }
 }
 
-template <int NC, bool CLAMP, bool SAMPLE>
+template <int NC, bool I64, bool FULL>
+__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[NC][I64 ? 2 : 1], uint32_t keep,
+                                          const uint32_t (&lmin)[NC]) {
+    uint32_t bk[NC][4];
+#pragma unroll
+    for (int s = 0; s < NC; ++s)
+        if (s < (int)P.nslots) slot_quad<I64, FULL>(P, P.slot[s], r[s], keep, bk[s], lmin[s]);
+    pairs_quad<NC, FULL>(P, bk, keep);
+}
+
+// Rows per thread per loop iteration: 4 * U, U chosen so each thread keeps >= 64 bytes
+// of every column in flight (plus the same again prefetched).
+template <int NC>
+struct Cfg {
+    static constexpr int U = NC >= 4 ? 1 : 4 / NC;
+};
+
+template <int NC, bool SAMPLE, bool I64>
 __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constant__ ProbeParams P) {
+    constexpr int U = Cfg<NC>::U;
     uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
     // tables -> shared memory; accumulators and registers -> 0
     for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) g_smem[i] = __ldg(P.image + i);
@@ -245,38 +265,72 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
         g_smem[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
 
-    const uint64_t nq = (P.nrows + 3) / 4;
+    const uint64_t nunits = P.nrows / (4 * U);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t kept = 0;
     uint32_t lmin[NC];
 #pragma unroll
     for (int s = 0; s < NC; ++s) lmin[s] = 0;
-    uint32_t it = 0, next_refresh = 8;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride, ++it) {
+    uint32_t it = 0, next_refresh = 4;
+    uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Unit<NC, U, I64> X;
+    if (u < nunits) load_unit(P, u, X);
+    for (; u < nunits; u += stride, ++it) {
+        Unit<NC, U, I64> Xn;
+        if (u + stride < nunits) load_unit(P, u + stride, Xn);           // prefetch
         if (it == next_refresh) {
-            next_refresh = it + min(it, 256u);
+            next_refresh = it + min(it, 128u);
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
                     if (s < (int)P.nslots && P.slot[s].has_hll) lmin[s] = hll_min(P.slot[s]);
             }
         }
-        const uint64_t rem = P.nrows - q * 4;
-        const uint32_t nvalid = rem >= 4 ? 4u : (uint32_t)rem;
-        uint32_t keep = (1u << nvalid) - 1u;
-        if (SAMPLE) {
-            uint32_t m = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t g = P.row0 + q * 4 + k;
-                m |= (mix64(P.seed + (g + 1) * GACE_GAMMA) < P.thr ? 1u : 0u) << k;
+        for (int j = 0; j < U; ++j) {
+            uint32_t keep = 0xFu;
+            if (SAMPLE) {
+                const uint64_t g0 = P.row0 + (u * U + j) * 4;
+                keep = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) keep |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
             }
-            keep &= m;
-            if (keep == 0) continue;
+            int4 rj[NC][I64 ? 2 : 1];
+#pragma unroll
+            for (int s = 0; s < NC; ++s) {
+                rj[s][0] = X.r[s][j][0];
+                if (I64) rj[s][I64 ? 1 : 0] = X.r[s][j][I64 ? 1 : 0];
+            }
+            kept += __popc(keep);
+            if (keep == 0xFu) quad_work<NC, I64, true>(P, rj, keep, lmin);
+            else if (keep) quad_work<NC, I64, false>(P, rj, keep, lmin);
         }
-        kept += __popc(keep);
-        if (keep == 0xFu) row_quad<NC, CLAMP, true>(P, q, 4, keep, lmin);
-        else row_quad<NC, CLAMP, false>(P, q, nvalid, keep, lmin);
+        X = Xn;
+    }
+    // tail rows [nunits * 4U, nrows): one row per thread of the last CTA, scalar loads
+    const uint64_t tail0 = nunits * 4 * U;
+    if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < P.nrows) {
+        const uint64_t r = tail0 + threadIdx.x;
+        const uint32_t keep = (!SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
+        int4 rj[NC][I64 ? 2 : 1];
+#pragma unroll
+        for (int s = 0; s < NC; ++s) {
+            if (s >= (int)P.nslots) continue;
+            if (!I64 || P.slot[s].dtype == 0) {
+                const int32_t x = __ldg(static_cast<const int32_t *>(P.slot[s].ptr) + r);
+                rj[s][0] = make_int4(x, x, x, x);     // rows 1..3 of the quad are masked off
+            } else {
+                const long long x = __ldg(static_cast<const long long *>(P.slot[s].ptr) + r);
+                const int lo = (int)(x & 0xFFFFFFFF), hi = (int)(x >> 32);
+                rj[s][0] = make_int4(lo, hi, lo, hi);
+                rj[s][I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
+            }
+        }
+        kept += keep;
+        uint32_t zero[NC];
+#pragma unroll
+        for (int s = 0; s < NC; ++s) zero[s] = 0;
+        if (keep) quad_work<NC, I64, false>(P, rj, 1u, zero);
     }
     __syncthreads();
 
@@ -470,9 +524,9 @@ __global__ void sample_mask_kernel(uint64_t nrows, uint64_t row0, uint64_t seed,
 
 // ------------------------------------------------------------------ launchers
 
-template <int NC, bool CLAMP, bool SAMPLE>
+template <int NC, bool SAMPLE, bool I64>
 static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
-    auto k = probe_kernel<NC, CLAMP, SAMPLE>;
+    auto k = probe_kernel<NC, SAMPLE, I64>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
@@ -484,17 +538,17 @@ static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
 }
 
 template <int NC>
-static cudaError_t launch_nc(const ProbeParams &P, bool clamp, bool sample, int grid, cudaStream_t s) {
-    if (clamp) return sample ? launch_t<NC, true, true>(P, grid, s) : launch_t<NC, true, false>(P, grid, s);
-    return sample ? launch_t<NC, false, true>(P, grid, s) : launch_t<NC, false, false>(P, grid, s);
+static cudaError_t launch_nc(const ProbeParams &P, bool sample, bool i64, int grid, cudaStream_t s) {
+    if (i64) return sample ? launch_t<NC, true, true>(P, grid, s) : launch_t<NC, false, true>(P, grid, s);
+    return sample ? launch_t<NC, true, false>(P, grid, s) : launch_t<NC, false, false>(P, grid, s);
 }
 
-cudaError_t launch_probe(const ProbeParams &P, bool clamp, bool sample, int grid, cudaStream_t s) {
+cudaError_t launch_probe(const ProbeParams &P, bool sample, bool i64, int grid, cudaStream_t s) {
     const uint32_t n = P.nslots;
-    if (n <= 1) return launch_nc<1>(P, clamp, sample, grid, s);
-    if (n <= 2) return launch_nc<2>(P, clamp, sample, grid, s);
-    if (n <= 4) return launch_nc<4>(P, clamp, sample, grid, s);
-    return launch_nc<8>(P, clamp, sample, grid, s);
+    if (n <= 1) return launch_nc<1>(P, sample, i64, grid, s);
+    if (n <= 2) return launch_nc<2>(P, sample, i64, grid, s);
+    if (n <= 4) return launch_nc<4>(P, sample, i64, grid, s);
+    return launch_nc<8>(P, sample, i64, grid, s);
 }
 
 cudaError_t launch_finalize(const FinParams &F, cudaStream_t s) {
@@ -522,16 +576,6 @@ cudaError_t launch_sample_mask(uint64_t nrows, uint64_t row0, uint64_t seed, uin
     if (!words) return cudaSuccess;
     sample_mask_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(nrows, row0, seed, thr, all, bits);
     return cudaGetLastError();
-}
-
-int probe_kernel_regs(int nc, bool clamp, bool sample) {
-    cudaFuncAttributes a;
-    cudaError_t e;
-    if (nc <= 4) e = cudaFuncGetAttributes(&a, clamp ? (sample ? probe_kernel<4, true, true> : probe_kernel<4, true, false>)
-                                                      : (sample ? probe_kernel<4, false, true> : probe_kernel<4, false, false>));
-    else e = cudaFuncGetAttributes(&a, clamp ? (sample ? probe_kernel<8, true, true> : probe_kernel<8, true, false>)
-                                             : (sample ? probe_kernel<8, false, true> : probe_kernel<8, false, false>));
-    return e == cudaSuccess ? a.numRegs : -1;
 }
 
 }  // namespace gace

@@ -21,7 +21,7 @@ constexpr int kMaxSlots = 8;           // GACE_MAX_PROBED_COLS
 constexpr int kMaxGroups = 28;         // unordered slot pairs
 constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
-constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM)
+constexpr int kThreads = 512;          // probe CTA size (one CTA per SM, <= 128 registers)
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
 constexpr uint32_t kSpecial = 0x80000000u;  // entry is a level-2 pointer or a list
 constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list
@@ -86,15 +86,17 @@ struct SlotParams {
 struct GroupParams {
     int32_t mapA_adj;       // u32 index of mapA minus hist_idx of slot a (indexed by absolute bucket)
     int32_t mapB_adj;
+    uint16_t dbeg, dend;    // this column pair's per-row ("direct") pairs: direct[dbeg .. dend)
     uint8_t a, b;           // slots, a < b
-    uint8_t pad[2];
+    uint8_t has_grid;       // 2-D grid in shared memory (else all its pairs are direct)
+    uint8_t pad;
 };
 
 // Cross-column pair evaluated per row (fallback when a group's 2-D grid does not fit).
 struct DirectPair {
-    uint32_t la, ha;        // absolute bucket interval of predicate on slot sa (la > ha: empty)
-    uint32_t lb, hb;
-    uint8_t sa, sb, nega, negb;
+    uint32_t la, ha;        // absolute bucket interval of the predicate on slot a (la > ha: empty)
+    uint32_t lb, hb;        // ... on slot b
+    uint32_t nega, negb;
     uint32_t acc_idx;       // u32 index of its counter in shared memory
 };
 
@@ -121,6 +123,7 @@ struct ProbeParams {
     uint64_t seed;
     uint32_t sample_all;                   // rate == 1
     uint32_t part_merge;                   // 1: max-merge into existing per-CTA partials (later chunk launches)
+    uint32_t clamp;                        // clamp keys into each slot's [clamp_lo, clamp_hi]
     uint32_t dbg;                          // ablation bits (env GACE_ABLATE; 0 in production):
                                            // 1 no HLL raise, 2 no histogram adds, 4 no grid adds, 8 no HLL
 };
