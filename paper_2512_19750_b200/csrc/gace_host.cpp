@@ -454,7 +454,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
         uint64_t target = 64;
-        while (target < 4096 && target < 16ull * S.T.size()) target <<= 1;
+        while (target < 4096 && target < 32ull * S.T.size()) target <<= 1;
         const uint64_t span = span_of(S);
         uint32_t sh = 0;
         while (sh < 31 && (span >> sh) + 1 > target) ++sh;

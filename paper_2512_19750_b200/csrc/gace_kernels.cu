@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "gace_kernels.h"
 #include "gace_plan.h"
 
@@ -149,50 +151,80 @@ __device__ __forceinline__ void load_unit(const ProbeParams &P, uint64_t u, Unit
     }
 }
 
-// One slot over one row quad whose keys are in registers: bucket, histogram, HLL.
-// keep: one bit per row (0xF when all four rows are kept).
-template <bool I64, bool FULL>
-__device__ __forceinline__ void slot_quad(const ProbeParams &P, const SlotParams &S, const int4 (&r)[I64 ? 2 : 1],
-                                          uint32_t keep, uint32_t (&bk)[4], uint32_t lmin) {
-    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
-    const bool clamp = P.clamp;
-    const uint32_t dbg = P.dbg;
+// Keys of one slot's row quad: int64 only in kernels that have an int64 column.
+template <bool I64>
+using KeyT = typename std::conditional<I64, int64_t, int32_t>::type;
+
+template <bool I64>
+__device__ __forceinline__ void decode(const SlotParams &S, const int4 (&r)[I64 ? 2 : 1], KeyT<I64> (&v)[4]) {
     if (!I64 || S.dtype == 0) {
-        const int32_t v[4] = {r[0].x, r[0].y, r[0].z, r[0].w};
-        if (S.mode != MODE_NOPRED) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bk[k] = bucket_i32(S, v[k], clamp);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
-        }
-        if (S.has_hll && !(dbg & 8)) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                // a key equal to the previous kept row's key cannot change a register
-                const bool dup = FULL && k > 0 && v[k] == v[k - 1];
-                if ((FULL || ((keep >> k) & 1u)) && !dup) hll_i32(S, v[k], lmin, dbg);
-            }
-        }
+        v[0] = r[0].x; v[1] = r[0].y; v[2] = r[0].z; v[3] = r[0].w;
     } else {
-        const int64_t v[4] = {
-            (static_cast<int64_t>(r[0].y) << 32) | static_cast<uint32_t>(r[0].x),
-            (static_cast<int64_t>(r[0].w) << 32) | static_cast<uint32_t>(r[0].z),
-            (static_cast<int64_t>(r[I64 ? 1 : 0].y) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].x),
-            (static_cast<int64_t>(r[I64 ? 1 : 0].w) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].z)};
-        if (S.mode != MODE_NOPRED) {
+        v[0] = static_cast<KeyT<I64>>((static_cast<int64_t>(r[0].y) << 32) | static_cast<uint32_t>(r[0].x));
+        v[1] = static_cast<KeyT<I64>>((static_cast<int64_t>(r[0].w) << 32) | static_cast<uint32_t>(r[0].z));
+        v[2] = static_cast<KeyT<I64>>((static_cast<int64_t>(r[I64 ? 1 : 0].y) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].x));
+        v[3] = static_cast<KeyT<I64>>((static_cast<int64_t>(r[I64 ? 1 : 0].w) << 32) | static_cast<uint32_t>(r[I64 ? 1 : 0].z));
+    }
+}
+
+// Offset u = key - base of a LUT-mode slot (with the optional clamp), 32-bit ops for int32.
+template <bool I64>
+__device__ __forceinline__ uint32_t offset_of(const SlotParams &S, KeyT<I64> xk, bool clamp) {
+    int64_t x = xk;
+    if (!I64 || S.dtype == 0) {
+        int32_t y = static_cast<int32_t>(xk);
+        if (clamp) y = min(max(y, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
+        return static_cast<uint32_t>(y) - static_cast<uint32_t>(S.base);
+    }
+    if (clamp) x = min(max(x, S.clamp_lo), S.clamp_hi);
+    return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
+}
+
+// Buckets of a batch of slots [S0, S0 + NB) over one row quad.  All level-1 lookups
+// are issued before any is consumed (independent shared-memory loads in flight);
+// the rare nested / list / search entries are resolved afterwards in one branch.
+template <int NC, int S0, int NB, bool I64>
+__device__ __forceinline__ void buckets_batch(const ProbeParams &P, const KeyT<I64> (&v)[NC][4],
+                                              uint32_t (&bk)[NC][4]) {
+    const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
+    const bool clamp = P.clamp;
+    uint32_t u[NB][4];
+    uint2 e[NB][4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) bk[k] = bucket_i64(S, v[k], clamp);
+    for (int i = 0; i < NB; ++i) {
+        const int s = S0 + i;
+        const SlotParams &S = P.slot[s];
+        const bool lut = s < (int)P.nslots && S.mode == MODE_LUT;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            u[i][k] = lut ? offset_of<I64>(S, v[s][k], clamp) : 0u;
+            e[i][k] = lut ? T[S.lut_idx + (u[i][k] >> S.s1)] : make_uint2(0u, 0u);
+        }
+    }
+    uint32_t spec = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            spec |= e[i][k].x;
+            bk[S0 + i][k] = (e[i][k].x & kBaseMask) + (u[i][k] > e[i][k].y ? 1u : 0u);
+        }
+    }
+    if (spec & kSpecial) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const SlotParams &S = P.slot[S0 + i];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if ((FULL || ((keep >> k) & 1u)) && !(dbg & 2)) atomicAdd(sm32 + bk[k], 1u);
+                if (e[i][k].x & kSpecial) bk[S0 + i][k] = lut_bucket(S, u[i][k]);
         }
-        if (S.has_hll && !(dbg & 8)) {
+    }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool dup = FULL && k > 0 && v[k] == v[k - 1];
-                if ((FULL || ((keep >> k) & 1u)) && !dup) hll_i64(S, v[k], lmin, dbg);
-            }
+    for (int i = 0; i < NB; ++i) {   // binary-search fallback columns
+        const int s = S0 + i;
+        if (s < (int)P.nslots && P.slot[s].mode == MODE_SEARCH) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk[s][k] = P.slot[s].hist_idx + search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
         }
     }
 }
@@ -241,10 +273,38 @@ __device__ __forceinline__ void pairs_quad(const ProbeParams &P, const uint32_t 
 template <int NC, bool I64, bool FULL>
 __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[NC][I64 ? 2 : 1], uint32_t keep,
                                           const uint32_t (&lmin)[NC]) {
-    uint32_t bk[NC][4];
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    const uint32_t dbg = P.dbg;
+    KeyT<I64> v[NC][4];
 #pragma unroll
     for (int s = 0; s < NC; ++s)
-        if (s < (int)P.nslots) slot_quad<I64, FULL>(P, P.slot[s], r[s], keep, bk[s], lmin[s]);
+        if (s < (int)P.nslots) decode<I64>(P.slot[s], r[s], v[s]);
+    uint32_t bk[NC][4];
+    buckets_batch<NC, 0, (NC < 4 ? NC : 4), I64>(P, v, bk);
+    if (NC > 4) buckets_batch<NC, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1), I64>(P, v, bk);
+    // per-column bucket histograms
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (s >= (int)P.nslots || P.slot[s].mode == MODE_NOPRED || (dbg & 2)) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[s][k], 1u);
+    }
+    // HLL registers
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        const SlotParams &S = P.slot[s];
+        if (s >= (int)P.nslots || !S.has_hll || (dbg & 8)) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            // a key equal to the previous row's key cannot change a register
+            const bool dup = FULL && k > 0 && v[s][k] == v[s][k - 1];
+            if ((FULL || ((keep >> k) & 1u)) && !dup) {
+                if (!I64 || S.dtype == 0) hll_i32(S, static_cast<int32_t>(v[s][k]), lmin[s], dbg);
+                else hll_i64(S, v[s][k], lmin[s], dbg);
+            }
+        }
+    }
     pairs_quad<NC, FULL>(P, bk, keep);
 }
 
