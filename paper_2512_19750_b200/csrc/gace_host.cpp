@@ -648,7 +648,6 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     ProbeParams &P = pl.P;
     memset(&P, 0, sizeof(P));
     P.nslots = (uint32_t)pl.slots.size();
-    for (int i = 0; i < kMaxSlots * kMaxSlots; ++i) P.combo[i] = -1;
     uint32_t bps = 0;
     for (size_t i = 0; i < pl.slots.size(); ++i) {
         SlotPlan &S = pl.slots[i];
@@ -688,8 +687,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             P.grp[g].mapA_adj = (int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx;
             P.grp[g].mapB_adj = (int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx;
         }
-        P.combo[G.a * kMaxSlots + G.b] = (int8_t)g;
     }
+    P.ngroups = (uint32_t)pl.groups.size();
     P.ndirect = (uint32_t)pl.direct.size();
     P.image_u4 = image_words / 4;
     P.acc_idx = pl.acc_idx;

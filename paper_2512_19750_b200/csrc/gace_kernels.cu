@@ -75,7 +75,7 @@ __device__ __forceinline__ void hll_i64(const SlotParams &S, int64_t x, uint32_t
 }
 
 // Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
-__device__ __forceinline__ uint32_t hll_min(const SlotParams &S) {
+__device__ __noinline__ uint32_t hll_min(const SlotParams &S) {
     const uint4 *R = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint32_t *>(g_smem) + S.hll_idx);
     const uint32_t lane = threadIdx.x & 31;
     uint32_t m = 0xFFFFFFFFu;
@@ -87,8 +87,9 @@ __device__ __forceinline__ uint32_t hll_min(const SlotParams &S) {
     return __reduce_min_sync(0xFFFFFFFFu, m);
 }
 
-// #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback).
-__device__ __forceinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, int64_t v) {
+// #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback; kept out of line
+// so the hot loop stays small enough for the instruction cache).
+__device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, int64_t v) {
     uint32_t lo = 0;
     while (n > 0) {
         const uint32_t half = n >> 1;
@@ -104,8 +105,9 @@ struct SmemTables {
     __device__ __forceinline__ uint32_t u32(uint32_t i) const { return reinterpret_cast<const uint32_t *>(g_smem)[i]; }
 };
 
-// Absolute shared-memory index of the histogram bucket of offset u.
-__device__ __forceinline__ uint32_t lut_bucket(const SlotParams &S, uint32_t u) {
+// Absolute shared-memory index of the histogram bucket of offset u (full walk through
+// nested cells and lists; out of line, only taken for the rare special entries).
+__device__ __noinline__ uint32_t lut_bucket(const SlotParams &S, uint32_t u) {
     return lut_lookup(SmemTables{}, S.lut_idx, S.s1, u);
 }
 
@@ -170,142 +172,75 @@ __device__ __forceinline__ void decode(const SlotParams &S, const int4 (&r)[I64 
 // Offset u = key - base of a LUT-mode slot (with the optional clamp), 32-bit ops for int32.
 template <bool I64>
 __device__ __forceinline__ uint32_t offset_of(const SlotParams &S, KeyT<I64> xk, bool clamp) {
-    int64_t x = xk;
     if (!I64 || S.dtype == 0) {
         int32_t y = static_cast<int32_t>(xk);
         if (clamp) y = min(max(y, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
         return static_cast<uint32_t>(y) - static_cast<uint32_t>(S.base);
     }
+    int64_t x = xk;
     if (clamp) x = min(max(x, S.clamp_lo), S.clamp_hi);
     return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
 }
 
-// Buckets of a batch of slots [S0, S0 + NB) over one row quad.  All level-1 lookups
-// are issued before any is consumed (independent shared-memory loads in flight);
-// the rare nested / list / search entries are resolved afterwards in one branch.
+// Absolute bucket ids of a row quad, 16 bits per slot (shared-memory u32 index < 2^16),
+// four slots per 64-bit word: extraction by a runtime slot index is a shift, so the
+// pair loop below can run over groups without spilling a per-slot array.
+template <int NC>
+struct Ids {
+    uint64_t w[(NC + 3) / 4][4];
+    __device__ __forceinline__ void set(int s, int k, uint32_t b) {   // s compile-time
+        w[s >> 2][k] |= static_cast<uint64_t>(b) << (16 * (s & 3));
+    }
+    __device__ __forceinline__ uint32_t get(uint32_t s, int k) const {
+        const uint64_t x = (NC > 4 && (s & 4)) ? w[(NC + 3) / 4 - 1][k] : w[0][k];
+        return static_cast<uint32_t>(x >> (16 * (s & 3))) & 0xFFFFu;
+    }
+};
+
+// Buckets of slots [S0, S0 + NB) over one row quad.  All level-1 lookups are issued
+// before any is consumed; the rare nested / list / search entries are resolved
+// afterwards behind one branch.
 template <int NC, int S0, int NB, bool I64>
-__device__ __forceinline__ void buckets_batch(const ProbeParams &P, const KeyT<I64> (&v)[NC][4],
-                                              uint32_t (&bk)[NC][4]) {
+__device__ __forceinline__ void buckets_batch(const ProbeParams &P, const KeyT<I64> (&v)[NC][4], Ids<NC> &ids) {
     const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
     const bool clamp = P.clamp;
     uint32_t u[NB][4];
     uint2 e[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const int s = S0 + i;
-        const SlotParams &S = P.slot[s];
-        const bool lut = s < (int)P.nslots && S.mode == MODE_LUT;
+        const SlotParams &S = P.slot[S0 + i];
+        const bool lut = S0 + i < (int)P.nslots && S.mode == MODE_LUT;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            u[i][k] = lut ? offset_of<I64>(S, v[s][k], clamp) : 0u;
+            u[i][k] = lut ? offset_of<I64>(S, v[S0 + i][k], clamp) : 0u;
             e[i][k] = lut ? T[S.lut_idx + (u[i][k] >> S.s1)] : make_uint2(0u, 0u);
         }
     }
     uint32_t spec = 0;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
+    for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            spec |= e[i][k].x;
-            bk[S0 + i][k] = (e[i][k].x & kBaseMask) + (u[i][k] > e[i][k].y ? 1u : 0u);
-        }
-    }
+        for (int k = 0; k < 4; ++k) spec |= e[i][k].x;
     if (spec & kSpecial) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const SlotParams &S = P.slot[S0 + i];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (e[i][k].x & kSpecial) bk[S0 + i][k] = lut_bucket(S, u[i][k]);
+                if (e[i][k].x & kSpecial) e[i][k] = make_uint2(lut_bucket(S, u[i][k]), kNoThr);
         }
     }
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {   // binary-search fallback columns
+    for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
-        if (s < (int)P.nslots && P.slot[s].mode == MODE_SEARCH) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bk[s][k] = P.slot[s].hist_idx + search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
-        }
-    }
-}
-
-// Pair counts of one row quad: one 2-D grid bin per row and column pair (a, b), and
-// per-row evaluation of the pairs of column pairs whose grid did not fit ("direct").
-template <int NC, bool FULL>
-__device__ __forceinline__ void pairs_quad(const ProbeParams &P, const uint32_t (&bk)[NC][4], uint32_t keep) {
-    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
-#pragma unroll
-    for (int a = 0; a < NC; ++a) {
-#pragma unroll
-        for (int b = a + 1; b < NC; ++b) {
-            const int g = P.combo[a * kMaxSlots + b];
-            if (g < 0) continue;
-            const GroupParams &G = P.grp[g];
-            if (G.has_grid) {
-                const int ma = G.mapA_adj;
-                const int mb = G.mapB_adj;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if ((FULL || ((keep >> k) & 1u)) && !(P.dbg & 4)) {
-                        const uint32_t ia = sm32[ma + (int)bk[a][k]];
-                        const uint32_t ib = sm32[mb + (int)bk[b][k]];
-                        atomicAdd(sm32 + ia + ib, 1u);
-                    }
-                }
-            }
-            for (uint32_t d = G.dbeg; d < G.dend; ++d) {
-                const DirectPair D = P.direct[d];
-                uint32_t c = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t ina = ((bk[a][k] >= D.la) & (bk[a][k] <= D.ha)) ^ D.nega;
-                    const uint32_t inb = ((bk[b][k] >= D.lb) & (bk[b][k] <= D.hb)) ^ D.negb;
-                    c += ((keep >> k) & 1u) & ina & inb;
-                }
-                const uint32_t m = __activemask();
-                const uint32_t tot = __reduce_add_sync(m, c);
-                if ((threadIdx.x & 31) == (uint32_t)(__ffs(m) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
-            }
-        }
-    }
-}
-
-template <int NC, bool I64, bool FULL>
-__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[NC][I64 ? 2 : 1], uint32_t keep,
-                                          const uint32_t (&lmin)[NC]) {
-    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
-    const uint32_t dbg = P.dbg;
-    KeyT<I64> v[NC][4];
-#pragma unroll
-    for (int s = 0; s < NC; ++s)
-        if (s < (int)P.nslots) decode<I64>(P.slot[s], r[s], v[s]);
-    uint32_t bk[NC][4];
-    buckets_batch<NC, 0, (NC < 4 ? NC : 4), I64>(P, v, bk);
-    if (NC > 4) buckets_batch<NC, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1), I64>(P, v, bk);
-    // per-column bucket histograms
-#pragma unroll
-    for (int s = 0; s < NC; ++s) {
-        if (s >= (int)P.nslots || P.slot[s].mode == MODE_NOPRED || (dbg & 2)) continue;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (FULL || ((keep >> k) & 1u)) atomicAdd(sm32 + bk[s][k], 1u);
-    }
-    // HLL registers
-#pragma unroll
-    for (int s = 0; s < NC; ++s) {
         const SlotParams &S = P.slot[s];
-        if (s >= (int)P.nslots || !S.has_hll || (dbg & 8)) continue;
+        if (s < (int)P.nslots && S.mode == MODE_SEARCH) {      // binary-search fallback column
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            // a key equal to the previous row's key cannot change a register
-            const bool dup = FULL && k > 0 && v[s][k] == v[s][k - 1];
-            if ((FULL || ((keep >> k) & 1u)) && !dup) {
-                if (!I64 || S.dtype == 0) hll_i32(S, static_cast<int32_t>(v[s][k]), lmin[s], dbg);
-                else hll_i64(S, v[s][k], lmin[s], dbg);
-            }
+            for (int k = 0; k < 4; ++k) e[i][k] = make_uint2(S.hist_idx + search_bucket(S.bps, S.nbp, v[s][k]), kNoThr);
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ids.set(s, k, (e[i][k].x & kBaseMask) + (u[i][k] > e[i][k].y ? 1u : 0u));
     }
-    pairs_quad<NC, FULL>(P, bk, keep);
 }
 
 // Rows per thread per loop iteration: 4 * U, U chosen so each thread keeps >= 64 bytes
@@ -314,6 +249,116 @@ template <int NC>
 struct Cfg {
     static constexpr int U = NC >= 4 ? 1 : 4 / NC;
 };
+
+// Everything one row quad contributes: histograms, HLL registers, 2-D pair grids and
+// per-row ("direct") pairs.  keep: one bit per row.
+template <int NC, bool I64>
+__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[NC][I64 ? 2 : 1], uint32_t keep,
+                                          const uint32_t (&lmin)[NC]) {
+    uint32_t *sm32 = reinterpret_cast<uint32_t *>(g_smem);
+    const uint32_t dbg = P.dbg;
+    KeyT<I64> v[NC][4];
+#pragma unroll
+    for (int s = 0; s < NC; ++s)
+        if (s < (int)P.nslots) decode<I64>(P.slot[s], r[s], v[s]);
+    Ids<NC> ids;
+#pragma unroll
+    for (int h = 0; h < (NC + 3) / 4; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ids.w[h][k] = 0;
+    buckets_batch<NC, 0, (NC < 4 ? NC : 4), I64>(P, v, ids);
+    if (NC > 4) buckets_batch<NC, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1), I64>(P, v, ids);
+    // per-column bucket histograms
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (s >= (int)P.nslots || P.slot[s].mode == MODE_NOPRED || (dbg & 2)) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((keep >> k) & 1u) atomicAdd(sm32 + ids.get(s, k), 1u);
+    }
+    // HLL: hash all four keys, then one branch for the (rare) ranks above the bound
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        const SlotParams &S = P.slot[s];
+        if (s >= (int)P.nslots || !S.has_hll || (dbg & 8)) continue;
+        uint32_t idx[4], rk[4], m = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!I64 || S.dtype == 0) {
+                const uint32_t h = fmix32(static_cast<uint32_t>(v[s][k]));
+                idx[k] = h >> (32 - kHllP);
+                rk[k] = __clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
+            } else {
+                const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
+                idx[k] = static_cast<uint32_t>(h >> (64 - kHllP));
+                rk[k] = __clzll((h << kHllP) | (1ull << (kHllP - 1))) + 1;
+            }
+            // a key equal to the previous kept row's key cannot change a register
+            const bool dup = k > 0 && ((keep >> (k - 1)) & 1u) && v[s][k] == v[s][k - 1];
+            m |= (((keep >> k) & 1u) && !dup && rk[k] > lmin[s]) ? (1u << k) : 0u;
+        }
+        if (m) {
+            uint32_t *R = sm32 + S.hll_idx;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (((m >> k) & 1u) && rk[k] > R[idx[k]] && !(dbg & 1)) atomicMax(R + idx[k], rk[k]);
+        }
+    }
+    // pairs: runtime loop over column pairs
+    for (uint32_t g = 0; g < P.ngroups; ++g) {
+        const GroupParams &G = P.grp[g];
+        if (G.has_grid && !(dbg & 4)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if ((keep >> k) & 1u) {
+                    const uint32_t ia = sm32[G.mapA_adj + (int)ids.get(G.a, k)];
+                    const uint32_t ib = sm32[G.mapB_adj + (int)ids.get(G.b, k)];
+                    atomicAdd(sm32 + ia + ib, 1u);
+                }
+            }
+        }
+        for (uint32_t d = G.dbeg; d < G.dend; ++d) {
+            const DirectPair D = P.direct[d];
+            uint32_t c = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t ba = ids.get(G.a, k), bb = ids.get(G.b, k);
+                const uint32_t ina = ((ba >= D.la) & (ba <= D.ha)) ^ D.nega;
+                const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
+                c += ((keep >> k) & 1u) & ina & inb;
+            }
+            const uint32_t am = __activemask();
+            const uint32_t tot = __reduce_add_sync(am, c);
+            if ((threadIdx.x & 31) == (uint32_t)(__ffs(am) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
+        }
+    }
+}
+
+// One row past the last full unit (scalar loads; out of line: cold code).
+template <int NC, bool SAMPLE, bool I64>
+__device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
+    const uint32_t keep = (!SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
+    if (!keep) return 0;
+    int4 rj[NC][I64 ? 2 : 1];
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (s >= (int)P.nslots) continue;
+        if (!I64 || P.slot[s].dtype == 0) {
+            const int32_t x = __ldg(static_cast<const int32_t *>(P.slot[s].ptr) + r);
+            rj[s][0] = make_int4(x, x, x, x);     // rows 1..3 of the quad are masked off
+        } else {
+            const long long x = __ldg(static_cast<const long long *>(P.slot[s].ptr) + r);
+            const int lo = (int)(x & 0xFFFFFFFF), hi = (int)(x >> 32);
+            rj[s][0] = make_int4(lo, hi, lo, hi);
+            rj[s][I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
+        }
+    }
+    uint32_t zero[NC];
+#pragma unroll
+    for (int s = 0; s < NC; ++s) zero[s] = 0;
+    quad_work<NC, I64>(P, rj, 1u, zero);
+    return 1;
+}
 
 template <int NC, bool SAMPLE, bool I64>
 __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constant__ ProbeParams P) {
@@ -354,6 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
                 keep = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) keep |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
+                kept += __popc(keep);
+                if (!keep) continue;
             }
             int4 rj[NC][I64 ? 2 : 1];
 #pragma unroll
@@ -361,37 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1) probe_kernel(const __grid_constan
                 rj[s][0] = X.r[s][j][0];
                 if (I64) rj[s][I64 ? 1 : 0] = X.r[s][j][I64 ? 1 : 0];
             }
-            kept += __popc(keep);
-            if (keep == 0xFu) quad_work<NC, I64, true>(P, rj, keep, lmin);
-            else if (keep) quad_work<NC, I64, false>(P, rj, keep, lmin);
+            quad_work<NC, I64>(P, rj, keep, lmin);
         }
         X = Xn;
     }
+    if (!SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed was kept
     // tail rows [nunits * 4U, nrows): one row per thread of the last CTA, scalar loads
     const uint64_t tail0 = nunits * 4 * U;
-    if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < P.nrows) {
-        const uint64_t r = tail0 + threadIdx.x;
-        const uint32_t keep = (!SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
-        int4 rj[NC][I64 ? 2 : 1];
-#pragma unroll
-        for (int s = 0; s < NC; ++s) {
-            if (s >= (int)P.nslots) continue;
-            if (!I64 || P.slot[s].dtype == 0) {
-                const int32_t x = __ldg(static_cast<const int32_t *>(P.slot[s].ptr) + r);
-                rj[s][0] = make_int4(x, x, x, x);     // rows 1..3 of the quad are masked off
-            } else {
-                const long long x = __ldg(static_cast<const long long *>(P.slot[s].ptr) + r);
-                const int lo = (int)(x & 0xFFFFFFFF), hi = (int)(x >> 32);
-                rj[s][0] = make_int4(lo, hi, lo, hi);
-                rj[s][I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
-            }
-        }
-        kept += keep;
-        uint32_t zero[NC];
-#pragma unroll
-        for (int s = 0; s < NC; ++s) zero[s] = 0;
-        if (keep) quad_work<NC, I64, false>(P, rj, 1u, zero);
-    }
+    if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < P.nrows)
+        kept += tail_row<NC, SAMPLE, I64>(P, tail0 + threadIdx.x);
     __syncthreads();
 
     // CTA partials -> global

@@ -103,8 +103,8 @@ struct DirectPair {
 struct ProbeParams {
     SlotParams slot[kMaxSlots];
     GroupParams grp[kMaxGroups];
-    int8_t combo[kMaxSlots * kMaxSlots];   // group of slots (a, b), a < b, or -1
     uint32_t nslots;
+    uint32_t ngroups;                      // column pairs carrying cross-column pairs
     uint32_t ndirect;
     const DirectPair *direct;              // device
     const uint4 *image;                    // device: tables copied into shared memory
