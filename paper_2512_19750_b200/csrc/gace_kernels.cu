@@ -327,9 +327,9 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
                 c += ((keep >> k) & 1u) & ina & inb;
             }
-            const uint32_t am = __activemask();
-            const uint32_t tot = __reduce_add_sync(am, c);
-            if ((threadIdx.x & 31) == (uint32_t)(__ffs(am) - 1) && tot) atomicAdd(sm32 + D.acc_idx, tot);
+            // per-thread add: this loop may run with a diverged warp (sampled quads), where a
+            // warp-collective reduction over __activemask() is not well defined
+            if (c) atomicAdd(sm32 + D.acc_idx, c);
         }
     }
 }
