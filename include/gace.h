@@ -202,6 +202,10 @@ typedef struct {
     double total_ms;        /* first to last event                                     */
     uint64_t scan_launches; /* probe-kernel launches in that call                      */
     uint64_t bytes_scanned; /* algorithmic bytes: rows x sum of probed column widths   */
+    int32_t jit;            /* 1: plan-specialised (NVRTC) kernel, 0: generic kernel,
+                               -1: specialisation failed, generic kernel used           */
+    int32_t pad;
+    double jit_compile_ms;  /* NVRTC compile time spent in that call (0 when cached)   */
 } gace_timing;
 
 gace_status gace_last_timing(const gace_table *t, gace_timing *out);
@@ -223,6 +227,14 @@ gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtypes, const i
                                uint64_t hll_mask, uint32_t col, const int64_t *values, uint64_t n,
                                uint32_t *out, uint32_t *mode, int64_t *bps, uint32_t cap,
                                uint32_t *nbp);
+
+/* Test hook (host only; needs libnvrtc, no device): plan a batch as gace_debug_buckets
+ * does and compile its plan-specialised probe kernel without launching
+ * it; *cubin_bytes = size of the compiled image.  GACE_EUNSUPPORTED carries the NVRTC log. */
+gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
+                                   const int64_t *dhi, int host, const gace_pred *preds,
+                                   uint32_t npreds, const gace_pair *pairs, uint32_t npairs,
+                                   uint64_t hll_mask, double sample_rate, uint64_t *cubin_bytes);
 
 /* Number of this library's CUDA kernels launched since load (all tables). */
 uint64_t gace_kernel_launches(void);

@@ -18,8 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["gace_kernels.cu", "gace_host.cpp"]
-HEADERS = ["gace_plan.h", "gace_kernels.h"]
+SOURCES = ["gace_kernels.cu", "gace_host.cpp", "gace_jit.cpp"]
+HEADERS = ["gace_plan.h", "gace_kernels.h", "gace_probe.cuh", "gace_jit.h"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -29,18 +29,34 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _embed_sources() -> str:
+    """build/gace_jit_sources.inc: the probe's device sources as C++ raw strings for NVRTC."""
+    inc = os.path.join(OBJ, "gace_jit_sources.inc")
+    parts = []
+    for var, name in (("kSrcPlanH", "gace_plan.h"), ("kSrcProbeCuh", "gace_probe.cuh")):
+        text = open(os.path.join(CSRC, name)).read()
+        assert ')GACESRC"' not in text
+        parts.append(f'static const char {var}[] = R"GACESRC({text})GACESRC";\n')
+    body = "".join(parts)
+    if not os.path.exists(inc) or open(inc).read() != body:
+        with open(inc, "w") as f:
+            f.write(body)
+    return inc
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    inc = _embed_sources()
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "gace.h")]
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
-        if force or _stale(o, [s] + hdrs):
+        if force or _stale(o, [s] + hdrs + [inc]):
             cmd = [NVCC] + ARCH + COMMON + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
             if src.endswith(".cpp"):
-                cmd = [NVCC] + COMMON + ["-x", "c++", "-c", s, "-o", o]
+                cmd = [NVCC] + COMMON + ["-I", OBJ, "-x", "c++", "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

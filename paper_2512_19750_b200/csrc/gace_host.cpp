@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/gace.h"
+#include "gace_jit.h"
 #include "gace_kernels.h"
 #include "gace_plan.h"
 
@@ -831,6 +832,56 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
 
 }  // namespace
 
+namespace {
+
+// Source of `struct JitShape` for gace_probe.cuh: the plan's structural decisions as
+// constexpr answers (predicate values stay in the kernel parameters).
+std::string jit_shape_source(const Plan &pl, bool sample, bool i64) {
+    const ProbeParams &P = pl.P;
+    const int nc = (int)P.nslots;
+    auto chain = [&](auto f, int n) {
+        std::string r;
+        for (int i = 0; i < n; ++i) r += "s == " + std::to_string(i) + " ? " + f(i) + " : ";
+        return r + "0";
+    };
+    std::string o = "namespace gace {\nstruct JitShape {\n";
+    o += "  static constexpr int NC = " + std::to_string(nc) + ";\n";
+    o += "  static constexpr bool SAMPLE = " + std::string(sample ? "true" : "false") + ";\n";
+    o += "  static constexpr bool I64 = " + std::string(i64 ? "true" : "false") + ";\n";
+    o += "  static constexpr bool STATIC = true;\n";
+    o += "  static constexpr int U = NC >= 4 ? 1 : 4 / NC;\n";
+    o += "  static constexpr int NG = " + std::to_string(P.ngroups) + ";\n";
+    o += "  __device__ static constexpr bool active(const ProbeParams &, int s) { return s < NC; }\n";
+    o += "  __device__ static constexpr int mode(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::to_string((int)P.slot[i].mode); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool is32(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].dtype == 0 ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool hll(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].has_hll ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool clamp(const ProbeParams &) { return " +
+         std::string(P.clamp ? "true" : "false") + "; }\n";
+    auto gchain = [&](auto f) {
+        std::string r;
+        for (uint32_t g = 0; g < P.ngroups; ++g) r += "g == " + std::to_string(g) + " ? " + f(g) + " : ";
+        return r + "0";
+    };
+    o += "  __device__ static constexpr int ga(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].a); }) + "; }\n";
+    o += "  __device__ static constexpr int gb(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].b); }) + "; }\n";
+    o += "  __device__ static constexpr bool ggrid(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].has_grid ? "1" : "0"); }) + "; }\n";
+    o += "  __device__ static constexpr bool gdirect(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].dend > P.grp[g].dbeg ? "1" : "0"); }) + "; }\n";
+    o += "};\n}  // namespace gace\n";
+    return o;
+}
+
+// GACE_JIT=0: never specialise; 1: always; unset: for launches of >= 2^24 rows.
+int jit_mode() {
+    const char *e = getenv("GACE_JIT");
+    if (!e) return 2;
+    return atoi(e) ? 1 : 0;
+}
+
+}  // namespace
+
 // ====================================================================== C-ABI
 
 extern "C" {
@@ -969,6 +1020,24 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const uint64_t max_rows = (uint64_t)grid * kThreads * (1ull << 19);
     uint64_t launches = 0;
     double h2d_ms = 0;
+    // specialised (NVRTC) kernel for large launches, generic precompiled kernel otherwise
+    const int jm = jit_mode();
+    std::string shape;
+    double jit_ms = 0;
+    int jit_used = 0;
+    auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
+        if (PP.nslots > 0 && (jm == 1 || (jm == 2 && n >= (1ull << 24)))) {
+            if (shape.empty()) shape = jit_shape_source(pl, sample, i64);
+            std::string err;
+            if (jit_launch(PP, t->device, shape, grid, s, &jit_ms, &err)) {
+                jit_used = 1;
+                return cudaSuccess;
+            }
+            jit_used = -1;     // fall back to the generic GPU kernel; reason in gace_last_error()
+            g_err = "jit unavailable, generic kernel used: " + err;
+        }
+        return launch_probe(PP, sample, i64, grid, s);
+    };
     if (t->nrows == 0) {
         CUDA_TRY(cudaMemsetAsync(t->d_part.p, 0, part_bytes, s));
     } else if (!t->host) {
@@ -981,7 +1050,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
             P.nrows = n;
             P.row0 = row_offset + r0;
             P.part_merge = launches ? 1u : 0u;
-            CUDA_TRY(launch_probe(P, sample, i64, grid, s));
+            CUDA_TRY(launch_scan(P, n));
             ++launches;
         }
     } else {
@@ -1013,7 +1082,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
             P.nrows = n;
             P.row0 = row_offset + r0;
             P.part_merge = launches ? 1u : 0u;
-            CUDA_TRY(launch_probe(P, sample, i64, grid, s));
+            CUDA_TRY(launch_scan(P, n));
             ++launches;
             CUDA_TRY(cudaEventRecord(t->ev_free[b], s));
         }
@@ -1076,6 +1145,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     }
     T.h2d_ms = h2d_ms;
     T.scan_launches = launches;
+    T.jit = jit_used;
+    T.jit_compile_ms = jit_ms;
     T.bytes_scanned = t->nrows * bytes_per_row;
     return GACE_OK;
 }
@@ -1257,5 +1328,35 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         if (b < S.hist_idx || b >= S.hist_idx + S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
         out[k] = b - S.hist_idx;
     }
+    return GACE_OK;
+}
+
+// Test hook: plan a batch (as gace_debug_buckets) and compile its specialised probe kernel
+// with NVRTC without launching it.  *cubin_bytes = size of the compiled kernel image.
+extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
+                                              const int64_t *dhi, int host, const gace_pred *preds,
+                                              uint32_t npreds, const gace_pair *pairs, uint32_t npairs,
+                                              uint64_t hll_mask, double sample_rate, uint64_t *cubin_bytes) {
+    if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "bad arguments");
+    gace_table t;
+    t.ncols = ncols;
+    t.host = host != 0;
+    for (uint32_t c = 0; c < ncols; ++c) {
+        t.dtypes.push_back((int)dtypes[c]);
+        t.dlo.push_back(dlo[c]);
+        t.dhi.push_back(dhi[c]);
+    }
+    gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, sample_rate, hll_mask, GACE_HLL_P);
+    if (st) return st;
+    Plan pl;
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    if (st) return st;
+    if (pl.P.nslots == 0) return fail(GACE_EINVAL, "no probed columns");
+    bool i64 = false;
+    for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
+    std::string err;
+    size_t n = 0;
+    if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64), &n, &err)) return fail(GACE_EUNSUPPORTED, err);
+    if (cubin_bytes) *cubin_bytes = n;
     return GACE_OK;
 }

@@ -1,0 +1,28 @@
+// gace_jit.h -- NVRTC specialisation of the probe kernel (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "gace_plan.h"
+
+namespace gace {
+
+constexpr int kMaxSmemJit = 227 * 1024;
+
+// True if NVRTC and the driver API could be loaded (else *why says which).
+bool jit_available(std::string *why);
+
+// Launch the probe kernel specialised for `shape_src` (a generated `struct JitShape`),
+// compiling and caching it on first use for (device, shape).  Adds the compile time to
+// *compile_ms.  Returns false (with *err) if compilation or launch failed; nothing has
+// been launched in that case.
+bool jit_launch(const ProbeParams &P, int device, const std::string &shape_src, int grid, cudaStream_t s,
+                double *compile_ms, std::string *err);
+
+// NVRTC compile only (no device needed): the test hook gace_debug_jit_compile.
+bool jit_compile_check(const std::string &shape_src, size_t *cubin_bytes, std::string *err);
+
+size_t jit_cache_size();
+
+}  // namespace gace

@@ -12,8 +12,19 @@
 // histogram over the sub-buckets of only the pair-relevant predicates (joints are
 // rectangle sums).  HLL registers live in shared memory as u8[4096] per column.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>   // uint2 / uint4
 #include <stdint.h>
+#else                       // NVRTC (gace_jit.cpp): built-in vector types, no libc headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
+#endif
 
 namespace gace {
 

@@ -1,0 +1,448 @@
+// gace_probe.cuh -- device code of the probe kernel.
+//
+// Compiled twice:
+//   * offline by nvcc into generic kernels probe_kernel<NC, SAMPLE, I64> (RtShape):
+//     per-column / per-pair decisions are read from the kernel parameters at run time;
+//   * at run time by NVRTC with a generated JitShape (gace_jit.cpp): the plan's shape --
+//     column modes, dtypes, HLL flags, the list of column pairs -- is compile-time, so
+//     the hot loop carries only the work this probe batch needs.
+// Both instantiate the same probe_body<Shape>, so they compute the same bits.
+//
+// Per row unit (4*U rows per thread): 128-bit non-allocating loads of every probed
+// column, prefetched one unit ahead; sample bits from SplitMix64 of the global row id;
+// bucket ids from the shared-memory lookup tables (all level-1 reads issued before any is
+// used, one branch for the rare nested / list / search entries); u32 bucket histograms
+// (ATOMS.ADD); HLL: hash every key, touch shared memory only when the rank beats an exact
+// per-warp lower bound of the registers (ATOMS.MAX); one 2-D grid bin per row and column
+// pair; per-row evaluation for pairs whose grid did not fit.
+#pragma once
+#include "gace_plan.h"
+
+namespace gace {
+
+#define GACE_GAMMA 0x9E3779B97F4A7C15ULL
+
+template <bool B, class T, class F> struct Cond { using type = T; };
+template <class T, class F> struct Cond<false, T, F> { using type = F; };
+
+// SplitMix64 finaliser (sample bit; int64 HLL hash).  DESIGN.md §2 steps 1 and 6.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// MurmurHash3 fmix32 (int32 HLL hash).  DESIGN.md §2 step 6.
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6BU;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35U;
+    h ^= h >> 16;
+    return h;
+}
+
+__device__ __forceinline__ int4 ld_stream(const void *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+extern __shared__ uint4 g_smem[];
+
+__device__ __forceinline__ uint32_t *smem32() { return reinterpret_cast<uint32_t *>(g_smem); }
+
+// Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
+__device__ __noinline__ uint32_t hll_min(uint32_t hll_idx) {
+    const uint4 *R = reinterpret_cast<const uint4 *>(smem32() + hll_idx);
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t m = 0xFFFFFFFFu;
+#pragma unroll 8
+    for (int i = 0; i < kHllM / 4 / 32; ++i) {
+        const uint4 v = R[i * 32 + lane];
+        m = min(m, min(min(v.x, v.y), min(v.z, v.w)));
+    }
+    return __reduce_min_sync(0xFFFFFFFFu, m);
+}
+
+// #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback; out of line).
+__device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, int64_t v) {
+    uint32_t lo = 0;
+    while (n > 0) {
+        const uint32_t half = n >> 1;
+        const bool right = __ldg(bps + lo + half) <= v;
+        lo = right ? lo + half + 1 : lo;
+        n = right ? n - half - 1 : half;
+    }
+    return lo;
+}
+
+struct SmemTables {
+    __device__ __forceinline__ uint2 u2(uint32_t i) const { return reinterpret_cast<const uint2 *>(g_smem)[i]; }
+    __device__ __forceinline__ uint32_t u32(uint32_t i) const { return smem32()[i]; }
+};
+
+// Full walk through nested cells and lists (out of line: rare special entries only).
+__device__ __noinline__ uint32_t lut_bucket(uint32_t lut_idx, uint32_t s1, uint32_t u) {
+    return lut_lookup(SmemTables{}, lut_idx, s1, u);
+}
+
+__device__ __forceinline__ bool keep_row(const ProbeParams &P, uint64_t g) {
+    return mix64(P.seed + (g + 1) * GACE_GAMMA) < P.thr;
+}
+
+// ------------------------------------------------------------------ plan shapes
+
+// Generic shape: only NC / SAMPLE / I64 are compile-time.
+template <int NC_, bool SAMPLE_, bool I64_>
+struct RtShape {
+    static constexpr int NC = NC_;
+    static constexpr bool SAMPLE = SAMPLE_;
+    static constexpr bool I64 = I64_;
+    static constexpr bool STATIC = false;
+    static constexpr int U = NC >= 4 ? 1 : 4 / NC;
+    static constexpr int NG = 0;
+    __device__ static bool active(const ProbeParams &P, int s) { return s < (int)P.nslots; }
+    __device__ static int mode(const ProbeParams &P, int s) { return P.slot[s].mode; }
+    __device__ static bool is32(const ProbeParams &P, int s) { return !I64 || P.slot[s].dtype == 0; }
+    __device__ static bool hll(const ProbeParams &P, int s) { return P.slot[s].has_hll; }
+    __device__ static bool clamp(const ProbeParams &P) { return P.clamp; }
+    __device__ static constexpr int ga(int) { return 0; }
+    __device__ static constexpr int gb(int) { return 0; }
+    __device__ static constexpr bool ggrid(int) { return false; }
+    __device__ static constexpr bool gdirect(int) { return false; }
+};
+
+// ------------------------------------------------------------------ row units
+
+template <class Sh>
+using KeyT = typename Cond<Sh::I64, int64_t, int32_t>::type;
+
+template <class Sh>
+struct Unit {
+    int4 r[Sh::NC][Sh::U][Sh::I64 ? 2 : 1];
+};
+
+template <class Sh>
+__device__ __forceinline__ void load_unit(const ProbeParams &P, uint64_t u, Unit<Sh> &X) {
+#pragma unroll
+    for (int s = 0; s < Sh::NC; ++s) {
+        if (!Sh::active(P, s)) continue;
+        const char *base = static_cast<const char *>(P.slot[s].ptr);
+        if (Sh::is32(P, s)) {
+#pragma unroll
+            for (int j = 0; j < Sh::U; ++j) X.r[s][j][0] = ld_stream(base + (u * Sh::U + j) * 16);
+        } else {
+#pragma unroll
+            for (int j = 0; j < Sh::U; ++j) {
+                X.r[s][j][0] = ld_stream(base + (u * Sh::U + j) * 32);
+                X.r[s][j][Sh::I64 ? 1 : 0] = ld_stream(base + (u * Sh::U + j) * 32 + 16);
+            }
+        }
+    }
+}
+
+template <class Sh>
+__device__ __forceinline__ void decode(const ProbeParams &P, int s, const int4 (&r)[Sh::I64 ? 2 : 1],
+                                       KeyT<Sh> (&v)[4]) {
+    if (Sh::is32(P, s)) {
+        v[0] = r[0].x; v[1] = r[0].y; v[2] = r[0].z; v[3] = r[0].w;
+    } else {
+        const int4 &a = r[0], &b = r[Sh::I64 ? 1 : 0];
+        v[0] = static_cast<KeyT<Sh>>((static_cast<int64_t>(a.y) << 32) | static_cast<uint32_t>(a.x));
+        v[1] = static_cast<KeyT<Sh>>((static_cast<int64_t>(a.w) << 32) | static_cast<uint32_t>(a.z));
+        v[2] = static_cast<KeyT<Sh>>((static_cast<int64_t>(b.y) << 32) | static_cast<uint32_t>(b.x));
+        v[3] = static_cast<KeyT<Sh>>((static_cast<int64_t>(b.w) << 32) | static_cast<uint32_t>(b.z));
+    }
+}
+
+// Offset u = key - base of a lookup-table column (with the optional clamp).
+template <class Sh>
+__device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<Sh> xk) {
+    const SlotParams &S = P.slot[s];
+    if (Sh::is32(P, s)) {
+        int32_t y = static_cast<int32_t>(xk);
+        if (Sh::clamp(P)) y = min(max(y, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
+        return static_cast<uint32_t>(y) - static_cast<uint32_t>(S.base);
+    }
+    int64_t x = xk;
+    if (Sh::clamp(P)) x = min(max(x, S.clamp_lo), S.clamp_hi);
+    return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
+}
+
+// Buckets (absolute shared-memory indices) of slots [S0, S0 + NB) over one row quad.
+template <class Sh, int S0, int NB>
+__device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
+                                        uint32_t (&bk)[Sh::NC][4]) {
+    const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
+    uint32_t u[NB][4];
+    uint2 e[NB][4];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int s = S0 + i;
+        const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
+            e[i][k] = lut ? T[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint2(0u, 0u);
+        }
+    }
+    uint32_t spec = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) spec |= e[i][k].x;
+    if (spec & kSpecial) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (e[i][k].x & kSpecial)
+                    e[i][k] = make_uint2(lut_bucket(P.slot[S0 + i].lut_idx, P.slot[S0 + i].s1, u[i][k]), kNoThr);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int s = S0 + i;
+        if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                e[i][k] = make_uint2(P.slot[s].hist_idx + search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]), kNoThr);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bk[s][k] = (e[i][k].x & kBaseMask) + (u[i][k] > e[i][k].y ? 1u : 0u);
+    }
+}
+
+// 16-bit packed bucket ids for the generic shape's runtime loop over column pairs.
+template <int NC>
+__device__ __forceinline__ uint32_t pick(const uint64_t (&w)[(NC + 3) / 4][4], uint32_t s, int k) {
+    const uint64_t x = (NC > 4 && (s & 4)) ? w[(NC + 3) / 4 - 1][k] : w[0][k];
+    return static_cast<uint32_t>(x >> (16 * (s & 3))) & 0xFFFFu;
+}
+
+__device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&ba)[4],
+                                             const uint32_t (&bb)[4], uint32_t keep) {
+    for (uint32_t d = G.dbeg; d < G.dend; ++d) {
+        const DirectPair D = P.direct[d];
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ina = ((ba[k] >= D.la) & (ba[k] <= D.ha)) ^ D.nega;
+            const uint32_t inb = ((bb[k] >= D.lb) & (bb[k] <= D.hb)) ^ D.negb;
+            c += ((keep >> k) & 1u) & ina & inb;
+        }
+        // per-thread add: this may run in a diverged warp (sampled quads), where a
+        // warp-collective reduction over __activemask() is not well defined
+        if (c) atomicAdd(smem32() + D.acc_idx, c);
+    }
+}
+
+__device__ __forceinline__ void grid_add(const GroupParams &G, const uint32_t (&ba)[4], const uint32_t (&bb)[4],
+                                         uint32_t keep) {
+    uint32_t *sm = smem32();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if ((keep >> k) & 1u) {
+            const uint32_t ia = sm[G.mapA_adj + (int)ba[k]];
+            const uint32_t ib = sm[G.mapB_adj + (int)bb[k]];
+            atomicAdd(sm + ia + ib, 1u);
+        }
+    }
+}
+
+// Everything one row quad contributes.  keep: one bit per row.
+template <class Sh>
+__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
+                                          uint32_t keep, const uint32_t (&lim)[Sh::NC]) {
+    constexpr int NC = Sh::NC;
+    uint32_t *sm = smem32();
+    const uint32_t dbg = P.dbg;
+    KeyT<Sh> v[NC][4];
+#pragma unroll
+    for (int s = 0; s < NC; ++s)
+        if (Sh::active(P, s)) decode<Sh>(P, s, r[s], v[s]);
+    uint32_t bk[NC][4];
+    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bk);
+    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bk);
+    // per-column bucket histograms
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (!Sh::active(P, s) || Sh::mode(P, s) == MODE_NOPRED || (dbg & 2)) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((keep >> k) & 1u) atomicAdd(sm + bk[s][k], 1u);
+    }
+    // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L,
+    // so the filter needs no clz; the (rare) survivors are checked against their register.
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
+        uint32_t idx[4], m = 0;
+        uint64_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            bool pass;
+            if (Sh::is32(P, s)) {
+                const uint32_t h = fmix32(static_cast<uint32_t>(v[s][k]));
+                idx[k] = h >> (32 - kHllP);
+                const uint32_t w32 = (h << kHllP) | (1u << (kHllP - 1));
+                w[k] = w32;
+                pass = w32 <= (0xFFFFFFFFu >> lim[s]);
+            } else {
+                const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
+                idx[k] = static_cast<uint32_t>(h >> (64 - kHllP));
+                w[k] = (h << kHllP) | (1ull << (kHllP - 1));
+                pass = w[k] <= (~0ull >> lim[s]);
+            }
+            m |= (((keep >> k) & 1u) && pass) ? (1u << k) : 0u;
+        }
+        if (m) {
+            uint32_t *R = sm + P.slot[s].hll_idx;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!((m >> k) & 1u)) continue;
+                const uint32_t rk = Sh::is32(P, s) ? __clz(static_cast<uint32_t>(w[k])) + 1 : __clzll(w[k]) + 1;
+                if (rk > R[idx[k]] && !(dbg & 1)) atomicMax(R + idx[k], rk);
+            }
+        }
+    }
+    // pairs
+    if (dbg & 4) return;
+    if (Sh::STATIC) {
+#pragma unroll
+        for (int g = 0; g < Sh::NG; ++g) {
+            const GroupParams &G = P.grp[g];
+            if (Sh::ggrid(g)) grid_add(G, bk[Sh::ga(g)], bk[Sh::gb(g)], keep);
+            if (Sh::gdirect(g)) direct_pairs(P, G, bk[Sh::ga(g)], bk[Sh::gb(g)], keep);
+        }
+    } else {
+        uint64_t ids[(NC + 3) / 4][4];
+#pragma unroll
+        for (int h = 0; h < (NC + 3) / 4; ++h)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint64_t x = 0;
+#pragma unroll
+                for (int q = 0; q < 4 && 4 * h + q < NC; ++q) x |= static_cast<uint64_t>(bk[4 * h + q][k]) << (16 * q);
+                ids[h][k] = x;
+            }
+        for (uint32_t g = 0; g < P.ngroups; ++g) {
+            const GroupParams &G = P.grp[g];
+            uint32_t ba[4], bb[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                ba[k] = pick<NC>(ids, G.a, k);
+                bb[k] = pick<NC>(ids, G.b, k);
+            }
+            if (G.has_grid) grid_add(G, ba, bb, keep);
+            if (G.dend > G.dbeg) direct_pairs(P, G, ba, bb, keep);
+        }
+    }
+}
+
+// One row past the last full unit (scalar loads; out of line: cold code).
+template <class Sh>
+__device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
+    const uint32_t keep = (!Sh::SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
+    if (!keep) return 0;
+    int4 rj[Sh::NC][Sh::I64 ? 2 : 1];
+#pragma unroll
+    for (int s = 0; s < Sh::NC; ++s) {
+        if (!Sh::active(P, s)) continue;
+        if (Sh::is32(P, s)) {
+            const int32_t x = __ldg(static_cast<const int32_t *>(P.slot[s].ptr) + r);
+            rj[s][0] = make_int4(x, x, x, x);     // rows 1..3 of the quad are masked off
+        } else {
+            const long long x = __ldg(static_cast<const long long *>(P.slot[s].ptr) + r);
+            const int lo = (int)(x & 0xFFFFFFFF), hi = (int)(x >> 32);
+            rj[s][0] = make_int4(lo, hi, lo, hi);
+            rj[s][Sh::I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
+        }
+    }
+    uint32_t zero[Sh::NC];
+#pragma unroll
+    for (int s = 0; s < Sh::NC; ++s) zero[s] = 0;
+    quad_work<Sh>(P, rj, 1u, zero);
+    return 1;
+}
+
+template <class Sh>
+__device__ __forceinline__ void probe_body(const ProbeParams &P) {
+    constexpr int NC = Sh::NC, U = Sh::U;
+    uint32_t *sm = smem32();
+    // tables -> shared memory; accumulators and registers -> 0
+    for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) g_smem[i] = __ldg(P.image + i);
+    for (uint32_t i = P.image_u4 + threadIdx.x; i < P.smem_bytes / 16; i += blockDim.x)
+        g_smem[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+
+    const uint64_t nunits = P.nrows / (4 * U);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t kept = 0;
+    uint32_t lim[NC];            // per-column lower bound L of the CTA's HLL registers
+#pragma unroll
+    for (int s = 0; s < NC; ++s) lim[s] = 0;
+    uint32_t it = 0, next_refresh = 4;
+    uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Unit<Sh> X;
+    if (u < nunits) load_unit<Sh>(P, u, X);
+    for (; u < nunits; u += stride, ++it) {
+        Unit<Sh> Xn;
+        if (u + stride < nunits) load_unit<Sh>(P, u + stride, Xn);       // prefetch
+        if (it == next_refresh) {
+            next_refresh = it + min(it, 128u);
+            if (__activemask() == 0xFFFFFFFFu) {
+#pragma unroll
+                for (int s = 0; s < NC; ++s)
+                    if (Sh::active(P, s) && Sh::hll(P, s)) lim[s] = min(hll_min(P.slot[s].hll_idx), 32u);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t keep = 0xFu;
+            if (Sh::SAMPLE) {
+                const uint64_t g0 = P.row0 + (u * U + j) * 4;
+                keep = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) keep |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
+                kept += __popc(keep);
+                if (!keep) continue;
+            }
+            int4 rj[NC][Sh::I64 ? 2 : 1];
+#pragma unroll
+            for (int s = 0; s < NC; ++s) {
+                rj[s][0] = X.r[s][j][0];
+                if (Sh::I64) rj[s][Sh::I64 ? 1 : 0] = X.r[s][j][Sh::I64 ? 1 : 0];
+            }
+            quad_work<Sh>(P, rj, keep, lim);
+        }
+        X = Xn;
+    }
+    if (!Sh::SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed
+    // tail rows [nunits * 4U, nrows): one row per thread of the last CTA
+    const uint64_t tail0 = nunits * 4 * U;
+    if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < P.nrows) kept += tail_row<Sh>(P, tail0 + threadIdx.x);
+    __syncthreads();
+
+    // CTA partials -> global
+    for (uint32_t i = threadIdx.x; i < P.acc_words; i += blockDim.x) {
+        const uint32_t x = sm[P.acc_idx + i];
+        if (x) atomicAdd(P.g_acc + i, (unsigned long long)x);
+    }
+    if (P.hll_bytes) {   // u32 registers -> packed u8 partial of this CTA
+        const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(g_smem) + P.hll_off);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes);
+        for (uint32_t i = threadIdx.x; i < P.hll_bytes / 4; i += blockDim.x) {
+            const uint4 q = src[i];
+            uint32_t x = q.x | (q.y << 8) | (q.z << 16) | (q.w << 24);
+            if (P.part_merge) x = __vmaxu4(x, dst[i]);   // later launch of a chunked probe
+            dst[i] = x;
+        }
+    }
+    kept = __reduce_add_sync(0xFFFFFFFFu, kept);
+    if ((threadIdx.x & 31) == 0 && kept) atomicAdd(P.g_nsamp, (unsigned long long)kept);
+}
+
+}  // namespace gace

@@ -34,7 +34,7 @@ PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
 EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
-           "gace_debug_buckets", "gace_kernel_launches", "gace_last_error"]
+           "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
 
 class GaceError(RuntimeError):
@@ -58,7 +58,8 @@ class _Timing(ctypes.Structure):
     _fields_ = [("plan_upload_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
                 ("finalize_ms", ctypes.c_double), ("merge_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("scan_launches", ctypes.c_uint64),
-                ("bytes_scanned", ctypes.c_uint64)]
+                ("bytes_scanned", ctypes.c_uint64), ("jit", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("jit_compile_ms", ctypes.c_double)]
 
 
 _lib = None
@@ -83,6 +84,7 @@ def lib() -> ctypes.CDLL:
     L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
     L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
     L.gace_nccl_unique_id.argtypes = [vp]
+    L.gace_debug_jit_compile.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, dbl, ctypes.POINTER(u64)]
     L.gace_debug_buckets.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, u32, vp, u64, vp,
                                      ctypes.POINTER(u32), vp, u32, ctypes.POINTER(u32)]
     for f in EXPORTS:
@@ -138,6 +140,24 @@ def debug_buckets(dtypes, dlo, dhi, host: bool, preds, pairs, hll_cols, col: int
                                     _ptr(Q), len(Q), mask, col, _ptr(v), len(v), out.ctypes.data,
                                     ctypes.byref(mode), bps.ctypes.data, len(bps), ctypes.byref(nbp)))
     return out[:len(v)], int(mode.value), bps[:nbp.value]
+
+
+def debug_jit_compile(dtypes, dlo, dhi, host: bool, preds, pairs, hll_cols, sample_rate=1.0) -> int:
+    """Test hook: NVRTC-compile the plan-specialised probe kernel of this batch (no device);
+    returns the cubin size."""
+    P = as_preds(preds)
+    Q = as_pairs(pairs)
+    mask = 0
+    for c in hll_cols:
+        mask |= 1 << int(c)
+    dt = np.ascontiguousarray(dtypes, dtype=np.int32)
+    lo = np.ascontiguousarray(dlo, dtype=np.int64)
+    hi = np.ascontiguousarray(dhi, dtype=np.int64)
+    n = ctypes.c_uint64()
+    _check(lib().gace_debug_jit_compile(len(dt), dt.ctypes.data, lo.ctypes.data, hi.ctypes.data, int(host),
+                                        _ptr(P), len(P), _ptr(Q), len(Q), mask, float(sample_rate),
+                                        ctypes.byref(n)))
+    return int(n.value)
 
 
 def kernel_launches() -> int:

@@ -263,3 +263,35 @@ def test_derived_values_end_to_end(G, oracle):
     np.testing.assert_allclose(pcs, opcs, rtol=1e-12)
     np.testing.assert_allclose(ndv, ondv, rtol=1e-12)
     np.testing.assert_allclose(drift, odrift, rtol=1e-12)
+
+
+@pytest.fixture
+def force_jit(monkeypatch):
+    monkeypatch.setenv("GACE_JIT", "1")
+    yield
+
+
+@pytest.mark.parametrize("name,nrows,rate", [
+    ("C1", 100_003, 1.0), ("C1", 50_001, 0.3), ("C2", 100_001, 0.01), ("C3", 200_002, 1.0),
+    ("C4", 60_003, 1.0), ("C5", 120_001, 1.0), ("C5_i64", 60_007, 1.0), ("C5", 50_000, 0.05),
+])
+def test_specialised_kernel_parity(G, oracle, force_jit, name, nrows, rate):
+    """The NVRTC plan-specialised kernel (the one large scans run) against the oracle."""
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    want = oracle.probe(cols, w.preds, w.pairs, rate=rate, seed=23, hll_cols=w.hll_cols)
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols])
+    try:
+        got = t.probe(w.preds, w.pairs, rate, 23, w.hll_cols)
+        assert t.last_timing()["jit"] == 1, G.lib().gace_last_error()
+    finally:
+        t.detach()
+    _assert_same(got, want)
+
+
+def test_specialised_kernel_edge_shapes(G, oracle, force_jit):
+    test_direct_pair_fallback(G, oracle)
+    test_eight_columns_every_group(G, oracle)
+    test_int64_wide_domain_search_mode(G, oracle)
+    for n in (1, 5, 33, 4097):
+        test_ragged_sizes(G, oracle, n)
