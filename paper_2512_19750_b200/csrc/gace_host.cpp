@@ -221,10 +221,11 @@ struct SlotPlan {
     bool clamp = false;
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
-    std::vector<uint2> l1, l2;         // entries with slot-relative indices (fixed up later)
+    std::vector<uint4> l1, l2;         // entries with slot-relative indices (fixed up later)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
     // layout
     uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_idx = 0, hll_idx = kNone, bps_off = 0, pre = 0;
+    uint32_t hist_addr() const { return 4 * hist_idx; }
 };
 
 uint32_t ceil_log2(uint64_t x) {
@@ -249,12 +250,16 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     S.lst.clear();
     bool ok = true;
     // entry for offsets [lo, hi] of a cell of size 2^s
-    std::function<uint2(uint64_t, uint64_t, uint32_t)> node = [&](uint64_t lo, uint64_t hi, uint32_t s) -> uint2 {
+    // entry for offsets [lo, hi] of a cell of size 2^s; relative bucket numbers here
+    std::function<uint4(uint64_t, uint64_t, uint32_t)> node = [&](uint64_t lo, uint64_t hi, uint32_t s) -> uint4 {
         const uint32_t b0 = le(lo), b1 = le(hi), cnt = b1 - b0;   // breakpoints in (lo, hi]
-        if (cnt == 0) return make_uint2(b0, kNoThr);
-        if (cnt == 1) return make_uint2(b0, (uint32_t)(toff[b0] - 1));
+        if (cnt <= 3) {
+            uint32_t t[3] = {kNoThr, kNoThr, kNoThr};
+            for (uint32_t i = 0; i < cnt; ++i) t[i] = (uint32_t)(toff[b0 + i] - 1);   // u > t  <=>  u >= toff
+            return make_uint4(b0, t[0], t[1], t[2]);
+        }
         if (cnt <= 8 || s == 0) {
-            uint2 e = make_uint2(kSpecial | kList | (cnt << 24) | b0, (uint32_t)S.lst.size());
+            uint4 e = make_uint4(kSpecial | kList | (cnt << 24) | b0, (uint32_t)S.lst.size(), 0, 0);
             for (uint32_t i = b0; i < b1; ++i) S.lst.push_back((uint32_t)toff[i]);
             return e;
         }
@@ -269,15 +274,15 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
             sc = s > want ? s - want : 0;
         }
         const uint64_t nsub = ((hi - lo) >> sc) + 1;
-        if (S.l2.size() + nsub > (1u << 22)) { ok = false; return make_uint2(b0, kNoThr); }
+        if (S.l2.size() + nsub > (1u << 20)) { ok = false; return make_uint4(b0, kNoThr, kNoThr, kNoThr); }
         const uint32_t first = (uint32_t)S.l2.size();
         S.l2.resize(first + nsub);
         for (uint64_t j = 0; j < nsub; ++j) {
             const uint64_t slo = lo + (j << sc), shi = std::min<uint64_t>(slo + (1ull << sc) - 1, hi);
-            const uint2 e = node(slo, shi, sc);
+            const uint4 e = node(slo, shi, sc);
             S.l2[first + j] = e;
         }
-        return make_uint2(kSpecial | (sc << 24), first);
+        return make_uint4(kSpecial | (sc << 24), first, 0, 0);
     };
     const uint64_t ncells = (span >> s1) + 1;
     const uint64_t csize = 1ull << s1;
@@ -288,7 +293,7 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     return ok;
 }
 
-size_t lut_bytes(const SlotPlan &S) { return 8 * (S.l1.size() + S.l2.size()) + 4 * S.lst.size() + 32; }
+size_t lut_bytes(const SlotPlan &S) { return 16 * (S.l1.size() + S.l2.size()) + 4 * S.lst.size() + 32; }
 
 struct Group {
     int a, b;                          // slots a < b
@@ -455,7 +460,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
         uint64_t target = 64;
-        while (target < 4096 && target < 32ull * S.T.size()) target <<= 1;
+        while (target < 4096 && target < 16ull * S.T.size()) target <<= 1;
         const uint64_t span = span_of(S);
         uint32_t sh = 0;
         while (sh < 31 && (span >> sh) + 1 > target) ++sh;
@@ -477,7 +482,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         SlotPlan &S = pl.slots[worst];
         // a coarser level 1 roughly halves it; when level 2 / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
-        if (s1[worst] >= 31 || S.l1.size() <= 64 || 8 * S.l2.size() + 4 * S.lst.size() > 8 * S.l1.size()) {
+        if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 16 * S.l1.size()) {
             to_search(S);
             continue;
         }
@@ -488,11 +493,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     uint32_t w = 0;    // u32 cursor
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        w = (w + 1) & ~1u;
-        S.lut_idx = w / 2;
-        w += 2 * (uint32_t)S.l1.size();
-        S.l2_idx = w / 2;
-        w += 2 * (uint32_t)S.l2.size();
+        w = (w + 3) & ~3u;
+        S.lut_idx = w / 4;
+        w += 4 * (uint32_t)S.l1.size();
+        S.l2_idx = w / 4;
+        w += 4 * (uint32_t)S.l2.size();
         S.lst_idx = w;
         w += (uint32_t)S.lst.size();
     }
@@ -532,22 +537,22 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     pl.smem_bytes = (uint32_t)align16(pl.hll_off + 4 * pl.hll_bytes);
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
-    if (w > kBaseMask) return fail(GACE_EUNSUPPORTED, "probe plan too large for 24-bit bucket indices");
+    if (4 * w > kBaseMask) return fail(GACE_EUNSUPPORTED, "probe plan too large for 24-bit bucket addresses");
 
     // ---- fill the image (absolute shared-memory indices)
     pl.image.assign((size_t)image_words * 4, 0);
-    uint2 *img2 = reinterpret_cast<uint2 *>(pl.image.data());
+    uint4 *img4 = reinterpret_cast<uint4 *>(pl.image.data());
     uint32_t *img32 = reinterpret_cast<uint32_t *>(pl.image.data());
-    auto fix = [&](uint2 e, const SlotPlan &S) {
-        if (!(e.x & kSpecial)) { e.x += S.hist_idx; return e; }
-        if (e.x & kList) { e.x += S.hist_idx; e.y += S.lst_idx; return e; }
+    auto fix = [&](uint4 e, const SlotPlan &S) {   // relative bucket numbers -> counter byte addresses
+        if (!(e.x & kSpecial)) { e.x = S.hist_addr() + 4 * e.x; return e; }
+        if (e.x & kList) { e.x = (e.x & ~kBaseMask) | (S.hist_addr() + 4 * (e.x & kBaseMask)); e.y += S.lst_idx; return e; }
         e.y += S.l2_idx;
         return e;
     };
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        for (size_t k = 0; k < S.l1.size(); ++k) img2[S.lut_idx + k] = fix(S.l1[k], S);
-        for (size_t k = 0; k < S.l2.size(); ++k) img2[S.l2_idx + k] = fix(S.l2[k], S);
+        for (size_t k = 0; k < S.l1.size(); ++k) img4[S.lut_idx + k] = fix(S.l1[k], S);
+        for (size_t k = 0; k < S.l2.size(); ++k) img4[S.l2_idx + k] = fix(S.l2[k], S);
         for (size_t k = 0; k < S.lst.size(); ++k) img32[S.lst_idx + k] = S.lst[k];
     }
     for (auto &G : pl.groups) {
@@ -555,9 +560,9 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         const SlotPlan &A = pl.slots[G.a], &B = pl.slots[G.b];
         for (uint32_t r = 0; r < A.nb; ++r) {
             const uint32_t sub = r == 0 ? 0 : count_le(G.TA, A.T[r - 1]);
-            img32[G.mapA_idx + r] = pl.acc_idx + G.grid_rel + sub * G.nbb;
+            img32[G.mapA_idx + r] = 4 * (pl.acc_idx + G.grid_rel + sub * G.nbb);
         }
-        for (uint32_t r = 0; r < B.nb; ++r) img32[G.mapB_idx + r] = r == 0 ? 0 : count_le(G.TB, B.T[r - 1]);
+        for (uint32_t r = 0; r < B.nb; ++r) img32[G.mapB_idx + r] = r == 0 ? 0 : 4 * count_le(G.TB, B.T[r - 1]);
     }
 
     // ---- finalize plan
@@ -611,11 +616,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                 DirectPair D{};
                 uint32_t lo, hi;
                 bucket_iv(pa, pl.slots[G.a].T, lo, hi);
-                D.la = lo + pl.slots[G.a].hist_idx;
-                D.ha = hi + pl.slots[G.a].hist_idx;
+                D.la = pl.slots[G.a].hist_addr() + 4 * lo;      // (empty: lo = 1 > hi = 0 stays empty)
+                D.ha = pl.slots[G.a].hist_addr() + 4 * hi;
                 bucket_iv(pb, pl.slots[G.b].T, lo, hi);
-                D.lb = lo + pl.slots[G.b].hist_idx;
-                D.hb = hi + pl.slots[G.b].hist_idx;
+                D.lb = pl.slots[G.b].hist_addr() + 4 * lo;
+                D.hb = pl.slots[G.b].hist_addr() + 4 * hi;
                 D.nega = na_;
                 D.negb = nb_;
                 dlist.push_back({(uint32_t)pl.gidx[std::make_pair(G.a, G.b)], q, D});
@@ -657,7 +662,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.mode = S.has_preds ? S.mode : (uint8_t)MODE_NOPRED;
         Q.has_hll = S.has_hll ? 1 : 0;
         Q.hll_idx = S.hll_idx;
-        Q.hist_idx = S.hist_idx;
+        Q.hist_addr = S.hist_addr();
         Q.base = S.base;
         Q.s1 = S.s1;
         Q.cell_mask = S.s1 >= 32 ? 0xFFFFFFFFu : (uint32_t)((1ull << S.s1) - 1);
@@ -685,8 +690,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         P.grp[g].dend = (uint16_t)dend[g];
         P.grp[g].has_grid = G.direct ? 0 : 1;
         if (!G.direct) {
-            P.grp[g].mapA_adj = (int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx;
-            P.grp[g].mapB_adj = (int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx;
+            P.grp[g].mapA_adj = 4 * ((int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx);
+            P.grp[g].mapB_adj = 4 * ((int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx);
         }
     }
     P.ngroups = (uint32_t)pl.groups.size();
@@ -1263,9 +1268,9 @@ namespace {
 struct CheckedTables {
     const std::vector<uint8_t> *img;
     mutable bool oob = false;
-    uint2 u2(uint32_t i) const {
-        if ((size_t)i * 8 + 8 > img->size()) { oob = true; return make_uint2(0, kNoThr); }
-        return reinterpret_cast<const uint2 *>(img->data())[i];
+    uint4 u4(uint32_t i) const {
+        if ((size_t)i * 16 + 16 > img->size()) { oob = true; return make_uint4(0, kNoThr, kNoThr, kNoThr); }
+        return reinterpret_cast<const uint4 *>(img->data())[i];
     }
     uint32_t u32(uint32_t i) const {
         if ((size_t)i * 4 + 4 > img->size()) { oob = true; return 0; }
@@ -1308,13 +1313,13 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         uint32_t ma = 0, mb = 0;
         for (uint32_t r = 0; r < pl.slots[G.a].nb; ++r) ma = std::max(ma, m32[G.mapA_idx + r]);
         for (uint32_t r = 0; r < pl.slots[G.b].nb; ++r) mb = std::max(mb, m32[G.mapB_idx + r]);
-        if (ma + mb >= pl.acc_idx + pl.acc_words) return fail(GACE_EUNSUPPORTED, "internal: grid map out of range");
+        if (ma + mb >= 4 * (pl.acc_idx + pl.acc_words)) return fail(GACE_EUNSUPPORTED, "internal: grid map out of range");
     }
     CheckedTables M{&pl.image};
     for (uint64_t k = 0; k < n; ++k) {
         uint32_t b;
         if (Q.mode == MODE_SEARCH) {
-            b = S.hist_idx + count_le(S.T, values[k]);
+            b = S.hist_addr() + 4 * count_le(S.T, values[k]);
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
@@ -1325,8 +1330,9 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
             b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
         }
         if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
-        if (b < S.hist_idx || b >= S.hist_idx + S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
-        out[k] = b - S.hist_idx;
+        if (b < S.hist_addr() || b >= S.hist_addr() + 4 * S.nb || (b & 3))
+            return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
+        out[k] = (b - S.hist_addr()) / 4;
     }
     return GACE_OK;
 }

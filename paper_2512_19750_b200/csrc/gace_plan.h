@@ -46,35 +46,37 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #define GACE_HD inline
 #endif
 
-// Absolute bucket index of offset u.  `M` reads the table image: M.u2(i) / M.u32(i)
-// (shared memory in the kernel; a bounds-checked copy in gace_debug_buckets).
+// Byte address (in shared memory) of the bucket counter of offset u.  `M` reads the
+// table image: M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy
+// in gace_debug_buckets).  Entry formats: see SlotParams below.
 template <class Mem>
 GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
     uint32_t s = s1;
-    uint2 e = M.u2(lut_idx + (u >> s));
-    while ((e.x & (kSpecial | kList)) == kSpecial) {        // sub-cell block (nested)
+    uint4 e = M.u4(lut_idx + (u >> s));
+    while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-cells (nested)
         const uint32_t sc = (e.x >> 24) & 63u;
-        e = M.u2(e.y + ((u & ((1u << s) - 1u)) >> sc));
+        e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
         s = sc;
     }
     if (e.x & kList) {
         uint32_t b = e.x & kBaseMask;
         const uint32_t n = (e.x >> 24) & 63u;
-        for (uint32_t i = 0; i < n; ++i) b += (u >= M.u32(e.y + i)) ? 1u : 0u;
+        for (uint32_t i = 0; i < n; ++i) b += (u >= M.u32(e.y + i)) ? 4u : 0u;
         return b;
     }
-    return (e.x & kBaseMask) + (u > e.y ? 1u : 0u);
+    return e.x + (u > e.y ? 4u : 0u) + (u > e.z ? 4u : 0u) + (u > e.w ? 4u : 0u);
 }
 
 enum SlotMode : uint8_t { MODE_LUT = 0, MODE_SEARCH = 1, MODE_NOPRED = 2 };
 
-// LUT entry (8 bytes), over the offset u = v - base of one column:
-//   direct : x = absolute u32 index of the cell's first bucket (bits 0..23),
-//            y = threshold, bucket = x + (u > y)        (at most one breakpoint in the cell)
-//   nested : x = kSpecial | sc << 24, y = uint2 index of a block of sub-cells of size
-//            2^sc; sub-entry = T2[y + ((u mod cell size) >> sc)] (any of the three kinds)
-//   list   : x = kSpecial | kList | n << 24 | first bucket, y = u32 index of n sorted
-//            breakpoint offsets t, bucket = first + #{t : u >= t}
+// LUT entry (16 bytes), over the offset u = v - base of one column.  Buckets are named
+// by the shared-memory BYTE address of their u32 counter (no scaling on the hot path).
+//   direct : x = address of the cell's first bucket, y <= z <= w = up to three
+//            thresholds (unused: ~0); bucket = x + 4 * #{t in (y, z, w) : u > t}
+//   nested : x = kSpecial | sc << 24, y = uint4 index of a block of sub-cells of size
+//            2^sc; sub-entry = T[y + ((u mod cell size) >> sc)] (any of the three kinds)
+//   list   : x = kSpecial | kList | n << 24 | first bucket address, y = u32 index of n
+//            sorted breakpoint offsets t, bucket = first + 4 * #{t : u >= t}
 struct SlotParams {
     const void *ptr;        // device column base for this launch
     const int64_t *bps;     // MODE_SEARCH: sorted breakpoints (device)
@@ -84,9 +86,9 @@ struct SlotParams {
     uint32_t nbp;           // MODE_SEARCH: number of breakpoints
     uint32_t s1;            // level-1 cell = u >> s1
     uint32_t cell_mask;     // (1 << s1) - 1
-    uint32_t lut_idx;       // level-1 table: uint2 index into shared memory
-    uint32_t l2_idx;        // level-2 table: uint2 index into shared memory
-    uint32_t hist_idx;      // u32 index of bucket 0 of this column's histogram
+    uint32_t lut_idx;       // level-1 table: uint4 index into shared memory
+    uint32_t l2_idx;        // nested sub-cell blocks: uint4 index into shared memory
+    uint32_t hist_addr;     // byte address of bucket 0 of this column's histogram
     uint32_t hll_idx;       // u32 index of this column's u32[4096] HLL registers, or kNone
     uint8_t dtype;          // 0 = int32, 1 = int64
     uint8_t mode;           // SlotMode
@@ -95,8 +97,8 @@ struct SlotParams {
 };
 
 struct GroupParams {
-    int32_t mapA_adj;       // u32 index of mapA minus hist_idx of slot a (indexed by absolute bucket)
-    int32_t mapB_adj;
+    int32_t mapA_adj;       // byte address of mapA minus hist_addr of slot a: map entry of a
+    int32_t mapB_adj;       //   bucket at [bucket address + adj]; values are grid byte offsets
     uint16_t dbeg, dend;    // this column pair's per-row ("direct") pairs: direct[dbeg .. dend)
     uint8_t a, b;           // slots, a < b
     uint8_t has_grid;       // 2-D grid in shared memory (else all its pairs are direct)
@@ -105,7 +107,7 @@ struct GroupParams {
 
 // Cross-column pair evaluated per row (fallback when a group's 2-D grid does not fit).
 struct DirectPair {
-    uint32_t la, ha;        // absolute bucket interval of the predicate on slot a (la > ha: empty)
+    uint32_t la, ha;        // bucket-address interval of the predicate on slot a (la > ha: empty)
     uint32_t lb, hb;        // ... on slot b
     uint32_t nega, negb;
     uint32_t acc_idx;       // u32 index of its counter in shared memory

@@ -54,6 +54,12 @@ extern __shared__ uint4 g_smem[];
 
 __device__ __forceinline__ uint32_t *smem32() { return reinterpret_cast<uint32_t *>(g_smem); }
 
+// u32 in shared memory at byte address a (bucket counters, maps and grids are addressed
+// in bytes so the hot loop never scales an index).
+__device__ __forceinline__ uint32_t *at(uint32_t a) {
+    return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(g_smem) + a);
+}
+
 // Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
 __device__ __noinline__ uint32_t hll_min(uint32_t hll_idx) {
     const uint4 *R = reinterpret_cast<const uint4 *>(smem32() + hll_idx);
@@ -80,7 +86,7 @@ __device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, i
 }
 
 struct SmemTables {
-    __device__ __forceinline__ uint2 u2(uint32_t i) const { return reinterpret_cast<const uint2 *>(g_smem)[i]; }
+    __device__ __forceinline__ uint4 u4(uint32_t i) const { return g_smem[i]; }
     __device__ __forceinline__ uint32_t u32(uint32_t i) const { return smem32()[i]; }
 };
 
@@ -172,13 +178,14 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
     return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
 }
 
-// Buckets (absolute shared-memory indices) of slots [S0, S0 + NB) over one row quad.
+// Buckets (counter byte addresses) of slots [S0, S0 + NB) over one row quad.  All
+// level-1 entries are read before any is used; a cell with <= 3 breakpoints resolves
+// branch-free; the rare nested / list / search cases take one branch.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
                                         uint32_t (&bk)[Sh::NC][4]) {
-    const uint2 *T = reinterpret_cast<const uint2 *>(g_smem);
     uint32_t u[NB][4];
-    uint2 e[NB][4];
+    uint4 e[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
@@ -186,21 +193,24 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            e[i][k] = lut ? T[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint2(0u, 0u);
+            e[i][k] = lut ? g_smem[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint4(0u, 0u, 0u, 0u);
         }
     }
     uint32_t spec = 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) spec |= e[i][k].x;
+        for (int k = 0; k < 4; ++k) {
+            spec |= e[i][k].x;
+            bk[S0 + i][k] = e[i][k].x + (u[i][k] > e[i][k].y ? 4u : 0u) + (u[i][k] > e[i][k].z ? 4u : 0u) +
+                            (u[i][k] > e[i][k].w ? 4u : 0u);
+        }
     if (spec & kSpecial) {
 #pragma unroll
         for (int i = 0; i < NB; ++i)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (e[i][k].x & kSpecial)
-                    e[i][k] = make_uint2(lut_bucket(P.slot[S0 + i].lut_idx, P.slot[S0 + i].s1, u[i][k]), kNoThr);
+                if (e[i][k].x & kSpecial) bk[S0 + i][k] = lut_bucket(P.slot[S0 + i].lut_idx, P.slot[S0 + i].s1, u[i][k]);
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -208,18 +218,17 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
         if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                e[i][k] = make_uint2(P.slot[s].hist_idx + search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]), kNoThr);
+                bk[s][k] = P.slot[s].hist_addr + 4 * search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) bk[s][k] = (e[i][k].x & kBaseMask) + (u[i][k] > e[i][k].y ? 1u : 0u);
     }
 }
 
-// 16-bit packed bucket ids for the generic shape's runtime loop over column pairs.
+// Bucket addresses packed 16 bits per column (address / 4 < 2^16) for the generic shape's
+// runtime loop over column pairs.
 template <int NC>
 __device__ __forceinline__ uint32_t pick(const uint64_t (&w)[(NC + 3) / 4][4], uint32_t s, int k) {
     const uint64_t x = (NC > 4 && (s & 4)) ? w[(NC + 3) / 4 - 1][k] : w[0][k];
-    return static_cast<uint32_t>(x >> (16 * (s & 3))) & 0xFFFFu;
+    return (static_cast<uint32_t>(x >> (16 * (s & 3))) & 0xFFFFu) << 2;
 }
 
 __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&ba)[4],
@@ -241,13 +250,12 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupPa
 
 __device__ __forceinline__ void grid_add(const GroupParams &G, const uint32_t (&ba)[4], const uint32_t (&bb)[4],
                                          uint32_t keep) {
-    uint32_t *sm = smem32();
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t ia = sm[G.mapA_adj + (int)ba[k]];
-            const uint32_t ib = sm[G.mapB_adj + (int)bb[k]];
-            atomicAdd(sm + ia + ib, 1u);
+            const uint32_t ia = *at(ba[k] + G.mapA_adj);    // grid row byte offset of a's sub-bucket
+            const uint32_t ib = *at(bb[k] + G.mapB_adj);    // column byte offset of b's sub-bucket
+            atomicAdd(at(ia + ib), 1u);
         }
     }
 }
@@ -255,7 +263,7 @@ __device__ __forceinline__ void grid_add(const GroupParams &G, const uint32_t (&
 // Everything one row quad contributes.  keep: one bit per row.
 template <class Sh>
 __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
-                                          uint32_t keep, const uint32_t (&lim)[Sh::NC]) {
+                                          uint32_t keep, const uint32_t (&lim_l)[Sh::NC]) {
     constexpr int NC = Sh::NC;
     uint32_t *sm = smem32();
     const uint32_t dbg = P.dbg;
@@ -272,39 +280,37 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
         if (!Sh::active(P, s) || Sh::mode(P, s) == MODE_NOPRED || (dbg & 2)) continue;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(sm + bk[s][k], 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(bk[s][k]), 1u);
     }
-    // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L,
-    // so the filter needs no clz; the (rare) survivors are checked against their register.
+    // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
+    // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
+    // which the rest of the loop leaves idle); survivors do a predicated ATOMS.MAX.
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
         if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
-        uint32_t idx[4], m = 0;
-        uint64_t w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            bool pass;
-            if (Sh::is32(P, s)) {
-                const uint32_t h = fmix32(static_cast<uint32_t>(v[s][k]));
-                idx[k] = h >> (32 - kHllP);
-                const uint32_t w32 = (h << kHllP) | (1u << (kHllP - 1));
-                w[k] = w32;
-                pass = w32 <= (0xFFFFFFFFu >> lim[s]);
-            } else {
-                const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
-                idx[k] = static_cast<uint32_t>(h >> (64 - kHllP));
-                w[k] = (h << kHllP) | (1ull << (kHllP - 1));
-                pass = w[k] <= (~0ull >> lim[s]);
-            }
-            m |= (((keep >> k) & 1u) && pass) ? (1u << k) : 0u;
-        }
-        if (m) {
-            uint32_t *R = sm + P.slot[s].hll_idx;
+        uint32_t *R = sm + P.slot[s].hll_idx;
+        if (Sh::is32(P, s)) {
+            const uint32_t lim = 0xFFFFFFFFu >> lim_l[s];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (!((m >> k) & 1u)) continue;
-                const uint32_t rk = Sh::is32(P, s) ? __clz(static_cast<uint32_t>(w[k])) + 1 : __clzll(w[k]) + 1;
-                if (rk > R[idx[k]] && !(dbg & 1)) atomicMax(R + idx[k], rk);
+                uint32_t h = static_cast<uint32_t>(v[s][k]);
+                h ^= __umulhi(h, 1u << 16);
+                h *= 0x85EBCA6BU;
+                h ^= __umulhi(h, 1u << 19);
+                h *= 0xC2B2AE35U;
+                h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
+                const uint32_t w32 = h * (1u << kHllP) + (1u << (kHllP - 1));
+                const uint32_t idx = __umulhi(h, 1u << kHllP);       // h >> (32 - p)
+                if (((keep >> k) & 1u) && w32 <= lim && !(dbg & 1)) atomicMax(R + idx, __clz(w32) + 1);
+            }
+        } else {
+            const uint64_t lim = ~0ull >> lim_l[s];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
+                const uint64_t w64 = (h << kHllP) | (1ull << (kHllP - 1));
+                const uint32_t idx = static_cast<uint32_t>(h >> (64 - kHllP));
+                if (((keep >> k) & 1u) && w64 <= lim && !(dbg & 1)) atomicMax(R + idx, __clzll(w64) + 1);
             }
         }
     }
@@ -325,7 +331,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             for (int k = 0; k < 4; ++k) {
                 uint64_t x = 0;
 #pragma unroll
-                for (int q = 0; q < 4 && 4 * h + q < NC; ++q) x |= static_cast<uint64_t>(bk[4 * h + q][k]) << (16 * q);
+                for (int q = 0; q < 4 && 4 * h + q < NC; ++q) x |= static_cast<uint64_t>(bk[4 * h + q][k] >> 2) << (16 * q);
                 ids[h][k] = x;
             }
         for (uint32_t g = 0; g < P.ngroups; ++g) {
