@@ -215,17 +215,21 @@ struct SlotPlan {
     bool has_preds = false, has_hll = false;
     int64_t dl = 0, dh = 0;
     std::vector<int64_t> T;            // sorted unique breakpoints
-    uint32_t nb = 1;
-    // LUT
+    uint32_t nb = 1;                   // buckets
+    // lookup table
     uint8_t mode = MODE_NOPRED;
     bool clamp = false;
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
     std::vector<uint4> l1, l2;         // entries with slot-relative indices (fixed up later)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
+    // roles in the pair grids
+    int hist_grp = -1;                 // group whose grid row sums give this column's histogram
+    int prim_b = -1;                   // group whose sub-bucket the entries pack
+    const std::vector<int64_t> *TBp = nullptr;   // that group's sub-bucket breakpoints
     // layout
-    uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_idx = 0, hll_idx = kNone, bps_off = 0, pre = 0;
-    uint32_t hist_addr() const { return 4 * hist_idx; }
+    uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_w = kNone, hll_idx = kNone, bps_off = 0;
+    uint32_t pre = 0, pre_stride = 1;  // finalize: bucket-count prefix of this column
 };
 
 uint32_t ceil_log2(uint64_t x) {
@@ -235,28 +239,32 @@ uint32_t ceil_log2(uint64_t x) {
 }
 
 // Build the lookup table of a slot for level-1 shift s1 over offsets u in [0, span]
-// (entry formats: gace_plan.h).  Entries hold RELATIVE bucket numbers and RELATIVE
-// sub-table / list indices here; make_plan adds the slot's shared-memory offsets.
-// A cell with <= 8 breakpoints is a leaf (direct or list); a denser cell points to a
-// block of uniform sub-cells, built recursively (shift strictly decreases).
+// (entry formats: gace_plan.h).  Entries hold RELATIVE sub-table / list indices here;
+// make_plan adds the slot's shared-memory offsets.  A cell with <= 3 breakpoints is a
+// direct entry (with the packed sub-bucket of the column's primary B role, if any), up to
+// 8 a list, a denser cell points to a block of uniform sub-cells built recursively.
 bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     std::vector<uint64_t> toff;
     toff.reserve(S.T.size());
     for (int64_t t : S.T) toff.push_back((uint64_t)t - (uint64_t)S.base);   // in [1, span]
     auto le = [&](uint64_t x) { return (uint32_t)(std::upper_bound(toff.begin(), toff.end(), x) - toff.begin()); };
+    // sub-bucket of bucket b in the packed group, and whether breakpoint T[i] cuts it
+    auto sub_of = [&](uint32_t b) -> uint32_t { return (!S.TBp || b == 0) ? 0 : count_le(*S.TBp, S.T[b - 1]); };
+    auto cuts = [&](uint32_t i) -> bool { return S.TBp && std::binary_search(S.TBp->begin(), S.TBp->end(), S.T[i]); };
     S.s1 = s1;
     S.l1.clear();
     S.l2.clear();
     S.lst.clear();
     bool ok = true;
-    // entry for offsets [lo, hi] of a cell of size 2^s
-    // entry for offsets [lo, hi] of a cell of size 2^s; relative bucket numbers here
     std::function<uint4(uint64_t, uint64_t, uint32_t)> node = [&](uint64_t lo, uint64_t hi, uint32_t s) -> uint4 {
         const uint32_t b0 = le(lo), b1 = le(hi), cnt = b1 - b0;   // breakpoints in (lo, hi]
         if (cnt <= 3) {
-            uint32_t t[3] = {kNoThr, kNoThr, kNoThr};
-            for (uint32_t i = 0; i < cnt; ++i) t[i] = (uint32_t)(toff[b0 + i] - 1);   // u > t  <=>  u >= toff
-            return make_uint4(b0, t[0], t[1], t[2]);
+            uint32_t t[3] = {kNoThr, kNoThr, kNoThr}, flags = 0;
+            for (uint32_t i = 0; i < cnt; ++i) {
+                t[i] = (uint32_t)(toff[b0 + i] - 1);               // u > t  <=>  u >= breakpoint
+                if (cuts(b0 + i)) flags |= 1u << (kIncShift + i);
+            }
+            return make_uint4(b0 | (sub_of(b0) << kSubShift) | flags, t[0], t[1], t[2]);
         }
         if (cnt <= 8 || s == 0) {
             uint4 e = make_uint4(kSpecial | kList | (cnt << 24) | b0, (uint32_t)S.lst.size(), 0, 0);
@@ -296,11 +304,13 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
 size_t lut_bytes(const SlotPlan &S) { return 16 * (S.l1.size() + S.l2.size()) + 4 * S.lst.size() + 32; }
 
 struct Group {
-    int a, b;                          // slots a < b
-    std::vector<int64_t> TA, TB;       // pair-relevant breakpoints (subsets of T_a, T_b)
-    uint32_t na = 1, nbb = 1;
-    bool direct = false;
-    uint32_t mapA_idx = 0, mapB_idx = 0, grid_rel = 0, sat = 0;
+    int a = -1, b = -1;                // oriented: a = full-resolution side, b = sub-bucket side
+    int s0, s1;                        // the two slots (s0 < s1), before orientation
+    std::vector<uint32_t> pq;          // its cross-column pairs
+    std::vector<int64_t> TB;           // sub-bucket breakpoints on b (b-side predicates of pq)
+    uint32_t na = 1, nbs = 1;
+    bool direct = false, packed = false;
+    uint32_t grid_w = 0, map_w = 0, sat = 0;
 };
 
 struct Plan {
@@ -362,66 +372,95 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         S.T.erase(std::unique(S.T.begin(), S.T.end()), S.T.end());
         S.nb = (uint32_t)S.T.size() + 1;
     }
-    // ---- pairs -> groups
-    pl.fpairs.resize(nq);
+    // ---- cross-column pairs -> groups (one per unordered column pair)
     for (uint32_t q = 0; q < nq; ++q) {
         const int si = pl.pslot[pairs[q].i], sj = pl.pslot[pairs[q].j];
         if (si == sj) continue;
-        const int a = std::min(si, sj), b = std::max(si, sj);
-        auto key = std::make_pair(a, b);
+        auto key = std::make_pair(std::min(si, sj), std::max(si, sj));
         if (!pl.gidx.count(key)) {
             pl.gidx[key] = (int)pl.groups.size();
             Group G;
-            G.a = a;
-            G.b = b;
+            G.s0 = key.first;
+            G.s1 = key.second;
             pl.groups.push_back(G);
         }
-        Group &G = pl.groups[pl.gidx[key]];
-        const uint32_t pa = (si == a) ? pairs[q].i : pairs[q].j;
-        const uint32_t pb = (si == a) ? pairs[q].j : pairs[q].i;
-        add_breakpoints(pl.iv[pa], pl.slots[a].dl, pl.slots[a].dh, G.TA);
-        add_breakpoints(pl.iv[pb], pl.slots[b].dl, pl.slots[b].dh, G.TB);
+        pl.groups[pl.gidx[key]].pq.push_back(q);
     }
-    size_t fixed = 0;
-    for (auto &S : pl.slots) {
-        if (S.has_preds) fixed += 4ull * S.nb;
+    auto side_bps = [&](const Group &G, int side) {      // breakpoints of G's predicates on `side`
+        std::vector<int64_t> TB;
+        for (uint32_t q : G.pq) {
+            const uint32_t p = pl.pslot[pairs[q].i] == side ? pairs[q].i : pairs[q].j;
+            add_breakpoints(pl.iv[p], pl.slots[side].dl, pl.slots[side].dh, TB);
+        }
+        std::sort(TB.begin(), TB.end());
+        TB.erase(std::unique(TB.begin(), TB.end()), TB.end());
+        return TB;
+    };
+    // orientation: prefer making a column the full-resolution side of one group (its
+    // histogram then comes from the grid) and the packed sub-bucket side of one group
+    {
+        std::vector<int> has_hist(pl.slots.size(), 0), has_prim(pl.slots.size(), 0);
+        for (auto &G : pl.groups) {
+            double best = -1e300;
+            for (int o = 0; o < 2; ++o) {
+                const int A = o ? G.s1 : G.s0, B = o ? G.s0 : G.s1;
+                std::vector<int64_t> TB = side_bps(G, B);
+                const double cells = (double)pl.slots[A].nb * (double)(TB.size() + 1);
+                const double score = 4.0 * !has_hist[A] + 2.0 * (!has_prim[B] && TB.size() + 1 <= kSubMax) - cells * 1e-6;
+                if (score > best) {
+                    best = score;
+                    G.a = A;
+                    G.b = B;
+                    G.TB.swap(TB);
+                }
+            }
+            G.na = pl.slots[G.a].nb;
+            G.nbs = (uint32_t)G.TB.size() + 1;
+            has_hist[G.a] = 1;
+            if (G.nbs <= kSubMax) has_prim[G.b] = 1;
+        }
+    }
+    // ---- budget: grids (+ the B side's bucket -> sub-bucket map) in increasing size while
+    // they fit with 4 KB per predicate column kept for its lookup table; the rest per row
+    size_t fixed = 256;
+    for (auto &S : pl.slots)
         if (S.has_hll) fixed += 4 * kHllM;
-    }
-    for (auto &G : pl.groups) {
-        std::sort(G.TA.begin(), G.TA.end());
-        G.TA.erase(std::unique(G.TA.begin(), G.TA.end()), G.TA.end());
-        std::sort(G.TB.begin(), G.TB.end());
-        G.TB.erase(std::unique(G.TB.begin(), G.TB.end()), G.TB.end());
-        G.na = (uint32_t)G.TA.size() + 1;
-        G.nbb = (uint32_t)G.TB.size() + 1;
-    }
-    // grids in increasing size while they fit (keeping 4 KB per column with predicates for
-    // its lookup table); the groups left over are evaluated per row ("direct")
     size_t lut_reserve = 0;
-    for (auto &S : pl.slots) lut_reserve += S.has_preds ? 4096 : 0;
+    for (auto &S : pl.slots) {
+        lut_reserve += S.has_preds ? 4096 : 0;
+        fixed += S.has_preds ? 4ull * S.nb : 0;        // worst case: every column keeps its own histogram
+    }
     {
         std::vector<int> order(pl.groups.size());
         for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
         std::sort(order.begin(), order.end(), [&](int x, int y) {
-            return (uint64_t)pl.groups[x].na * pl.groups[x].nbb < (uint64_t)pl.groups[y].na * pl.groups[y].nbb;
+            return (uint64_t)pl.groups[x].na * pl.groups[x].nbs < (uint64_t)pl.groups[y].na * pl.groups[y].nbs;
         });
         size_t used = 0;
         for (int gi : order) {
             Group &G = pl.groups[gi];
-            const size_t need = 4ull * ((uint64_t)G.na * G.nbb + pl.slots[G.a].nb + pl.slots[G.b].nb) + 64;
+            const size_t need = 4ull * ((uint64_t)G.na * G.nbs + pl.slots[G.b].nb) + 64;
             if (fixed + used + need + lut_reserve <= kSmemBudget) used += need;
             else G.direct = true;
         }
         fixed += used;
     }
     size_t ndirect = 0;
-    for (uint32_t q = 0; q < nq; ++q) {
-        const int si = pl.pslot[pairs[q].i], sj = pl.pslot[pairs[q].j];
-        if (si != sj && pl.groups[pl.gidx[std::make_pair(std::min(si, sj), std::max(si, sj))]].direct) ++ndirect;
-    }
-    fixed += 4 * ndirect + 256;
+    for (auto &G : pl.groups) ndirect += G.direct ? G.pq.size() : 0;
+    fixed += 4 * ndirect;
     if (fixed > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory (" + std::to_string(fixed) + " B)");
+    // roles among the groups that got a grid
+    for (size_t g = 0; g < pl.groups.size(); ++g) {
+        Group &G = pl.groups[g];
+        if (G.direct) continue;
+        if (pl.slots[G.a].hist_grp < 0) pl.slots[G.a].hist_grp = (int)g;
+        if (G.nbs <= kSubMax && pl.slots[G.b].prim_b < 0) {
+            pl.slots[G.b].prim_b = (int)g;
+            pl.slots[G.b].TBp = &G.TB;
+            G.packed = true;
+        }
+    }
 
     // ---- lookup tables within the remaining budget
     const size_t lut_budget = kSmemBudget - fixed;
@@ -480,7 +519,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         }
         if (tot <= lut_budget || worst < 0) break;
         SlotPlan &S = pl.slots[worst];
-        // a coarser level 1 roughly halves it; when level 2 / lists dominate (dense
+        // a coarser level 1 roughly halves it; when nested blocks / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
         if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 16 * S.l1.size()) {
             to_search(S);
@@ -489,7 +528,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (!build_lut(S, span_of(S), ++s1[worst])) to_search(S);
     }
 
-    // ---- layout: image [per slot: L1 | L2 | lists][group maps] | acc [hists][grids][direct] | hll
+    // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] | hll
     uint32_t w = 0;    // u32 cursor
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
@@ -504,23 +543,21 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     w = (w + 3) & ~3u;
     for (auto &G : pl.groups) {
         if (G.direct) continue;
-        G.mapA_idx = w;
-        w += pl.slots[G.a].nb;
-        G.mapB_idx = w;
+        G.map_w = w;
         w += pl.slots[G.b].nb;
     }
     w = (w + 3) & ~3u;
     const uint32_t image_words = w;
     pl.acc_idx = w;
     for (auto &S : pl.slots) {
-        if (!S.has_preds) continue;
-        S.hist_idx = w;
+        if (!S.has_preds || S.hist_grp >= 0) continue;
+        S.hist_w = w;
         w += S.nb;
     }
     for (auto &G : pl.groups) {
         if (G.direct) continue;
-        G.grid_rel = w - pl.acc_idx;
-        w += G.na * G.nbb;
+        G.grid_w = w;
+        w += G.na * G.nbs;
     }
     const uint32_t direct_idx = w;
     w += (uint32_t)ndirect;
@@ -537,16 +574,15 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     pl.smem_bytes = (uint32_t)align16(pl.hll_off + 4 * pl.hll_bytes);
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
-    if (4 * w > kBaseMask) return fail(GACE_EUNSUPPORTED, "probe plan too large for 24-bit bucket addresses");
 
     // ---- fill the image (absolute shared-memory indices)
     pl.image.assign((size_t)image_words * 4, 0);
     uint4 *img4 = reinterpret_cast<uint4 *>(pl.image.data());
     uint32_t *img32 = reinterpret_cast<uint32_t *>(pl.image.data());
-    auto fix = [&](uint4 e, const SlotPlan &S) {   // relative bucket numbers -> counter byte addresses
-        if (!(e.x & kSpecial)) { e.x = S.hist_addr() + 4 * e.x; return e; }
-        if (e.x & kList) { e.x = (e.x & ~kBaseMask) | (S.hist_addr() + 4 * (e.x & kBaseMask)); e.y += S.lst_idx; return e; }
-        e.y += S.l2_idx;
+    auto fix = [&](uint4 e, const SlotPlan &S) {   // relative sub-table / list indices -> absolute
+        if (!(e.x & kSpecial)) return e;
+        if (e.x & kList) e.y += S.lst_idx;
+        else e.y += S.l2_idx;
         return e;
     };
     for (auto &S : pl.slots) {
@@ -557,27 +593,30 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     }
     for (auto &G : pl.groups) {
         if (G.direct) continue;
-        const SlotPlan &A = pl.slots[G.a], &B = pl.slots[G.b];
-        for (uint32_t r = 0; r < A.nb; ++r) {
-            const uint32_t sub = r == 0 ? 0 : count_le(G.TA, A.T[r - 1]);
-            img32[G.mapA_idx + r] = 4 * (pl.acc_idx + G.grid_rel + sub * G.nbb);
-        }
-        for (uint32_t r = 0; r < B.nb; ++r) img32[G.mapB_idx + r] = r == 0 ? 0 : 4 * count_le(G.TB, B.T[r - 1]);
+        const SlotPlan &B = pl.slots[G.b];
+        for (uint32_t r = 0; r < B.nb; ++r) img32[G.map_w + r] = r == 0 ? 0 : count_le(G.TB, B.T[r - 1]);
     }
 
     // ---- finalize plan
     uint32_t pre = 0;
     for (auto &S : pl.slots) {
-        if (!S.has_preds) continue;
+        if (!S.has_preds || S.hist_grp >= 0) continue;
         S.pre = pre;
-        pl.jobs.push_back(FinJob{JOB_HIST, S.hist_idx - pl.acc_idx, pre, 0, S.nb});
+        S.pre_stride = 1;
+        pl.jobs.push_back(FinJob{JOB_HIST, S.hist_w - pl.acc_idx, pre, 0, S.nb});
         pre += S.nb + 1;
     }
     for (auto &G : pl.groups) {
         if (G.direct) continue;
         G.sat = pre;
-        pl.jobs.push_back(FinJob{JOB_SAT, G.grid_rel, pre, G.na, G.nbb});
-        pre += (G.na + 1) * (G.nbb + 1);
+        pl.jobs.push_back(FinJob{JOB_SAT, G.grid_w - pl.acc_idx, pre, G.na, G.nbs});
+        pre += (G.na + 1) * (G.nbs + 1);
+    }
+    for (auto &S : pl.slots) {           // grid-provided histograms: the SAT's last column
+        if (S.hist_grp < 0) continue;
+        const Group &G = pl.groups[S.hist_grp];
+        S.pre = G.sat + G.nbs;
+        S.pre_stride = G.nbs + 1;
     }
     pl.pre_words = pre;
     auto bucket_iv = [&](uint32_t p, const std::vector<int64_t> &T, uint32_t &lo, uint32_t &hi) {
@@ -585,15 +624,18 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         lo = count_le(T, pl.iv[p].lo);
         hi = count_le(T, pl.iv[p].hi);
     };
+    auto negated = [&](uint32_t p) -> uint32_t { return (preds[p].flags & GACE_PRED_NEGATE) ? 1 : 0; };
     pl.fpreds.resize(np);
     for (uint32_t p = 0; p < np; ++p) {
         const SlotPlan &S = pl.slots[pl.pslot[p]];
         FinPred F{};
         F.pre = S.pre;
+        F.stride = S.pre_stride;
         bucket_iv(p, S.T, F.lo, F.hi);
-        F.neg = (preds[p].flags & GACE_PRED_NEGATE) ? 1 : 0;
+        F.neg = negated(p);
         pl.fpreds[p] = F;
     }
+    pl.fpairs.resize(nq);
     struct DEnt { uint32_t g, q; DirectPair D; };
     std::vector<DEnt> dlist;
     for (uint32_t q = 0; q < nq; ++q) {
@@ -603,37 +645,32 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (si == sj) {
             F.kind = PAIR_SAME;
             F.pre = pl.slots[si].pre;
+            F.stride = pl.slots[si].pre_stride;
             bucket_iv(i, pl.slots[si].T, F.li, F.hi);
             bucket_iv(j, pl.slots[sj].T, F.lj, F.hj);
-            F.negi = (preds[i].flags & GACE_PRED_NEGATE) ? 1 : 0;
-            F.negj = (preds[j].flags & GACE_PRED_NEGATE) ? 1 : 0;
+            F.negi = negated(i);
+            F.negj = negated(j);
         } else {
-            const Group &G = pl.groups[pl.gidx[std::make_pair(std::min(si, sj), std::max(si, sj))]];
+            const int g = pl.gidx[std::make_pair(std::min(si, sj), std::max(si, sj))];
+            const Group &G = pl.groups[g];
             const uint32_t pa = (si == G.a) ? i : j, pb = (si == G.a) ? j : i;
-            const uint32_t na_ = (preds[pa].flags & GACE_PRED_NEGATE) ? 1 : 0;
-            const uint32_t nb_ = (preds[pb].flags & GACE_PRED_NEGATE) ? 1 : 0;
             if (G.direct) {
                 DirectPair D{};
-                uint32_t lo, hi;
-                bucket_iv(pa, pl.slots[G.a].T, lo, hi);
-                D.la = pl.slots[G.a].hist_addr() + 4 * lo;      // (empty: lo = 1 > hi = 0 stays empty)
-                D.ha = pl.slots[G.a].hist_addr() + 4 * hi;
-                bucket_iv(pb, pl.slots[G.b].T, lo, hi);
-                D.lb = pl.slots[G.b].hist_addr() + 4 * lo;
-                D.hb = pl.slots[G.b].hist_addr() + 4 * hi;
-                D.nega = na_;
-                D.negb = nb_;
-                dlist.push_back({(uint32_t)pl.gidx[std::make_pair(G.a, G.b)], q, D});
+                bucket_iv(pa, pl.slots[G.a].T, D.la, D.ha);
+                bucket_iv(pb, pl.slots[G.b].T, D.lb, D.hb);
+                D.nega = negated(pa);
+                D.negb = negated(pb);
+                dlist.push_back({(uint32_t)g, q, D});
                 F.kind = PAIR_DIRECT;
             } else {
                 F.kind = PAIR_GRID;
                 F.pre = G.sat;
                 F.na = G.na;
-                F.nb = G.nbb;
-                bucket_iv(pa, G.TA, F.li, F.hi);
-                bucket_iv(pb, G.TB, F.lj, F.hj);
-                F.negi = na_;
-                F.negj = nb_;
+                F.nb = G.nbs;
+                bucket_iv(pa, pl.slots[G.a].T, F.li, F.hi);     // full resolution on A
+                bucket_iv(pb, G.TB, F.lj, F.hj);                // sub-buckets on B
+                F.negi = negated(pa);
+                F.negj = negated(pb);
             }
         }
         pl.fpairs[q] = F;
@@ -662,12 +699,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.mode = S.has_preds ? S.mode : (uint8_t)MODE_NOPRED;
         Q.has_hll = S.has_hll ? 1 : 0;
         Q.hll_idx = S.hll_idx;
-        Q.hist_addr = S.hist_addr();
+        Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
+        Q.prim_b = (int8_t)S.prim_b;
         Q.base = S.base;
         Q.s1 = S.s1;
-        Q.cell_mask = S.s1 >= 32 ? 0xFFFFFFFFu : (uint32_t)((1ull << S.s1) - 1);
         Q.lut_idx = S.lut_idx;
-        Q.l2_idx = S.l2_idx;
         if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
         else { Q.clamp_lo = INT64_MIN; Q.clamp_hi = INT64_MAX; }
         if (S.has_preds && S.mode == MODE_LUT && S.clamp) {
@@ -684,15 +720,16 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     }
     for (size_t g = 0; g < pl.groups.size(); ++g) {
         const Group &G = pl.groups[g];
-        P.grp[g].a = (uint8_t)G.a;
-        P.grp[g].b = (uint8_t)G.b;
-        P.grp[g].dbeg = (uint16_t)dbeg[g];
-        P.grp[g].dend = (uint16_t)dend[g];
-        P.grp[g].has_grid = G.direct ? 0 : 1;
-        if (!G.direct) {
-            P.grp[g].mapA_adj = 4 * ((int32_t)G.mapA_idx - (int32_t)pl.slots[G.a].hist_idx);
-            P.grp[g].mapB_adj = 4 * ((int32_t)G.mapB_idx - (int32_t)pl.slots[G.b].hist_idx);
-        }
+        GroupParams &R = P.grp[g];
+        R.a = (uint8_t)G.a;
+        R.b = (uint8_t)G.b;
+        R.dbeg = (uint16_t)dbeg[g];
+        R.dend = (uint16_t)dend[g];
+        R.has_grid = G.direct ? 0 : 1;
+        R.packed = G.packed ? 1 : 0;
+        R.nbs = G.nbs;
+        R.grid_addr = G.direct ? kNone : 4 * G.grid_w;
+        R.map_addr = G.direct ? kNone : 4 * G.map_w;
     }
     P.ngroups = (uint32_t)pl.groups.size();
     P.ndirect = (uint32_t)pl.direct.size();
@@ -865,6 +902,10 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64) {
          chain([&](int i) { return std::string(P.slot[i].has_hll ? "1" : "0"); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool clamp(const ProbeParams &) { return " +
          std::string(P.clamp ? "true" : "false") + "; }\n";
+    o += "  __device__ static constexpr bool packs(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].prim_b >= 0 ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool ownh(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].mode != MODE_NOPRED && P.slot[i].hist_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
     auto gchain = [&](auto f) {
         std::string r;
         for (uint32_t g = 0; g < P.ngroups; ++g) r += "g == " + std::to_string(g) + " ? " + f(g) + " : ";
@@ -872,6 +913,7 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64) {
     };
     o += "  __device__ static constexpr int ga(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].a); }) + "; }\n";
     o += "  __device__ static constexpr int gb(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].b); }) + "; }\n";
+    o += "  __device__ static constexpr bool gpacked(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].packed ? "1" : "0"); }) + "; }\n";
     o += "  __device__ static constexpr bool ggrid(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].has_grid ? "1" : "0"); }) + "; }\n";
     o += "  __device__ static constexpr bool gdirect(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].dend > P.grp[g].dbeg ? "1" : "0"); }) + "; }\n";
     o += "};\n}  // namespace gace\n";
@@ -1306,20 +1348,20 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
     if (mode) *mode = Q.mode;
     if (nbp) *nbp = (uint32_t)S.T.size();
     for (uint32_t i = 0; bps && i < S.T.size() && i < cap; ++i) bps[i] = S.T[i];
-    // static layout checks: every map entry of every grid lands inside the accumulators
+    // static layout checks: every grid cell a (bucket, sub-bucket) pair can address lies
+    // inside the accumulators, and every map entry is a valid sub-bucket
     for (const Group &G : pl.groups) {
         if (G.direct) continue;
         const uint32_t *m32 = reinterpret_cast<const uint32_t *>(pl.image.data());
-        uint32_t ma = 0, mb = 0;
-        for (uint32_t r = 0; r < pl.slots[G.a].nb; ++r) ma = std::max(ma, m32[G.mapA_idx + r]);
-        for (uint32_t r = 0; r < pl.slots[G.b].nb; ++r) mb = std::max(mb, m32[G.mapB_idx + r]);
-        if (ma + mb >= 4 * (pl.acc_idx + pl.acc_words)) return fail(GACE_EUNSUPPORTED, "internal: grid map out of range");
+        for (uint32_t r = 0; r < pl.slots[G.b].nb; ++r)
+            if (m32[G.map_w + r] >= G.nbs) return fail(GACE_EUNSUPPORTED, "internal: sub-bucket map out of range");
+        if (G.grid_w + G.na * G.nbs > pl.acc_idx + pl.acc_words) return fail(GACE_EUNSUPPORTED, "internal: grid out of range");
     }
     CheckedTables M{&pl.image};
     for (uint64_t k = 0; k < n; ++k) {
         uint32_t b;
         if (Q.mode == MODE_SEARCH) {
-            b = S.hist_addr() + 4 * count_le(S.T, values[k]);
+            b = count_le(S.T, values[k]);
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
@@ -1330,9 +1372,20 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
             b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
         }
         if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
-        if (b < S.hist_addr() || b >= S.hist_addr() + 4 * S.nb || (b & 3))
-            return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
-        out[k] = (b - S.hist_addr()) / 4;
+        if (b >= S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
+        out[k] = b;
+        // the packed sub-bucket of a direct entry must agree with the group's map
+        if (Q.mode == MODE_LUT && S.prim_b >= 0) {
+            const Group &G = pl.groups[S.prim_b];
+            const uint32_t u = Q.dtype == GACE_I32
+                ? (uint32_t)std::min(std::max((int32_t)values[k], pl.clamp ? (int32_t)Q.clamp_lo : INT32_MIN),
+                                     pl.clamp ? (int32_t)Q.clamp_hi : INT32_MAX) - (uint32_t)Q.base
+                : (uint32_t)((uint64_t)std::min(std::max(values[k], pl.clamp ? Q.clamp_lo : INT64_MIN),
+                                                pl.clamp ? Q.clamp_hi : INT64_MAX) - (uint64_t)Q.base);
+            const uint32_t sub = entry_sub(lut_entry(M, Q.lut_idx, Q.s1, u), u);
+            const uint32_t want = reinterpret_cast<const uint32_t *>(pl.image.data())[G.map_w + b];
+            if (sub != kNone && sub != want) return fail(GACE_EUNSUPPORTED, "internal: packed sub-bucket differs from the map");
+        }
     }
     return GACE_OK;
 }

@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
     }
 }
 
-__device__ __forceinline__ unsigned long long iv(const unsigned long long *pre, uint32_t lo, uint32_t hi) {
-    return lo <= hi ? pre[hi + 1] - pre[lo] : 0ull;
+// count of buckets [lo, hi] from a bucket-count prefix P(b) = pre[b * stride]
+__device__ __forceinline__ unsigned long long iv(const unsigned long long *pre, uint32_t stride, uint32_t lo,
+                                                 uint32_t hi) {
+    return lo <= hi ? pre[(size_t)(hi + 1) * stride] - pre[(size_t)lo * stride] : 0ull;
 }
 
 __device__ __forceinline__ unsigned long long rect(const unsigned long long *S, uint32_t st, uint32_t r0,
@@ -134,7 +136,7 @@ __global__ void fin_output(const FinParams F) {
     if (t == 0) F.out[0] = n;
     if (t >= 1 && t <= F.npreds) {
         const FinPred p = F.preds[t - 1];
-        const unsigned long long c = iv(F.g_pre + p.pre, p.lo, p.hi);
+        const unsigned long long c = iv(F.g_pre + p.pre, p.stride, p.lo, p.hi);
         F.out[t] = p.neg ? n - c : c;
     } else if (t > F.npreds && t <= F.npreds + F.npairs) {
         const FinPair q = F.pairs[t - 1 - F.npreds];
@@ -144,7 +146,8 @@ __global__ void fin_output(const FinParams F) {
         } else if (q.kind == PAIR_SAME) {
             const unsigned long long *pre = F.g_pre + q.pre;
             const uint32_t lo = max(q.li, q.lj), hi = min(q.hi, q.hj);
-            r = combine(n, iv(pre, q.li, q.hi), iv(pre, q.lj, q.hj), iv(pre, lo, hi), q.negi, q.negj);
+            r = combine(n, iv(pre, q.stride, q.li, q.hi), iv(pre, q.stride, q.lj, q.hj), iv(pre, q.stride, lo, hi),
+                        q.negi, q.negj);
         } else {
             const unsigned long long *S = F.g_pre + q.pre;
             const uint32_t st = q.nb + 1;

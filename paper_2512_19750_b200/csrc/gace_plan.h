@@ -1,16 +1,19 @@
-// gace_plan.h -- internal plan layout shared by the host planner (gace_host.cpp)
-// and the sm_100a kernels (gace_kernels.cu).  Not part of the C-ABI.
+// gace_plan.h -- internal plan layout shared by the host planner (gace_host.cpp), the
+// sm_100a kernels (gace_kernels.cu, gace_probe.cuh) and NVRTC (gace_jit.cpp).  Not part
+// of the C-ABI.
 //
 // The planner turns a predicate batch into, per probed column ("slot"):
-//   * the sorted breakpoints T of all its predicates (interval ends lo and hi+1,
-//     clipped to the column's value domain), so that every predicate is a
-//     contiguous bucket range of  bucket(v) = #{t in T : t <= v};
-//   * a two-level lookup table over the offset u = v - base that resolves
-//     bucket(v) with one shared-memory load and one compare;
-//   * a u32 shared-memory histogram over the buckets (counts are prefix sums);
-// and, per pair of probed columns carrying cross-column pairs ("group"), a 2-D
-// histogram over the sub-buckets of only the pair-relevant predicates (joints are
-// rectangle sums).  HLL registers live in shared memory as u8[4096] per column.
+//   * the sorted breakpoints T of all its predicates (interval ends lo and hi+1, clipped
+//     to the column's value domain), so every predicate is a contiguous range of
+//     bucket(v) = #{t in T : t <= v};
+//   * a lookup table over the offset u = v - base that resolves bucket(v) with one
+//     16-byte shared-memory load and three compares;
+// and, per pair of probed columns carrying cross-column pairs ("group"), a 2-D histogram
+// grid[bucket of the A column][sub-bucket of the B column], the sub-buckets being cut only
+// by the B-side predicates of that group's pairs.  Joints are rectangle sums of the grid;
+// the grid's row sums are the A column's bucket histogram, so a column that is the A side
+// of a group needs no histogram of its own.  The sub-bucket of a column's primary B role
+// is packed into its lookup-table entries.  HLL registers live in shared memory as u32.
 #pragma once
 #ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>   // uint2 / uint4
@@ -34,10 +37,13 @@ constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
 constexpr int kThreads = 512;          // probe CTA size (one CTA per SM, <= 128 registers)
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
-constexpr uint32_t kSpecial = 0x80000000u;  // entry is a level-2 pointer or a list
+constexpr uint32_t kSpecial = 0x80000000u;  // entry is a nested block or a list
 constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list
-constexpr uint32_t kBaseMask = 0x00FFFFFFu;
-constexpr uint32_t kListMax = 63;
+constexpr uint32_t kIdxMask = 0x3FFFu;      // bucket index field (<= 8193 buckets)
+constexpr uint32_t kSubShift = 14;          // packed sub-bucket field: bits 14..20
+constexpr uint32_t kSubMask = 0x7Fu;
+constexpr uint32_t kSubMax = 127;           // sub-buckets per group side that can be packed
+constexpr uint32_t kIncShift = 21;          // sub-bucket increment flags of the 3 thresholds
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 #if defined(__CUDACC__)
@@ -46,11 +52,21 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #define GACE_HD inline
 #endif
 
-// Byte address (in shared memory) of the bucket counter of offset u.  `M` reads the
-// table image: M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy
-// in gace_debug_buckets).  Entry formats: see SlotParams below.
+// LUT entry (16 bytes), over the offset u = v - base of one column:
+//   direct : x = first bucket index (bits 0..13) | packed sub-bucket of that bucket
+//            (bits 14..20) | flags (bits 21..23): threshold i also cuts the sub-buckets;
+//            y <= z <= w = up to three thresholds (unused: ~0).
+//            bucket = x.idx + #{t in (y, z, w) : u > t};  sub = x.sub + #{flagged t : u > t}
+//   nested : x = kSpecial | sc << 24, y = uint4 index of a block of sub-cells of size
+//            2^sc; sub-entry = T[y + ((u mod cell size) >> sc)] (any of the three kinds)
+//   list   : x = kSpecial | kList | n << 24 | first bucket index, y = u32 index of n sorted
+//            breakpoint offsets t; bucket = first + #{t : u >= t} (sub-bucket via the map)
+//
+// Final (direct or list) entry for offset u, walking nested blocks.  `M` reads the table
+// image: M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy in
+// gace_debug_buckets).
 template <class Mem>
-GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
+GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
     uint32_t s = s1;
     uint4 e = M.u4(lut_idx + (u >> s));
     while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-cells (nested)
@@ -58,56 +74,61 @@ GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_
         e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
         s = sc;
     }
+    return e;
+}
+
+// Bucket index of offset u (full walk).
+template <class Mem>
+GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
+    const uint4 e = lut_entry(M, lut_idx, s1, u);
+    uint32_t b = e.x & kIdxMask;
     if (e.x & kList) {
-        uint32_t b = e.x & kBaseMask;
         const uint32_t n = (e.x >> 24) & 63u;
-        for (uint32_t i = 0; i < n; ++i) b += (u >= M.u32(e.y + i)) ? 4u : 0u;
+        for (uint32_t i = 0; i < n; ++i) b += (u >= M.u32(e.y + i)) ? 1u : 0u;
         return b;
     }
-    return e.x + (u > e.y ? 4u : 0u) + (u > e.z ? 4u : 0u) + (u > e.w ? 4u : 0u);
+    return b + (u > e.y ? 1u : 0u) + (u > e.z ? 1u : 0u) + (u > e.w ? 1u : 0u);
+}
+
+// Packed sub-bucket of offset u from a DIRECT entry (kNone for a list entry).
+GACE_HD uint32_t entry_sub(const uint4 &e, uint32_t u) {
+    if (e.x & kSpecial) return kNone;
+    return ((e.x >> kSubShift) & kSubMask) + ((u > e.y && (e.x >> kIncShift) & 1u) ? 1u : 0u) +
+           ((u > e.z && (e.x >> (kIncShift + 1)) & 1u) ? 1u : 0u) + ((u > e.w && (e.x >> (kIncShift + 2)) & 1u) ? 1u : 0u);
 }
 
 enum SlotMode : uint8_t { MODE_LUT = 0, MODE_SEARCH = 1, MODE_NOPRED = 2 };
 
-// LUT entry (16 bytes), over the offset u = v - base of one column.  Buckets are named
-// by the shared-memory BYTE address of their u32 counter (no scaling on the hot path).
-//   direct : x = address of the cell's first bucket, y <= z <= w = up to three
-//            thresholds (unused: ~0); bucket = x + 4 * #{t in (y, z, w) : u > t}
-//   nested : x = kSpecial | sc << 24, y = uint4 index of a block of sub-cells of size
-//            2^sc; sub-entry = T[y + ((u mod cell size) >> sc)] (any of the three kinds)
-//   list   : x = kSpecial | kList | n << 24 | first bucket address, y = u32 index of n
-//            sorted breakpoint offsets t, bucket = first + 4 * #{t : u >= t}
 struct SlotParams {
     const void *ptr;        // device column base for this launch
     const int64_t *bps;     // MODE_SEARCH: sorted breakpoints (device)
     int64_t base;           // u = (uint32)(v - base)
-    int64_t clamp_lo;       // CLAMP kernels: v = min(max(v, clamp_lo), clamp_hi)
+    int64_t clamp_lo;       // clamped plans: v = min(max(v, clamp_lo), clamp_hi)
     int64_t clamp_hi;
     uint32_t nbp;           // MODE_SEARCH: number of breakpoints
     uint32_t s1;            // level-1 cell = u >> s1
-    uint32_t cell_mask;     // (1 << s1) - 1
     uint32_t lut_idx;       // level-1 table: uint4 index into shared memory
-    uint32_t l2_idx;        // nested sub-cell blocks: uint4 index into shared memory
-    uint32_t hist_addr;     // byte address of bucket 0 of this column's histogram
+    uint32_t hist_addr;     // byte address of bucket 0 of this column's own histogram, or kNone
     uint32_t hll_idx;       // u32 index of this column's u32[4096] HLL registers, or kNone
     uint8_t dtype;          // 0 = int32, 1 = int64
     uint8_t mode;           // SlotMode
     uint8_t has_hll;
-    uint8_t pad;
+    int8_t prim_b;          // group whose sub-bucket this column's entries pack, or -1
 };
 
 struct GroupParams {
-    int32_t mapA_adj;       // byte address of mapA minus hist_addr of slot a: map entry of a
-    int32_t mapB_adj;       //   bucket at [bucket address + adj]; values are grid byte offsets
+    uint32_t grid_addr;     // byte address of grid[0][0]; grid[i][j] at + 4 * (i * nbs + j)
+    uint32_t nbs;           // sub-buckets on the B side
+    uint32_t map_addr;      // byte address of the B column's bucket -> sub-bucket map (u32 each)
     uint16_t dbeg, dend;    // this column pair's per-row ("direct") pairs: direct[dbeg .. dend)
-    uint8_t a, b;           // slots, a < b
+    uint8_t a, b;           // slots: a = full-resolution side, b = sub-bucket side
     uint8_t has_grid;       // 2-D grid in shared memory (else all its pairs are direct)
-    uint8_t pad;
+    uint8_t packed;         // b's lookup-table entries carry this group's sub-bucket
 };
 
-// Cross-column pair evaluated per row (fallback when a group's 2-D grid does not fit).
+// Cross-column pair evaluated per row (fallback when a group's grid does not fit).
 struct DirectPair {
-    uint32_t la, ha;        // bucket-address interval of the predicate on slot a (la > ha: empty)
+    uint32_t la, ha;        // bucket-index interval of the predicate on slot a (la > ha: empty)
     uint32_t lb, hb;        // ... on slot b
     uint32_t nega, negb;
     uint32_t acc_idx;       // u32 index of its counter in shared memory
@@ -128,7 +149,7 @@ struct ProbeParams {
     uint32_t hll_bytes;                    // nh * 4096: bytes of the packed u8 registers output
     uint32_t smem_bytes;                   // total dynamic shared memory
     unsigned long long *g_acc;             // u64[acc_words], summed over CTAs (and launches)
-    uint8_t *g_hll_part;                   // [part_slot][hll_bytes] per-CTA register partials
+    uint8_t *g_hll_part;                   // [CTA][hll_bytes] per-CTA register partials
     unsigned long long *g_nsamp;
     uint64_t nrows;                        // rows in this launch
     uint64_t row0;                         // global id of the launch's first row
@@ -154,17 +175,20 @@ struct FinJob {
 
 enum FinPairKind : uint32_t { PAIR_SAME = 0, PAIR_GRID = 1, PAIR_DIRECT = 2 };
 
+// A column's bucket-count prefix: P(b) = g_pre[pre + b * stride] = #{kept rows with bucket < b}
+// (own histogram: its exclusive prefix, stride 1; A side of a grid: the grid's summed-area
+// table at the last column, stride nbs + 1).
 struct FinPred {
-    uint32_t pre;           // g_pre index of the column's exclusive prefix (nb + 1 values)
+    uint32_t pre, stride;
     uint32_t lo, hi;        // bucket interval (lo > hi: empty)
     uint32_t neg;
 };
 
 struct FinPair {
     uint32_t kind;
-    uint32_t pre;           // SAME: 1-D prefix; GRID: SAT (row stride nb + 1); DIRECT: g_acc index
+    uint32_t pre, stride;   // SAME: the column's prefix; GRID: SAT (row stride nb + 1); DIRECT: g_acc index
     uint32_t na, nb;        // GRID: grid extent
-    uint32_t li, hi, lj, hj;// SAME: bucket intervals; GRID: i on the A side, j on the B side
+    uint32_t li, hi, lj, hj;// SAME: bucket intervals; GRID: i on the A side (buckets), j on the B side (sub-buckets)
     uint32_t negi, negj;
 };
 

@@ -115,6 +115,11 @@ struct RtShape {
     __device__ static bool is32(const ProbeParams &P, int s) { return !I64 || P.slot[s].dtype == 0; }
     __device__ static bool hll(const ProbeParams &P, int s) { return P.slot[s].has_hll; }
     __device__ static bool clamp(const ProbeParams &P) { return P.clamp; }
+    __device__ static bool packs(const ProbeParams &P, int s) { return P.slot[s].prim_b >= 0; }
+    __device__ static bool ownh(const ProbeParams &P, int s) {
+        return P.slot[s].mode != MODE_NOPRED && P.slot[s].hist_addr != kNone;
+    }
+    __device__ static constexpr bool gpacked(int) { return false; }
     __device__ static constexpr int ga(int) { return 0; }
     __device__ static constexpr int gb(int) { return 0; }
     __device__ static constexpr bool ggrid(int) { return false; }
@@ -178,12 +183,12 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
     return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
 }
 
-// Buckets (counter byte addresses) of slots [S0, S0 + NB) over one row quad.  All
-// level-1 entries are read before any is used; a cell with <= 3 breakpoints resolves
-// branch-free; the rare nested / list / search cases take one branch.
+// Bucket indices (bi) and packed sub-buckets (sb) of slots [S0, S0 + NB) over one row quad.
+// All level-1 entries are read before any is used; a cell with <= 3 breakpoints resolves
+// branch-free; the rare nested / list / search cases take one branch (sub-bucket via map).
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
-                                        uint32_t (&bk)[Sh::NC][4]) {
+                                        uint32_t (&bi)[Sh::NC][4], uint32_t (&sb)[Sh::NC][4]) {
     uint32_t u[NB][4];
     uint4 e[NB][4];
 #pragma unroll
@@ -193,42 +198,48 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            e[i][k] = lut ? g_smem[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint4(0u, 0u, 0u, 0u);
+            e[i][k] = lut ? g_smem[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint4(0u, kNoThr, kNoThr, kNoThr);
         }
     }
     uint32_t spec = 0;
 #pragma unroll
-    for (int i = 0; i < NB; ++i)
+    for (int i = 0; i < NB; ++i) {
+        const int s = S0 + i;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            spec |= e[i][k].x;
-            bk[S0 + i][k] = e[i][k].x + (u[i][k] > e[i][k].y ? 4u : 0u) + (u[i][k] > e[i][k].z ? 4u : 0u) +
-                            (u[i][k] > e[i][k].w ? 4u : 0u);
+            const uint4 &x = e[i][k];
+            spec |= x.x;
+            const uint32_t c1 = u[i][k] > x.y, c2 = u[i][k] > x.z, c3 = u[i][k] > x.w;
+            bi[s][k] = (x.x & kIdxMask) + c1 + c2 + c3;
+            if (Sh::packs(P, s))
+                sb[s][k] = ((x.x >> kSubShift) & kSubMask) + (c1 & (x.x >> kIncShift)) +
+                           (c2 & (x.x >> (kIncShift + 1))) + (c3 & (x.x >> (kIncShift + 2)));
         }
+    }
     if (spec & kSpecial) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i)
+        for (int i = 0; i < NB; ++i) {
+            const int s = S0 + i;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (e[i][k].x & kSpecial) bk[S0 + i][k] = lut_bucket(P.slot[S0 + i].lut_idx, P.slot[S0 + i].s1, u[i][k]);
+            for (int k = 0; k < 4; ++k) {
+                if (e[i][k].x & kSpecial) {
+                    bi[s][k] = lut_bucket(P.slot[s].lut_idx, P.slot[s].s1, u[i][k]);
+                    if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
+                }
+            }
+        }
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
-        if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {
+        if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {      // binary-search fallback column
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                bk[s][k] = P.slot[s].hist_addr + 4 * search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
+            for (int k = 0; k < 4; ++k) {
+                bi[s][k] = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
+                if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
+            }
         }
     }
-}
-
-// Bucket addresses packed 16 bits per column (address / 4 < 2^16) for the generic shape's
-// runtime loop over column pairs.
-template <int NC>
-__device__ __forceinline__ uint32_t pick(const uint64_t (&w)[(NC + 3) / 4][4], uint32_t s, int k) {
-    const uint64_t x = (NC > 4 && (s & 4)) ? w[(NC + 3) / 4 - 1][k] : w[0][k];
-    return (static_cast<uint32_t>(x >> (16 * (s & 3))) & 0xFFFFu) << 2;
 }
 
 __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&ba)[4],
@@ -248,16 +259,24 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupPa
     }
 }
 
-__device__ __forceinline__ void grid_add(const GroupParams &G, const uint32_t (&ba)[4], const uint32_t (&bb)[4],
-                                         uint32_t keep) {
+// grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
+__device__ __forceinline__ void grid_add(const GroupParams &G, bool packed, const uint32_t (&ba)[4],
+                                         const uint32_t (&bb)[4], const uint32_t (&sbb)[4], uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t ia = *at(ba[k] + G.mapA_adj);    // grid row byte offset of a's sub-bucket
-            const uint32_t ib = *at(bb[k] + G.mapB_adj);    // column byte offset of b's sub-bucket
-            atomicAdd(at(ia + ib), 1u);
+            const uint32_t sub = packed ? sbb[k] : *at(G.map_addr + 4 * bb[k]);
+            atomicAdd(at(G.grid_addr + 4 * (ba[k] * G.nbs + sub)), 1u);
         }
     }
+}
+
+template <int NC>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NC][4], uint32_t s, int k) {
+    uint32_t r = x[0][k];
+#pragma unroll
+    for (int c = 1; c < NC; ++c) r = (s == (uint32_t)c) ? x[c][k] : r;
+    return r;
 }
 
 // Everything one row quad contributes.  keep: one bit per row.
@@ -271,16 +290,17 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
     for (int s = 0; s < NC; ++s)
         if (Sh::active(P, s)) decode<Sh>(P, s, r[s], v[s]);
-    uint32_t bk[NC][4];
-    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bk);
-    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bk);
-    // per-column bucket histograms
+    uint32_t bi[NC][4], sb[NC][4];
+    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bi, sb);
+    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bi, sb);
+    // own bucket histograms (columns that are no grid's full-resolution side)
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
-        if (!Sh::active(P, s) || Sh::mode(P, s) == MODE_NOPRED || (dbg & 2)) continue;
+        if (!Sh::active(P, s) || !Sh::ownh(P, s) || (dbg & 2)) continue;
+        const uint32_t h = P.slot[s].hist_addr;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(bk[s][k]), 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * bi[s][k]), 1u);
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
@@ -320,29 +340,20 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
         for (int g = 0; g < Sh::NG; ++g) {
             const GroupParams &G = P.grp[g];
-            if (Sh::ggrid(g)) grid_add(G, bk[Sh::ga(g)], bk[Sh::gb(g)], keep);
-            if (Sh::gdirect(g)) direct_pairs(P, G, bk[Sh::ga(g)], bk[Sh::gb(g)], keep);
+            if (Sh::ggrid(g)) grid_add(G, Sh::gpacked(g), bi[Sh::ga(g)], bi[Sh::gb(g)], sb[Sh::gb(g)], keep);
+            if (Sh::gdirect(g)) direct_pairs(P, G, bi[Sh::ga(g)], bi[Sh::gb(g)], keep);
         }
     } else {
-        uint64_t ids[(NC + 3) / 4][4];
-#pragma unroll
-        for (int h = 0; h < (NC + 3) / 4; ++h)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint64_t x = 0;
-#pragma unroll
-                for (int q = 0; q < 4 && 4 * h + q < NC; ++q) x |= static_cast<uint64_t>(bk[4 * h + q][k] >> 2) << (16 * q);
-                ids[h][k] = x;
-            }
         for (uint32_t g = 0; g < P.ngroups; ++g) {
             const GroupParams &G = P.grp[g];
-            uint32_t ba[4], bb[4];
+            uint32_t ba[4], bb[4], sbb[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                ba[k] = pick<NC>(ids, G.a, k);
-                bb[k] = pick<NC>(ids, G.b, k);
+                ba[k] = pick<NC>(bi, G.a, k);
+                bb[k] = pick<NC>(bi, G.b, k);
+                sbb[k] = G.packed ? pick<NC>(sb, G.b, k) : 0u;
             }
-            if (G.has_grid) grid_add(G, ba, bb, keep);
+            if (G.has_grid) grid_add(G, G.packed, ba, bb, sbb, keep);
             if (G.dend > G.dbeg) direct_pairs(P, G, ba, bb, keep);
         }
     }
