@@ -221,7 +221,8 @@ struct SlotPlan {
     bool clamp = false;
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
-    std::vector<uint4> l1, l2;         // entries with slot-relative indices (fixed up later)
+    std::vector<uint32_t> l1;          // level-1 cells (boundary cells: slot-relative record index)
+    std::vector<uint4> l2;             // records and nested blocks (slot-relative indices)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
     // roles in the pair grids
     int hist_grp = -1;                 // group whose grid row sums give this column's histogram
@@ -239,10 +240,10 @@ uint32_t ceil_log2(uint64_t x) {
 }
 
 // Build the lookup table of a slot for level-1 shift s1 over offsets u in [0, span]
-// (entry formats: gace_plan.h).  Entries hold RELATIVE sub-table / list indices here;
-// make_plan adds the slot's shared-memory offsets.  A cell with <= 3 breakpoints is a
-// direct entry (with the packed sub-bucket of the column's primary B role, if any), up to
-// 8 a list, a denser cell points to a block of uniform sub-cells built recursively.
+// (formats: gace_plan.h).  Indices are RELATIVE here; make_plan adds the slot's
+// shared-memory offsets.  A cell without breakpoints is a plain u32 (bucket + packed
+// sub-bucket of the column's primary B role); a boundary cell points to a record: direct
+// (<= 3 breakpoints), list (<= 8) or a block of uniform sub-cells built recursively.
 bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     std::vector<uint64_t> toff;
     toff.reserve(S.T.size());
@@ -296,12 +297,19 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     const uint64_t csize = 1ull << s1;
     for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
-        S.l1.push_back(node(lo, hi, s1));
+        const uint32_t b0 = le(lo);
+        if (le(hi) == b0) {                                        // plain cell
+            S.l1.push_back(b0 | (sub_of(b0) << kSubShift));
+        } else {                                                   // boundary cell -> record
+            const uint4 e = node(lo, hi, s1);
+            S.l1.push_back(kSpecial | (uint32_t)S.l2.size());
+            S.l2.push_back(e);
+        }
     }
     return ok;
 }
 
-size_t lut_bytes(const SlotPlan &S) { return 16 * (S.l1.size() + S.l2.size()) + 4 * S.lst.size() + 32; }
+size_t lut_bytes(const SlotPlan &S) { return 4 * S.l1.size() + 16 * S.l2.size() + 4 * S.lst.size() + 48; }
 
 struct Group {
     int a = -1, b = -1;                // oriented: a = full-resolution side, b = sub-bucket side
@@ -499,7 +507,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
         uint64_t target = 64;
-        while (target < 4096 && target < 16ull * S.T.size()) target <<= 1;
+        while (target < 8192 && target < 32ull * S.T.size()) target <<= 1;
         const uint64_t span = span_of(S);
         uint32_t sh = 0;
         while (sh < 31 && (span >> sh) + 1 > target) ++sh;
@@ -521,7 +529,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         SlotPlan &S = pl.slots[worst];
         // a coarser level 1 roughly halves it; when nested blocks / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
-        if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 16 * S.l1.size()) {
+        if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 4 * S.l1.size()) {
             to_search(S);
             continue;
         }
@@ -533,10 +541,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
         w = (w + 3) & ~3u;
-        S.lut_idx = w / 4;
-        w += 4 * (uint32_t)S.l1.size();
         S.l2_idx = w / 4;
         w += 4 * (uint32_t)S.l2.size();
+        S.lut_idx = w;
+        w += (uint32_t)S.l1.size();
         S.lst_idx = w;
         w += (uint32_t)S.lst.size();
     }
@@ -579,7 +587,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     pl.image.assign((size_t)image_words * 4, 0);
     uint4 *img4 = reinterpret_cast<uint4 *>(pl.image.data());
     uint32_t *img32 = reinterpret_cast<uint32_t *>(pl.image.data());
-    auto fix = [&](uint4 e, const SlotPlan &S) {   // relative sub-table / list indices -> absolute
+    auto fix = [&](uint4 e, const SlotPlan &S) {   // relative record / list indices -> absolute
         if (!(e.x & kSpecial)) return e;
         if (e.x & kList) e.y += S.lst_idx;
         else e.y += S.l2_idx;
@@ -587,7 +595,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     };
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        for (size_t k = 0; k < S.l1.size(); ++k) img4[S.lut_idx + k] = fix(S.l1[k], S);
+        for (size_t k = 0; k < S.l1.size(); ++k)
+            img32[S.lut_idx + k] = (S.l1[k] & kSpecial) ? kSpecial | (S.l2_idx + (S.l1[k] & kRecMask)) : S.l1[k];
         for (size_t k = 0; k < S.l2.size(); ++k) img4[S.l2_idx + k] = fix(S.l2[k], S);
         for (size_t k = 0; k < S.lst.size(); ++k) img32[S.lst_idx + k] = S.lst[k];
     }
@@ -703,7 +712,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.prim_b = (int8_t)S.prim_b;
         Q.base = S.base;
         Q.s1 = S.s1;
-        Q.lut_idx = S.lut_idx;
+        Q.lut_w = S.lut_idx;
         if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
         else { Q.clamp_lo = INT64_MIN; Q.clamp_hi = INT64_MAX; }
         if (S.has_preds && S.mode == MODE_LUT && S.clamp) {
@@ -1365,11 +1374,11 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
-            b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)x - (uint32_t)Q.base);
+            b = lut_lookup(M, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base);
         } else {
             int64_t x = values[k];
             if (pl.clamp) x = std::min(std::max(x, Q.clamp_lo), Q.clamp_hi);
-            b = lut_lookup(M, Q.lut_idx, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
+            b = lut_lookup(M, Q.lut_w, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
         }
         if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
         if (b >= S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
@@ -1382,7 +1391,7 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
                                      pl.clamp ? (int32_t)Q.clamp_hi : INT32_MAX) - (uint32_t)Q.base
                 : (uint32_t)((uint64_t)std::min(std::max(values[k], pl.clamp ? Q.clamp_lo : INT64_MIN),
                                                 pl.clamp ? Q.clamp_hi : INT64_MAX) - (uint64_t)Q.base);
-            const uint32_t sub = entry_sub(lut_entry(M, Q.lut_idx, Q.s1, u), u);
+            const uint32_t sub = entry_sub(lut_entry(M, Q.lut_w, Q.s1, u), u);
             const uint32_t want = reinterpret_cast<const uint32_t *>(pl.image.data())[G.map_w + b];
             if (sub != kNone && sub != want) return fail(GACE_EUNSUPPORTED, "internal: packed sub-bucket differs from the map");
         }

@@ -44,6 +44,7 @@ constexpr uint32_t kSubShift = 14;          // packed sub-bucket field: bits 14.
 constexpr uint32_t kSubMask = 0x7Fu;
 constexpr uint32_t kSubMax = 127;           // sub-buckets per group side that can be packed
 constexpr uint32_t kIncShift = 21;          // sub-bucket increment flags of the 3 thresholds
+constexpr uint32_t kRecMask = 0x3FFFFFFFu;  // level-1 boundary cell: record index
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 #if defined(__CUDACC__)
@@ -52,24 +53,31 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 #define GACE_HD inline
 #endif
 
-// LUT entry (16 bytes), over the offset u = v - base of one column:
-//   direct : x = first bucket index (bits 0..13) | packed sub-bucket of that bucket
-//            (bits 14..20) | flags (bits 21..23): threshold i also cuts the sub-buckets;
-//            y <= z <= w = up to three thresholds (unused: ~0).
-//            bucket = x.idx + #{t in (y, z, w) : u > t};  sub = x.sub + #{flagged t : u > t}
-//   nested : x = kSpecial | sc << 24, y = uint4 index of a block of sub-cells of size
-//            2^sc; sub-entry = T[y + ((u mod cell size) >> sc)] (any of the three kinds)
-//   list   : x = kSpecial | kList | n << 24 | first bucket index, y = u32 index of n sorted
-//            breakpoint offsets t; bucket = first + #{t : u >= t} (sub-bucket via the map)
+// Lookup table over the offset u = v - base of one column.  Level 1 is one u32 per cell
+// of 2^s1 offsets:
+//   plain    : bit 31 clear; bucket index (bits 0..13) | packed sub-bucket (bits 14..20) of
+//              the whole cell (no breakpoint inside it) -- the common case: one LDS.32
+//   boundary : kSpecial | uint4 index of the cell's 16-byte record:
+//     direct : x = first bucket index (bits 0..13) | packed sub-bucket of that bucket
+//              (bits 14..20) | flags (bits 21..23): threshold i also cuts the sub-buckets;
+//              y <= z <= w = up to three thresholds (unused: ~0).
+//              bucket = x.idx + #{t in (y, z, w) : u > t};  sub = x.sub + #{flagged t : u > t}
+//     nested : x = kSpecial | sc << 24, y = uint4 index of a block of sub-records of size
+//              2^sc; sub-record = R[y + ((u mod cell size) >> sc)] (any of the three kinds)
+//     list   : x = kSpecial | kList | n << 24 | first bucket index, y = u32 index of n sorted
+//              breakpoint offsets t; bucket = first + #{t : u >= t} (sub-bucket via the map)
 //
-// Final (direct or list) entry for offset u, walking nested blocks.  `M` reads the table
-// image: M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy in
+// Final (direct or list) record for offset u, walking nested blocks (a plain cell is
+// returned as a direct record without thresholds).  `M` reads the table image:
+// M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy in
 // gace_debug_buckets).
 template <class Mem>
-GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
+GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t u) {
+    const uint32_t c = M.u32(lut_w + (u >> s1));
+    if (!(c & kSpecial)) return make_uint4(c, kNoThr, kNoThr, kNoThr);
     uint32_t s = s1;
-    uint4 e = M.u4(lut_idx + (u >> s));
-    while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-cells (nested)
+    uint4 e = M.u4(c & kRecMask);
+    while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-records (nested)
         const uint32_t sc = (e.x >> 24) & 63u;
         e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
         s = sc;
@@ -79,8 +87,8 @@ GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u)
 
 // Bucket index of offset u (full walk).
 template <class Mem>
-GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_idx, uint32_t s1, uint32_t u) {
-    const uint4 e = lut_entry(M, lut_idx, s1, u);
+GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t u) {
+    const uint4 e = lut_entry(M, lut_w, s1, u);
     uint32_t b = e.x & kIdxMask;
     if (e.x & kList) {
         const uint32_t n = (e.x >> 24) & 63u;
@@ -107,7 +115,7 @@ struct SlotParams {
     int64_t clamp_hi;
     uint32_t nbp;           // MODE_SEARCH: number of breakpoints
     uint32_t s1;            // level-1 cell = u >> s1
-    uint32_t lut_idx;       // level-1 table: uint4 index into shared memory
+    uint32_t lut_w;         // level-1 table: u32 index into shared memory
     uint32_t hist_addr;     // byte address of bucket 0 of this column's own histogram, or kNone
     uint32_t hll_idx;       // u32 index of this column's u32[4096] HLL registers, or kNone
     uint8_t dtype;          // 0 = int32, 1 = int64

@@ -91,8 +91,8 @@ struct SmemTables {
 };
 
 // Full walk through nested cells and lists (out of line: rare special entries only).
-__device__ __noinline__ uint32_t lut_bucket(uint32_t lut_idx, uint32_t s1, uint32_t u) {
-    return lut_lookup(SmemTables{}, lut_idx, s1, u);
+__device__ __noinline__ uint32_t lut_bucket(uint32_t lut_w, uint32_t s1, uint32_t u) {
+    return lut_lookup(SmemTables{}, lut_w, s1, u);
 }
 
 __device__ __forceinline__ bool keep_row(const ProbeParams &P, uint64_t g) {
@@ -184,13 +184,14 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
 }
 
 // Bucket indices (bi) and packed sub-buckets (sb) of slots [S0, S0 + NB) over one row quad.
-// All level-1 entries are read before any is used; a cell with <= 3 breakpoints resolves
-// branch-free; the rare nested / list / search cases take one branch (sub-bucket via map).
+// Common case: one LDS.32 per key (a plain level-1 cell carries both).  Keys in boundary
+// cells (a few percent) read their 16-byte record behind one branch per quad; nested /
+// list / search cases go through the out-of-line full walk and the sub-bucket map.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
                                         uint32_t (&bi)[Sh::NC][4], uint32_t (&sb)[Sh::NC][4]) {
-    uint32_t u[NB][4];
-    uint4 e[NB][4];
+    const uint32_t *sm = smem32();
+    uint32_t u[NB][4], e[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
@@ -198,7 +199,7 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            e[i][k] = lut ? g_smem[P.slot[s].lut_idx + (u[i][k] >> P.slot[s].s1)] : make_uint4(0u, kNoThr, kNoThr, kNoThr);
+            e[i][k] = lut ? sm[P.slot[s].lut_w + (u[i][k] >> P.slot[s].s1)] : 0u;
         }
     }
     uint32_t spec = 0;
@@ -207,13 +208,9 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
         const int s = S0 + i;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint4 &x = e[i][k];
-            spec |= x.x;
-            const uint32_t c1 = u[i][k] > x.y, c2 = u[i][k] > x.z, c3 = u[i][k] > x.w;
-            bi[s][k] = (x.x & kIdxMask) + c1 + c2 + c3;
-            if (Sh::packs(P, s))
-                sb[s][k] = ((x.x >> kSubShift) & kSubMask) + (c1 & (x.x >> kIncShift)) +
-                           (c2 & (x.x >> (kIncShift + 1))) + (c3 & (x.x >> (kIncShift + 2)));
+            spec |= e[i][k];
+            bi[s][k] = e[i][k] & kIdxMask;
+            if (Sh::packs(P, s)) sb[s][k] = (e[i][k] >> kSubShift) & kSubMask;
         }
     }
     if (spec & kSpecial) {
@@ -222,9 +219,18 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
             const int s = S0 + i;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (e[i][k].x & kSpecial) {
-                    bi[s][k] = lut_bucket(P.slot[s].lut_idx, P.slot[s].s1, u[i][k]);
-                    if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
+                if (e[i][k] & kSpecial) {
+                    const uint4 r = g_smem[e[i][k] & kRecMask];
+                    if (!(r.x & kSpecial)) {                      // direct record: <= 3 thresholds
+                        const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
+                        bi[s][k] = (r.x & kIdxMask) + c1 + c2 + c3;
+                        if (Sh::packs(P, s))
+                            sb[s][k] = ((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) +
+                                       (c2 & (r.x >> (kIncShift + 1))) + (c3 & (r.x >> (kIncShift + 2)));
+                    } else {                                      // nested block or list
+                        bi[s][k] = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u[i][k]);
+                        if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
+                    }
                 }
             }
         }

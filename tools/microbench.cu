@@ -1,5 +1,5 @@
-// Shared-memory update throughput on this GPU (design input for the probe's counters).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench.cu && /tmp/mb
+// Shared-memory access throughput on this GPU (design input for the probe's tables/counters).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/microbench tools/microbench.cu && build/microbench
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -8,44 +8,47 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
     x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
 }
 
-// mode 0: atomicAdd random bucket of NB; 1: atomicAdd same address; 2: atomicAdd lane-distinct banks;
-// 3: private byte counters (LDS.U8/STS.U8, thread-private region); 4: LDS random (read only);
-// 5: atomicAdd random bucket, per-warp private copy of the histogram
+// Each thread performs `iters` accesses at pseudo-random word indices in [0, nwords).
+// MODE 0: atomicAdd(+1)          (compiles to ATOMS.POPC.INC)
+// MODE 1: atomicAdd(+v), v reg   (ATOMS.ADD)
+// MODE 2: LDS.32   3: LDS.64   4: LDS.128 (entry index random, 16-B aligned)
+// MODE 5: atomicMax(+v)          6: LDS.32 all lanes of a warp same address (broadcast)
 template <int MODE>
-__global__ void k_smem(int iters, int nb, uint32_t smem_words, uint32_t *out) {
+__global__ void k_smem(int iters, uint32_t nwords, uint32_t smem_words, uint32_t *out) {
     extern __shared__ uint32_t sm[];
     const int tid = threadIdx.x;
-    for (uint32_t i = tid; i < smem_words; i += blockDim.x) sm[i] = 0;
+    for (uint32_t i = tid; i < smem_words; i += blockDim.x) sm[i] = i;
     __syncthreads();
     uint32_t x = hash32(blockIdx.x * 4096 + tid);
     uint32_t acc = 0;
-    uint8_t *sm8 = reinterpret_cast<uint8_t *>(sm);
     for (int it = 0; it < iters; ++it) {
         x = x * 1664525u + 1013904223u;
-        const uint32_t b = (x >> 8) % nb;
+        const uint32_t b = (x >> 8) % nwords;
         if (MODE == 0) atomicAdd(sm + b, 1u);
-        if (MODE == 1) atomicAdd(sm + 7, 1u);
-        if (MODE == 2) atomicAdd(sm + (tid & 31) + 32 * (it & 7), 1u);
-        if (MODE == 3) { uint8_t *p = sm8 + b * blockDim.x + tid; *p = *p + 1; }
-        if (MODE == 4) acc += sm[b];
-        if (MODE == 5) atomicAdd(sm + (tid >> 5) * nb + b, 1u);
+        if (MODE == 1) atomicAdd(sm + b, (x & 1) + 1);
+        if (MODE == 2) acc += sm[b];
+        if (MODE == 3) { const uint2 v = reinterpret_cast<const uint2 *>(sm)[b >> 1]; acc += v.x ^ v.y; }
+        if (MODE == 4) { const uint4 v = reinterpret_cast<const uint4 *>(sm)[b >> 2]; acc += v.x ^ v.y ^ v.z ^ v.w; }
+        if (MODE == 5) atomicMax(sm + b, x);
+        if (MODE == 6) acc += sm[__shfl_sync(0xffffffffu, b, 0)];
     }
     if (acc == 0x12345678) out[0] = acc;
 }
 
 template <int MODE>
-float run(int nb, int threads, int iters, size_t smem) {
-    cudaFuncSetAttribute(k_smem<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+float run(uint32_t nwords, int threads, int iters) {
+    const size_t smem = 200 * 1024;
+    cudaFuncSetAttribute(k_smem<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t *out;
     cudaMalloc(&out, 16);
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    k_smem<MODE><<<sms, threads, smem>>>(iters, nb, (uint32_t)(smem / 4), out);
+    k_smem<MODE><<<sms, threads, smem>>>(iters, nwords, (uint32_t)(smem / 4), out);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    k_smem<MODE><<<sms, threads, smem>>>(iters, nb, (uint32_t)(smem / 4), out);
+    k_smem<MODE><<<sms, threads, smem>>>(iters, nwords, (uint32_t)(smem / 4), out);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -53,20 +56,18 @@ float run(int nb, int threads, int iters, size_t smem) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("err %s\n", cudaGetErrorString(e));
     cudaFree(out);
-    // lane-ops per SM per ns
-    return (float)threads * iters / (ms * 1e6f);
+    // SM-cycles per warp-instruction at 1.965 GHz
+    const double warp_instr_per_sm = (double)threads / 32 * iters;
+    return (float)(ms * 1e-3 * 1.965e9 / warp_instr_per_sm);
 }
 
 int main() {
     const int it = 4096;
-    printf("lane-updates per SM per ns (x1.965 GHz -> per cycle: divide by 1.965)\n");
-    for (int nb : {129, 1025}) {
-        printf("nb=%d atomic random        : %.2f\n", nb, run<0>(nb, 1024, it, 64 * 1024));
-        printf("nb=%d atomic per-warp hist : %.2f\n", nb, run<5>(nb, 1024, it, 32 * nb * 4 > 200 * 1024 ? 200 * 1024 : 32 * nb * 4 + 64));
-        printf("nb=%d private u8 (128 thr) : %.2f\n", nb, run<3>(nb, 128, it, nb * 128 + 64));
-        printf("nb=%d lds random           : %.2f\n", nb, run<4>(nb, 1024, it, 64 * 1024));
+    printf("SM cycles per warp-wide access (random word in a table of N words), 512 threads/SM\n");
+    for (uint32_t n : {129u, 4257u, 16384u}) {
+        printf("N=%5u  ATOMS.POPC.INC %.2f  ATOMS.ADD %.2f  ATOMS.MAX %.2f  LDS.32 %.2f  LDS.64 %.2f  LDS.128 %.2f  bcast %.2f\n", n,
+               run<0>(n, 512, it), run<1>(n, 512, it), run<5>(n, 512, it), run<2>(n, 512, it), run<3>(n, 512, it),
+               run<4>(n, 512, it), run<6>(n, 512, it));
     }
-    printf("atomic same address     : %.2f\n", run<1>(129, 1024, it / 4, 64 * 1024));
-    printf("atomic distinct banks   : %.2f\n", run<2>(129, 1024, it, 64 * 1024));
     return 0;
 }
