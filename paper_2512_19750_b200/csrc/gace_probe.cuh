@@ -60,6 +60,21 @@ __device__ __forceinline__ uint32_t *at(uint32_t a) {
     return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(g_smem) + a);
 }
 
+// Predicated shared-memory ops as single instructions (a C++ `if` around them becomes a
+// branch with reconvergence barriers on every key).
+__device__ __forceinline__ uint32_t saddr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void red_max_if(bool pred, const uint32_t *addr, uint32_t v) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.max.u32 [%1], %2;\n}"
+                 :: "r"((uint32_t)pred), "r"(saddr(addr)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void lds128_if(bool pred, const uint4 *addr, uint4 &r) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n @q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n}"
+                 : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+                 : "r"((uint32_t)pred), "r"(saddr(addr)));
+}
+
 // Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
 __device__ __noinline__ uint32_t hll_min(uint32_t hll_idx) {
     const uint4 *R = reinterpret_cast<const uint4 *>(smem32() + hll_idx);
@@ -183,13 +198,13 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
     return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
 }
 
-// Bucket indices (bi) and packed sub-buckets (sb) of slots [S0, S0 + NB) over one row quad.
-// Common case: one LDS.32 per key (a plain level-1 cell carries both).  Keys in boundary
-// cells (a few percent) read their 16-byte record behind one branch per quad; nested /
-// list / search cases go through the out-of-line full walk and the sub-bucket map.
+// Bucket index | sub-bucket << 16 (bs) of slots [S0, S0 + NB) over one row quad.  One
+// LDS.32 per key; keys in boundary cells (a few percent) additionally load their 16-byte
+// record with a predicated LDS.128 and resolve branch-free (<= 3 thresholds); nested /
+// list records and binary-search columns go through the out-of-line full walk.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
-                                        uint32_t (&bi)[Sh::NC][4], uint32_t (&sb)[Sh::NC][4]) {
+                                        uint32_t (&bs)[Sh::NC][4]) {
     const uint32_t *sm = smem32();
     uint32_t u[NB][4], e[NB][4];
 #pragma unroll
@@ -202,35 +217,32 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
             e[i][k] = lut ? sm[P.slot[s].lut_w + (u[i][k] >> P.slot[s].s1)] : 0u;
         }
     }
-    uint32_t spec = 0;
+    uint32_t deep = 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            spec |= e[i][k];
-            bi[s][k] = e[i][k] & kIdxMask;
-            if (Sh::packs(P, s)) sb[s][k] = (e[i][k] >> kSubShift) & kSubMask;
+            uint4 r = make_uint4(e[i][k], kNoThr, kNoThr, kNoThr);   // a plain cell as a direct record
+            lds128_if(e[i][k] & kSpecial, g_smem + (e[i][k] & kRecMask), r);
+            deep |= r.x;                                             // nested / list record?
+            const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
+            uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
+            if (Sh::packs(P, s))
+                b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) + (c2 & (r.x >> (kIncShift + 1))) +
+                      (c3 & (r.x >> (kIncShift + 2)))) << 16;
+            bs[s][k] = b;
         }
     }
-    if (spec & kSpecial) {
+    if (deep & kSpecial) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const int s = S0 + i;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (e[i][k] & kSpecial) {
-                    const uint4 r = g_smem[e[i][k] & kRecMask];
-                    if (!(r.x & kSpecial)) {                      // direct record: <= 3 thresholds
-                        const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
-                        bi[s][k] = (r.x & kIdxMask) + c1 + c2 + c3;
-                        if (Sh::packs(P, s))
-                            sb[s][k] = ((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) +
-                                       (c2 & (r.x >> (kIncShift + 1))) + (c3 & (r.x >> (kIncShift + 2)));
-                    } else {                                      // nested block or list
-                        bi[s][k] = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u[i][k]);
-                        if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
-                    }
+                if ((e[i][k] & kSpecial) && (g_smem[e[i][k] & kRecMask].x & kSpecial)) {
+                    const uint32_t b = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u[i][k]);
+                    bs[s][k] = b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
                 }
             }
         }
@@ -241,22 +253,23 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
         if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {      // binary-search fallback column
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                bi[s][k] = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
-                if (Sh::packs(P, s)) sb[s][k] = *at(P.grp[P.slot[s].prim_b].map_addr + 4 * bi[s][k]);
+                const uint32_t b = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
+                bs[s][k] = b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
             }
         }
     }
 }
 
-__device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&ba)[4],
-                                             const uint32_t (&bb)[4], uint32_t keep) {
+__device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&bsa)[4],
+                                             const uint32_t (&bsb)[4], uint32_t keep) {
     for (uint32_t d = G.dbeg; d < G.dend; ++d) {
         const DirectPair D = P.direct[d];
         uint32_t c = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t ina = ((ba[k] >= D.la) & (ba[k] <= D.ha)) ^ D.nega;
-            const uint32_t inb = ((bb[k] >= D.lb) & (bb[k] <= D.hb)) ^ D.negb;
+            const uint32_t ba = bsa[k] & 0xFFFFu, bb = bsb[k] & 0xFFFFu;
+            const uint32_t ina = ((ba >= D.la) & (ba <= D.ha)) ^ D.nega;
+            const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
             c += ((keep >> k) & 1u) & ina & inb;
         }
         // per-thread add: this may run in a diverged warp (sampled quads), where a
@@ -266,13 +279,13 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupPa
 }
 
 // grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
-__device__ __forceinline__ void grid_add(const GroupParams &G, bool packed, const uint32_t (&ba)[4],
-                                         const uint32_t (&bb)[4], const uint32_t (&sbb)[4], uint32_t keep) {
+__device__ __forceinline__ void grid_add(const GroupParams &G, bool packed, const uint32_t (&bsa)[4],
+                                         const uint32_t (&bsb)[4], uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t sub = packed ? sbb[k] : *at(G.map_addr + 4 * bb[k]);
-            atomicAdd(at(G.grid_addr + 4 * (ba[k] * G.nbs + sub)), 1u);
+            const uint32_t sub = packed ? bsb[k] >> 16 : *at(G.map_addr + 4 * (bsb[k] & 0xFFFFu));
+            atomicAdd(at(G.grid_addr + 4 * ((bsa[k] & 0xFFFFu) * G.nbs + sub)), 1u);
         }
     }
 }
@@ -296,9 +309,9 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
     for (int s = 0; s < NC; ++s)
         if (Sh::active(P, s)) decode<Sh>(P, s, r[s], v[s]);
-    uint32_t bi[NC][4], sb[NC][4];
-    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bi, sb);
-    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bi, sb);
+    uint32_t bs[NC][4];
+    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bs);
+    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bs);
     // own bucket histograms (columns that are no grid's full-resolution side)
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
@@ -306,7 +319,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
         const uint32_t h = P.slot[s].hist_addr;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * bi[s][k]), 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & 0xFFFFu)), 1u);
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
@@ -327,7 +340,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
                 const uint32_t w32 = h * (1u << kHllP) + (1u << (kHllP - 1));
                 const uint32_t idx = __umulhi(h, 1u << kHllP);       // h >> (32 - p)
-                if (((keep >> k) & 1u) && w32 <= lim && !(dbg & 1)) atomicMax(R + idx, __clz(w32) + 1);
+                red_max_if(((keep >> k) & 1u) && w32 <= lim && !(dbg & 1), R + idx, __clz(w32) + 1);
             }
         } else {
             const uint64_t lim = ~0ull >> lim_l[s];
@@ -336,7 +349,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
                 const uint64_t w64 = (h << kHllP) | (1ull << (kHllP - 1));
                 const uint32_t idx = static_cast<uint32_t>(h >> (64 - kHllP));
-                if (((keep >> k) & 1u) && w64 <= lim && !(dbg & 1)) atomicMax(R + idx, __clzll(w64) + 1);
+                red_max_if(((keep >> k) & 1u) && w64 <= lim && !(dbg & 1), R + idx, __clzll(w64) + 1);
             }
         }
     }
@@ -346,20 +359,19 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
         for (int g = 0; g < Sh::NG; ++g) {
             const GroupParams &G = P.grp[g];
-            if (Sh::ggrid(g)) grid_add(G, Sh::gpacked(g), bi[Sh::ga(g)], bi[Sh::gb(g)], sb[Sh::gb(g)], keep);
-            if (Sh::gdirect(g)) direct_pairs(P, G, bi[Sh::ga(g)], bi[Sh::gb(g)], keep);
+            if (Sh::ggrid(g)) grid_add(G, Sh::gpacked(g), bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
+            if (Sh::gdirect(g)) direct_pairs(P, G, bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
         }
     } else {
         for (uint32_t g = 0; g < P.ngroups; ++g) {
             const GroupParams &G = P.grp[g];
-            uint32_t ba[4], bb[4], sbb[4];
+            uint32_t ba[4], bb[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                ba[k] = pick<NC>(bi, G.a, k);
-                bb[k] = pick<NC>(bi, G.b, k);
-                sbb[k] = G.packed ? pick<NC>(sb, G.b, k) : 0u;
+                ba[k] = pick<NC>(bs, G.a, k);
+                bb[k] = pick<NC>(bs, G.b, k);
             }
-            if (G.has_grid) grid_add(G, G.packed, ba, bb, sbb, keep);
+            if (G.has_grid) grid_add(G, G.packed, ba, bb, keep);
             if (G.dend > G.dbeg) direct_pairs(P, G, ba, bb, keep);
         }
     }
