@@ -423,7 +423,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                 }
             }
             G.na = pl.slots[G.a].nb;
-            G.nbs = (uint32_t)G.TB.size() + 1;
+            // row stride = sub-bucket count rounded up to odd: rows then start in different
+            // shared-memory banks, so a warp whose rows share one sub-bucket (a sorted B
+            // column) does not serialise on a single bank (the extra column stays zero)
+            G.nbs = ((uint32_t)G.TB.size() + 1) | 1u;
             has_hist[G.a] = 1;
             if (G.nbs <= kSubMax) has_prim[G.b] = 1;
         }
