@@ -744,6 +744,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         R.map_addr = G.direct ? kNone : 4 * G.map_w;
     }
     P.ngroups = (uint32_t)pl.groups.size();
+    P.clamp = pl.clamp ? 1u : 0u;      // (the specialised kernel bakes this in: set it here)
     P.ndirect = (uint32_t)pl.direct.size();
     P.image_u4 = image_words / 4;
     P.acc_idx = pl.acc_idx;
@@ -1068,7 +1069,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
     if (const char *ab = getenv("GACE_ABLATE")) P.dbg = (uint32_t)strtoul(ab, nullptr, 0);   // design experiments only
     const bool sample = sample_rate < 1.0;
-    P.clamp = pl.clamp ? 1u : 0u;
     bool i64 = false;
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;

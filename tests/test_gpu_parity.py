@@ -295,3 +295,11 @@ def test_specialised_kernel_edge_shapes(G, oracle, force_jit):
     test_int64_wide_domain_search_mode(G, oracle)
     for n in (1, 5, 33, 4097):
         test_ragged_sizes(G, oracle, n)
+
+
+@pytest.mark.parametrize("name,rate", [("C1", 1.0), ("C5", 1.0), ("C5", 0.3), ("C5_i64", 1.0)])
+def test_specialised_kernel_host_tables(G, oracle, force_jit, name, rate):
+    """Host tables (clamped lookup tables, chunked launches) through the specialised kernel."""
+    w = synth.get(name, 70_001)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, 3, w.hll_cols, host=True)
