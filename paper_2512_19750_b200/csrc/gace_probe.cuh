@@ -198,10 +198,26 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
     return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
 }
 
+// Bucket | sub-bucket << 16 of a key in a boundary cell: its 16-byte record (<= 3
+// thresholds), or the full walk for nested / list records (sub-bucket via the map).
+template <class Sh>
+__device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s, uint32_t e, uint32_t u) {
+    const uint4 r = g_smem[e & kRecMask];
+    if (!(r.x & kSpecial)) {
+        const uint32_t c1 = u > r.y, c2 = u > r.z, c3 = u > r.w;
+        uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
+        if (Sh::packs(P, s))
+            b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) + (c2 & (r.x >> (kIncShift + 1))) +
+                  (c3 & (r.x >> (kIncShift + 2)))) << 16;
+        return b;
+    }
+    const uint32_t b = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u);
+    return b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
+}
+
 // Bucket index | sub-bucket << 16 (bs) of slots [S0, S0 + NB) over one row quad.  One
-// LDS.32 per key; keys in boundary cells (a few percent) additionally load their 16-byte
-// record with a predicated LDS.128 and resolve branch-free (<= 3 thresholds); nested /
-// list records and binary-search columns go through the out-of-line full walk.
+// LDS.32 per key and two ALU ops in a plain cell; keys in boundary cells (a few percent)
+// branch to their record; binary-search columns go through the out-of-line search.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
                                         uint32_t (&bs)[Sh::NC][4]) {
@@ -217,34 +233,14 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
             e[i][k] = lut ? sm[P.slot[s].lut_w + (u[i][k] >> P.slot[s].s1)] : 0u;
         }
     }
-    uint32_t deep = 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uint4 r = make_uint4(e[i][k], kNoThr, kNoThr, kNoThr);   // a plain cell as a direct record
-            lds128_if(e[i][k] & kSpecial, g_smem + (e[i][k] & kRecMask), r);
-            deep |= r.x;                                             // nested / list record?
-            const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
-            uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
-            if (Sh::packs(P, s))
-                b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) + (c2 & (r.x >> (kIncShift + 1))) +
-                      (c3 & (r.x >> (kIncShift + 2)))) << 16;
-            bs[s][k] = b;
-        }
-    }
-    if (deep & kSpecial) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int s = S0 + i;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if ((e[i][k] & kSpecial) && (g_smem[e[i][k] & kRecMask].x & kSpecial)) {
-                    const uint32_t b = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u[i][k]);
-                    bs[s][k] = b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
-                }
-            }
+            // plain cell: bucket | sub-bucket << 16 straight from the level-1 word
+            bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
+            if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k], u[i][k]);
         }
     }
 #pragma unroll
