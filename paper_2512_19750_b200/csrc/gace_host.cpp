@@ -147,6 +147,7 @@ struct gace_table {
     std::vector<const void *> cols;
     std::vector<int> dtypes;
     std::vector<int64_t> dlo, dhi;     // value domain per column (measured for device tables)
+    std::vector<uint8_t> clustered;    // >= half of the aligned row quads hold one key (device tables)
     bool has_dist = false;
     gace_dist dist{};
     void *comm = nullptr;
@@ -833,24 +834,29 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
         t->dlo[c] = dtypes[c] == GACE_I32 ? INT32_MIN : INT64_MIN;
         t->dhi[c] = dtypes[c] == GACE_I32 ? INT32_MAX : INT64_MAX;
     }
+    t->clustered.assign(ncols, 0);
     if (!host && nrows) {
         DevBuf mm;
-        if (mm.ensure(16 * ncols) != cudaSuccess) return bail(fail(GACE_ENOMEM, "minmax scratch"));
-        std::vector<long long> init(2 * ncols);
-        for (uint32_t c = 0; c < ncols; ++c) { init[2 * c] = LLONG_MAX; init[2 * c + 1] = LLONG_MIN; }
-        cudaMemcpyAsync(mm.p, init.data(), 16 * ncols, cudaMemcpyHostToDevice, t->stream);
+        if (mm.ensure(24 * ncols) != cudaSuccess) return bail(fail(GACE_ENOMEM, "minmax scratch"));
+        std::vector<long long> init(3 * ncols);
+        for (uint32_t c = 0; c < ncols; ++c) { init[3 * c] = LLONG_MAX; init[3 * c + 1] = LLONG_MIN; init[3 * c + 2] = 0; }
+        cudaMemcpyAsync(mm.p, init.data(), 24 * ncols, cudaMemcpyHostToDevice, t->stream);
         for (uint32_t c = 0; c < ncols; ++c) {
-            if (launch_minmax(ptrs[c], dtypes[c], nrows, mm.as<long long>(16 * c), t->sms, t->stream) != cudaSuccess) {
+            if (launch_minmax(ptrs[c], dtypes[c], nrows, mm.as<long long>(24 * c), t->sms, t->stream) != cudaSuccess) {
                 mm.release();
                 return bail(fail(GACE_ECUDA, "minmax launch failed"));
             }
             ++g_launches;
         }
-        cudaMemcpyAsync(init.data(), mm.p, 16 * ncols, cudaMemcpyDeviceToHost, t->stream);
+        cudaMemcpyAsync(init.data(), mm.p, 24 * ncols, cudaMemcpyDeviceToHost, t->stream);
         cudaError_t e = cudaStreamSynchronize(t->stream);
         mm.release();
         if (e != cudaSuccess) return bail(fail(GACE_ECUDA, std::string("attach scan: ") + cudaGetErrorString(e)));
-        for (uint32_t c = 0; c < ncols; ++c) { t->dlo[c] = init[2 * c]; t->dhi[c] = init[2 * c + 1]; }
+        for (uint32_t c = 0; c < ncols; ++c) {
+            t->dlo[c] = init[3 * c];
+            t->dhi[c] = init[3 * c + 1];
+            t->clustered[c] = 2ull * (uint64_t)init[3 * c + 2] >= nrows / 4 && nrows >= 4;
+        }
     }
     if (host) {
         if (cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -891,7 +897,7 @@ namespace {
 
 // Source of `struct JitShape` for gace_probe.cuh: the plan's structural decisions as
 // constexpr answers (predicate values stay in the kernel parameters).
-std::string jit_shape_source(const Plan &pl, bool sample, bool i64) {
+std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::vector<uint8_t> &clustered) {
     const ProbeParams &P = pl.P;
     const int nc = (int)P.nslots;
     auto chain = [&](auto f, int n) {
@@ -917,6 +923,8 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64) {
          std::string(P.clamp ? "true" : "false") + "; }\n";
     o += "  __device__ static constexpr bool packs(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(P.slot[i].prim_b >= 0 ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool clust(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(clustered[i] ? "1" : "0"); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool ownh(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(P.slot[i].mode != MODE_NOPRED && P.slot[i].hist_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
     auto gchain = [&](auto f) {
@@ -1086,7 +1094,11 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     int jit_used = 0;
     auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
         if (PP.nslots > 0 && (jm == 1 || (jm == 2 && n >= (1ull << 24)))) {
-            if (shape.empty()) shape = jit_shape_source(pl, sample, i64);
+            if (shape.empty()) {
+                std::vector<uint8_t> cl(pl.slots.size(), 0);
+                for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
+                shape = jit_shape_source(pl, sample, i64, cl);
+            }
             std::string err;
             if (jit_launch(PP, t->device, shape, grid, s, &jit_ms, &err)) {
                 jit_used = 1;
@@ -1427,7 +1439,8 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     std::string err;
     size_t n = 0;
-    if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64), &n, &err)) return fail(GACE_EUNSUPPORTED, err);
+    std::vector<uint8_t> cl(pl.slots.size(), getenv("GACE_DEBUG_CLUSTERED") ? 1 : 0);   // compile that path too
+    if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64, cl), &n, &err)) return fail(GACE_EUNSUPPORTED, err);
     if (cubin_bytes) *cubin_bytes = n;
     return GACE_OK;
 }

@@ -162,23 +162,36 @@ __global__ void fin_output(const FinParams F) {
 
 // ------------------------------------------------------------------ attach / test hook
 
+// Attach-time column statistics: mm[0] = min, mm[1] = max, mm[2] = number of aligned row
+// quads (rows 4q..4q+3) whose four keys are equal (clustered columns, e.g. a sorted key
+// with repeats: the specialised probe then resolves such a quad once).
 __global__ void minmax_kernel(const void *col, int dtype, uint64_t n, long long *mm) {
     long long lo = LLONG_MAX, hi = LLONG_MIN;
+    unsigned long long eq = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const long long v = dtype == 0 ? (long long)__ldg(static_cast<const int32_t *>(col) + i)
-                                       : __ldg(static_cast<const long long *>(col) + i);
-        lo = min(lo, v);
-        hi = max(hi, v);
+    const uint64_t nq = (n + 3) / 4;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+        long long v[4];
+        const uint32_t cnt = n - 4 * q >= 4 ? 4u : (uint32_t)(n - 4 * q);
+        for (uint32_t k = 0; k < 4; ++k) {
+            const uint64_t i = 4 * q + (k < cnt ? k : 0);
+            v[k] = dtype == 0 ? (long long)__ldg(static_cast<const int32_t *>(col) + i)
+                              : __ldg(static_cast<const long long *>(col) + i);
+            lo = min(lo, v[k]);
+            hi = max(hi, v[k]);
+        }
+        eq += (cnt == 4 && v[0] == v[1] && v[1] == v[2] && v[2] == v[3]) ? 1 : 0;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
         hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+        eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
     }
     if ((threadIdx.x & 31) == 0) {
         atomicMin(mm, lo);
         atomicMax(mm + 1, hi);
+        atomicAdd(reinterpret_cast<unsigned long long *>(mm + 2), eq);
     }
 }
 

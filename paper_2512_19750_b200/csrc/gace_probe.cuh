@@ -135,6 +135,7 @@ struct RtShape {
         return P.slot[s].mode != MODE_NOPRED && P.slot[s].hist_addr != kNone;
     }
     __device__ static constexpr bool gpacked(int) { return false; }
+    __device__ static constexpr bool clust(const ProbeParams &, int) { return false; }
     __device__ static constexpr int ga(int) { return 0; }
     __device__ static constexpr int gb(int) { return 0; }
     __device__ static constexpr bool ggrid(int) { return false; }
@@ -221,16 +222,18 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
                                         uint32_t (&bs)[Sh::NC][4]) {
-    const uint32_t *sm = smem32();
     uint32_t u[NB][4], e[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
         const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
+        const uint32_t base = 4 * P.slot[s].lut_w;
+        const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            e[i][k] = lut ? sm[P.slot[s].lut_w + (u[i][k] >> P.slot[s].s1)] : 0u;
+            e[i][k] = lut && (k == 0 || !same) ? *at(base + ((u[i][k] >> P.slot[s].s1) << 2)) : 0u;
+            if (k > 0 && same) e[i][k] = e[i][0];
         }
     }
 #pragma unroll
@@ -326,8 +329,11 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
         uint32_t *R = sm + P.slot[s].hll_idx;
         if (Sh::is32(P, s)) {
             const uint32_t lim = 0xFFFFFFFFu >> lim_l[s];
+            // clustered column, all four keys equal: one hash covers the quad
+            const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+                if (same && k > 0) break;
                 uint32_t h = static_cast<uint32_t>(v[s][k]);
                 h ^= __umulhi(h, 1u << 16);
                 h *= 0x85EBCA6BU;
@@ -336,7 +342,8 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
                 const uint32_t w32 = h * (1u << kHllP) + (1u << (kHllP - 1));
                 const uint32_t idx = __umulhi(h, 1u << kHllP);       // h >> (32 - p)
-                red_max_if(((keep >> k) & 1u) && w32 <= lim && !(dbg & 1), R + idx, __clz(w32) + 1);
+                const bool kept_k = same ? keep != 0 : ((keep >> k) & 1u);
+                red_max_if(kept_k && w32 <= lim && !(dbg & 1), R + idx, __clz(w32) + 1);
             }
         } else {
             const uint64_t lim = ~0ull >> lim_l[s];

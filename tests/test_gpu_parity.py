@@ -303,3 +303,18 @@ def test_specialised_kernel_host_tables(G, oracle, force_jit, name, rate):
     w = synth.get(name, 70_001)
     cols = [x.numpy() for x in w.table()]
     _check(G, oracle, cols, w.preds, w.pairs, rate, 3, w.hll_cols, host=True)
+
+
+def test_clustered_columns(G, oracle, force_jit):
+    """Sorted keys with runs (every aligned row quad equal in most places): the specialised
+    kernel resolves such quads once; results must not change."""
+    g = np.random.default_rng(7)
+    n = 400_003
+    ok = np.repeat(np.arange(n // 4 + 1, dtype=np.int32) * 3 + 5, 4)[:n]
+    ok[1000:1003] = [7, 8, 9]                               # a few broken quads
+    other = g.integers(0, 1000, size=n).astype(np.int32)
+    P = np.array([(0, 5, 0, 100, 90_000), (0, 1, 0, 50_000, 0), (0, 0, 0, 3 * 77 + 5, 0), (1, 5, 1, 10, 500),
+                  (0, 4, 1, 123_456, 0)], dtype=synth.PRED_DTYPE)
+    Q = np.array([(0, 3), (1, 3), (2, 3), (4, 3)], dtype=synth.PAIR_DTYPE)
+    for rate in (1.0, 0.4):
+        _check(G, oracle, [ok, other], P, Q, rate, 5, [0, 1])

@@ -134,13 +134,16 @@ def test_random_batches(G, oracle):
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5", "C5_i64"])
-def test_specialised_kernel_compiles(G, name):
-    """The plan-specialised probe kernel (NVRTC) compiles for every workload shape."""
+def test_specialised_kernel_compiles(G, name, monkeypatch):
+    """The plan-specialised probe kernel (NVRTC) compiles for every workload shape, with
+    and without the clustered-column path."""
     from paper_2512_19750_b200 import gace
     w = synth.get(name, 20_000)
     t = [x.numpy() for x in w.table()]
     dt = [0 if x.dtype == np.int32 else 1 for x in t]
-    for rate in (1.0, 0.25):
+    for rate, clustered in ((1.0, False), (0.25, False), (1.0, True)):
+        if clustered:
+            monkeypatch.setenv("GACE_DEBUG_CLUSTERED", "1")
         n = gace.debug_jit_compile(dt, [int(x.min()) for x in t], [int(x.max()) for x in t], False,
                                    w.preds, w.pairs, w.hll_cols, rate)
         assert n > 1000
