@@ -222,7 +222,8 @@ struct SlotPlan {
     bool clamp = false;
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
-    std::vector<uint32_t> l1;          // level-1 cells (boundary cells: slot-relative record index)
+    uint8_t fmt = FMT32;               // level-1 cell format (gace_plan.h LutFmt)
+    std::vector<uint32_t> l1;          // level-1 cells in FMT32 encoding (boundary: slot-relative record index)
     std::vector<uint4> l2;             // records and nested blocks (slot-relative indices)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
     // roles in the pair grids
@@ -310,7 +311,19 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     return ok;
 }
 
-size_t lut_bytes(const SlotPlan &S) { return 4 * S.l1.size() + 16 * S.l2.size() + 4 * S.lst.size() + 48; }
+size_t lut_bytes(const SlotPlan &S) {
+    return (S.fmt == FMT16 ? 2 : 4) * S.l1.size() + 16 * S.l2.size() + 4 * S.lst.size() + 48;
+}
+
+// MurmurHash3 fmix32 (the int32 HLL hash, DESIGN.md §2 step 6) for exact-cell tables.
+uint32_t host_fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6BU;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35U;
+    h ^= h >> 16;
+    return h;
+}
 
 struct Group {
     int a = -1, b = -1;                // oriented: a = full-resolution side, b = sub-bucket side
@@ -507,16 +520,27 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         S.l2.clear();
         S.lst.clear();
     };
+    // level-1 formats: exact cells (one per key value, HLL info folded in) for small int32
+    // domains; 16-bit cells when buckets <= 512 and packed sub-buckets <= 64; else 32-bit
+    auto small_subs = [&](const SlotPlan &S) { return S.prim_b < 0 || pl.groups[S.prim_b].nbs <= 64; };
     for (size_t i = 0; i < pl.slots.size(); ++i) {
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
-        uint64_t target = 64;
-        while (target < 8192 && target < 32ull * S.T.size()) target <<= 1;
         const uint64_t span = span_of(S);
-        uint32_t sh = 0;
-        while (sh < 31 && (span >> sh) + 1 > target) ++sh;
-        s1[i] = sh;
-        if (!build_lut(S, span, sh)) to_search(S);
+        const bool narrow = S.nb <= 512 && small_subs(S);
+        if (narrow && !S.clamp && S.dtype == GACE_I32 && span < 16384) {
+            S.fmt = FMTEX;
+            s1[i] = 0;
+        } else {
+            S.fmt = narrow ? FMT16 : FMT32;
+            const uint64_t cap = S.fmt == FMT16 ? 16384 : 8192;
+            uint64_t target = 64;
+            while (target < cap && target < 32ull * S.T.size()) target <<= 1;
+            uint32_t sh = 0;
+            while (sh < 31 && (span >> sh) + 1 > target) ++sh;
+            s1[i] = sh;
+        }
+        if (!build_lut(S, span, s1[i]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
     for (int iter = 0; iter < 256; ++iter) {
         size_t tot = 0;
@@ -531,13 +555,14 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         }
         if (tot <= lut_budget || worst < 0) break;
         SlotPlan &S = pl.slots[worst];
+        if (S.fmt == FMTEX) S.fmt = small_subs(S) && S.nb <= 512 ? FMT16 : FMT32;   // exact cells cost too much
         // a coarser level 1 roughly halves it; when nested blocks / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
         if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 4 * S.l1.size()) {
             to_search(S);
             continue;
         }
-        if (!build_lut(S, span_of(S), ++s1[worst])) to_search(S);
+        if (!build_lut(S, span_of(S), ++s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
 
     // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] | hll
@@ -548,7 +573,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         S.l2_idx = w / 4;
         w += 4 * (uint32_t)S.l2.size();
         S.lut_idx = w;
-        w += (uint32_t)S.l1.size();
+        w += S.fmt == FMT16 ? ((uint32_t)S.l1.size() + 1) / 2 : (uint32_t)S.l1.size();
         S.lst_idx = w;
         w += (uint32_t)S.lst.size();
     }
@@ -599,8 +624,24 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     };
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
-        for (size_t k = 0; k < S.l1.size(); ++k)
-            img32[S.lut_idx + k] = (S.l1[k] & kSpecial) ? kSpecial | (S.l2_idx + (S.l1[k] & kRecMask)) : S.l1[k];
+        uint16_t *img16 = reinterpret_cast<uint16_t *>(img32 + S.lut_idx);
+        for (size_t k = 0; k < S.l1.size(); ++k) {
+            const uint32_t c = S.l1[k];
+            const uint32_t idx = c & kIdxMask, sub = (c >> kSubShift) & kSubMask;
+            if (S.fmt == FMT16) {
+                img16[k] = (uint16_t)((c & kSpecial) ? 0x8000u | (S.l2_idx + (c & kRecMask)) : idx | (sub << 9));
+            } else if (S.fmt == FMTEX) {                   // cell k is the key base + k
+                uint32_t hidx = 0, rank = 0;
+                if (S.has_hll) {
+                    const uint32_t h = host_fmix32((uint32_t)(int32_t)(S.base + (int64_t)k));
+                    hidx = h >> (32 - kHllP);
+                    rank = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
+                }
+                img32[S.lut_idx + k] = idx | (sub << 9) | (hidx << 15) | (rank << 27);
+            } else {
+                img32[S.lut_idx + k] = (c & kSpecial) ? kSpecial | (S.l2_idx + (c & kRecMask)) : c;
+            }
+        }
         for (size_t k = 0; k < S.l2.size(); ++k) img4[S.l2_idx + k] = fix(S.l2[k], S);
         for (size_t k = 0; k < S.lst.size(); ++k) img32[S.lst_idx + k] = S.lst[k];
     }
@@ -717,6 +758,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.base = S.base;
         Q.s1 = S.s1;
         Q.lut_w = S.lut_idx;
+        Q.fmt = S.fmt;
         if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
         else { Q.clamp_lo = INT64_MIN; Q.clamp_hi = INT64_MAX; }
         if (S.has_preds && S.mode == MODE_LUT && S.clamp) {
@@ -923,6 +965,8 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
          std::string(P.clamp ? "true" : "false") + "; }\n";
     o += "  __device__ static constexpr bool packs(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(P.slot[i].prim_b >= 0 ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr int fmt(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::to_string((int)P.slot[i].fmt); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool clust(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(clustered[i] ? "1" : "0"); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool ownh(const ProbeParams &, int s) { return " +
@@ -1342,6 +1386,10 @@ struct CheckedTables {
         if ((size_t)i * 4 + 4 > img->size()) { oob = true; return 0; }
         return reinterpret_cast<const uint32_t *>(img->data())[i];
     }
+    uint32_t u16(uint32_t i) const {
+        if ((size_t)i * 2 + 2 > img->size()) { oob = true; return 0; }
+        return reinterpret_cast<const uint16_t *>(img->data())[i];
+    }
 };
 }  // namespace
 
@@ -1389,11 +1437,11 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
-            b = lut_lookup(M, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base);
+            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base);
         } else {
             int64_t x = values[k];
             if (pl.clamp) x = std::min(std::max(x, Q.clamp_lo), Q.clamp_hi);
-            b = lut_lookup(M, Q.lut_w, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
+            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
         }
         if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
         if (b >= S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
@@ -1406,7 +1454,7 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
                                      pl.clamp ? (int32_t)Q.clamp_hi : INT32_MAX) - (uint32_t)Q.base
                 : (uint32_t)((uint64_t)std::min(std::max(values[k], pl.clamp ? Q.clamp_lo : INT64_MIN),
                                                 pl.clamp ? Q.clamp_hi : INT64_MAX) - (uint64_t)Q.base);
-            const uint32_t sub = entry_sub(lut_entry(M, Q.lut_w, Q.s1, u), u);
+            const uint32_t sub = entry_sub(lut_entry(M, Q.fmt, Q.lut_w, Q.s1, u), u);
             const uint32_t want = reinterpret_cast<const uint32_t *>(pl.image.data())[G.map_w + b];
             if (sub != kNone && sub != want) return fail(GACE_EUNSUPPORTED, "internal: packed sub-bucket differs from the map");
         }

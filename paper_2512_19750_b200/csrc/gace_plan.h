@@ -45,6 +45,15 @@ constexpr uint32_t kSubMask = 0x7Fu;
 constexpr uint32_t kSubMax = 127;           // sub-buckets per group side that can be packed
 constexpr uint32_t kIncShift = 21;          // sub-bucket increment flags of the 3 thresholds
 constexpr uint32_t kRecMask = 0x3FFFFFFFu;  // level-1 boundary cell: record index
+
+// Level-1 cell formats (per column, chosen by the planner):
+enum LutFmt : uint8_t {
+    FMT32 = 0,   // u32: plain = idx (0..13) | sub (14..20); boundary = kSpecial | record index
+    FMT16 = 1,   // u16: plain = idx (0..8) | sub (9..14);   boundary = 0x8000 | record index (15 bits)
+    FMTEX = 2,   // u32, one cell per key value (s1 = 0, never a boundary): idx (0..8) | sub (9..14) |
+                 //      HLL register index (15..26) | HLL rank (27..31) of that key (int32 columns)
+};
+constexpr uint32_t kRecMask16 = 0x7FFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 #if defined(__CUDACC__)
@@ -69,14 +78,25 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 //
 // Final (direct or list) record for offset u, walking nested blocks (a plain cell is
 // returned as a direct record without thresholds).  `M` reads the table image:
-// M.u4(i) / M.u32(i) (shared memory in the kernel; a bounds-checked copy in
-// gace_debug_buckets).
+// M.u4(i) / M.u32(i) / M.u16(i) (shared memory in the kernel; a bounds-checked copy in
+// gace_debug_buckets).  lut_w: u32 index of the level-1 table.
 template <class Mem>
-GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t u) {
-    const uint32_t c = M.u32(lut_w + (u >> s1));
-    if (!(c & kSpecial)) return make_uint4(c, kNoThr, kNoThr, kNoThr);
+GACE_HD uint4 lut_entry(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t s1, uint32_t u) {
+    uint32_t rec;
+    if (fmt == FMT16) {
+        const uint32_t c = M.u16(2 * lut_w + (u >> s1));
+        if (!(c & 0x8000u)) return make_uint4((c & 0x1FFu) | (((c >> 9) & 63u) << kSubShift), kNoThr, kNoThr, kNoThr);
+        rec = c & kRecMask16;
+    } else if (fmt == FMTEX) {
+        const uint32_t c = M.u32(lut_w + u);
+        return make_uint4((c & 0x1FFu) | (((c >> 9) & 63u) << kSubShift), kNoThr, kNoThr, kNoThr);
+    } else {
+        const uint32_t c = M.u32(lut_w + (u >> s1));
+        if (!(c & kSpecial)) return make_uint4(c, kNoThr, kNoThr, kNoThr);
+        rec = c & kRecMask;
+    }
     uint32_t s = s1;
-    uint4 e = M.u4(c & kRecMask);
+    uint4 e = M.u4(rec);
     while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-records (nested)
         const uint32_t sc = (e.x >> 24) & 63u;
         e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
@@ -87,8 +107,8 @@ GACE_HD uint4 lut_entry(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t u) {
 
 // Bucket index of offset u (full walk).
 template <class Mem>
-GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t u) {
-    const uint4 e = lut_entry(M, lut_w, s1, u);
+GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t s1, uint32_t u) {
+    const uint4 e = lut_entry(M, fmt, lut_w, s1, u);
     uint32_t b = e.x & kIdxMask;
     if (e.x & kList) {
         const uint32_t n = (e.x >> 24) & 63u;
@@ -122,6 +142,8 @@ struct SlotParams {
     uint8_t mode;           // SlotMode
     uint8_t has_hll;
     int8_t prim_b;          // group whose sub-bucket this column's entries pack, or -1
+    uint8_t fmt;            // LutFmt of the level-1 table
+    uint8_t pad[3];
 };
 
 struct GroupParams {

@@ -103,11 +103,12 @@ __device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, i
 struct SmemTables {
     __device__ __forceinline__ uint4 u4(uint32_t i) const { return g_smem[i]; }
     __device__ __forceinline__ uint32_t u32(uint32_t i) const { return smem32()[i]; }
+    __device__ __forceinline__ uint32_t u16(uint32_t i) const { return reinterpret_cast<const uint16_t *>(g_smem)[i]; }
 };
 
 // Full walk through nested cells and lists (out of line: rare special entries only).
-__device__ __noinline__ uint32_t lut_bucket(uint32_t lut_w, uint32_t s1, uint32_t u) {
-    return lut_lookup(SmemTables{}, lut_w, s1, u);
+__device__ __noinline__ uint32_t lut_bucket(uint32_t fmt, uint32_t lut_w, uint32_t s1, uint32_t u) {
+    return lut_lookup(SmemTables{}, fmt, lut_w, s1, u);
 }
 
 __device__ __forceinline__ bool keep_row(const ProbeParams &P, uint64_t g) {
@@ -136,6 +137,7 @@ struct RtShape {
     }
     __device__ static constexpr bool gpacked(int) { return false; }
     __device__ static constexpr bool clust(const ProbeParams &, int) { return false; }
+    __device__ static int fmt(const ProbeParams &P, int s) { return P.slot[s].fmt; }
     __device__ static constexpr int ga(int) { return 0; }
     __device__ static constexpr int gb(int) { return 0; }
     __device__ static constexpr bool ggrid(int) { return false; }
@@ -202,8 +204,8 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
 // Bucket | sub-bucket << 16 of a key in a boundary cell: its 16-byte record (<= 3
 // thresholds), or the full walk for nested / list records (sub-bucket via the map).
 template <class Sh>
-__device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s, uint32_t e, uint32_t u) {
-    const uint4 r = g_smem[e & kRecMask];
+__device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s, uint32_t rec, uint32_t u) {
+    const uint4 r = g_smem[rec];
     if (!(r.x & kSpecial)) {
         const uint32_t c1 = u > r.y, c2 = u > r.z, c3 = u > r.w;
         uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
@@ -212,7 +214,7 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
                   (c3 & (r.x >> (kIncShift + 2)))) << 16;
         return b;
     }
-    const uint32_t b = lut_bucket(P.slot[s].lut_w, P.slot[s].s1, u);
+    const uint32_t b = lut_bucket(Sh::fmt(P, s), P.slot[s].lut_w, P.slot[s].s1, u);
     return b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
 }
 
@@ -221,29 +223,40 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
 // branch to their record; binary-search columns go through the out-of-line search.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
-                                        uint32_t (&bs)[Sh::NC][4]) {
+                                        uint32_t (&bs)[Sh::NC][4], uint32_t (&ex)[Sh::NC][4]) {
     uint32_t u[NB][4], e[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
         const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
         const uint32_t base = 4 * P.slot[s].lut_w;
+        const int f = Sh::fmt(P, s);
         const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            e[i][k] = lut && (k == 0 || !same) ? *at(base + ((u[i][k] >> P.slot[s].s1) << 2)) : 0u;
+            const uint32_t cell = f == FMTEX ? u[i][k] : u[i][k] >> P.slot[s].s1;
+            if (!lut || (k > 0 && same)) e[i][k] = 0u;
+            else if (f == FMT16) e[i][k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
+            else e[i][k] = *at(base + 4 * cell);
             if (k > 0 && same) e[i][k] = e[i][0];
         }
+        ex[s][0] = e[i][0]; ex[s][1] = e[i][1]; ex[s][2] = e[i][2]; ex[s][3] = e[i][3];
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
+        const int f = Sh::fmt(P, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             // plain cell: bucket | sub-bucket << 16 straight from the level-1 word
-            bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
-            if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k], u[i][k]);
+            if (f == FMT32) {
+                bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
+                if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
+            } else {
+                bs[s][k] = (e[i][k] & 0x1FFu) | (Sh::packs(P, s) ? (e[i][k] << 7) & (63u << 16) : 0u);
+                if (f == FMT16 && (e[i][k] & 0x8000u)) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask16, u[i][k]);
+            }
         }
     }
 #pragma unroll
@@ -308,9 +321,9 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
     for (int s = 0; s < NC; ++s)
         if (Sh::active(P, s)) decode<Sh>(P, s, r[s], v[s]);
-    uint32_t bs[NC][4];
-    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bs);
-    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bs);
+    uint32_t bs[NC][4], ex[NC][4];
+    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bs, ex);
+    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bs, ex);
     // own bucket histograms (columns that are no grid's full-resolution side)
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
@@ -327,7 +340,12 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
     for (int s = 0; s < NC; ++s) {
         if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
         uint32_t *R = sm + P.slot[s].hll_idx;
-        if (Sh::is32(P, s)) {
+        if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {   // (index, rank) precomputed per key
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                red_max_if(((keep >> k) & 1u) && (ex[s][k] >> 27) > lim_l[s] && !(dbg & 1), R + ((ex[s][k] >> 15) & 0xFFFu),
+                           ex[s][k] >> 27);
+        } else if (Sh::is32(P, s)) {
             const uint32_t lim = 0xFFFFFFFFu >> lim_l[s];
             // clustered column, all four keys equal: one hash covers the quad
             const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
