@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -160,6 +161,11 @@ struct gace_table {
     cudaEvent_t ev_copied[2]{}, ev_free[2]{}, ev_c0{}, ev_c1{};
     gace_timing last{};
     std::mutex mu;
+    // plan cache: the last batch's plan and its uploaded device blob (repeated probes of the
+    // same batch skip planning and the H2D of the tables)
+    std::string plan_key;
+    std::shared_ptr<void> plan;
+    size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0;
 };
 
 namespace {
@@ -1066,30 +1072,42 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (npairs && !joint_counts) return fail(GACE_EINVAL, "joint_counts is NULL");
     if (nh && !hll_regs) return fail(GACE_EINVAL, "hll_regs is NULL");
 
-    Plan pl;
-    st = make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, pl);
-    if (st) return st;
     CUDA_TRY(cudaSetDevice(t->device));
-
-    // ---- one pinned blob -> one H2D copy: image | direct | jobs | fpreds | fpairs | bps
-    size_t off = 0;
-    const size_t o_img = off; off = align16(off + pl.image.size());
-    const size_t o_dir = off; off = align16(off + pl.direct.size() * sizeof(DirectPair));
-    const size_t o_job = off; off = align16(off + pl.jobs.size() * sizeof(FinJob));
-    const size_t o_fp = off; off = align16(off + pl.fpreds.size() * sizeof(FinPred));
-    const size_t o_fq = off; off = align16(off + pl.fpairs.size() * sizeof(FinPair));
-    const size_t o_bps = off; off = align16(off + pl.bps.size() * sizeof(int64_t));
-    const size_t blob = std::max<size_t>(off, 16);
     CUDA_TRY(cudaStreamSynchronize(t->stream));   // previous call fully done with the staging buffers
-    if (t->h_plan.ensure(blob) != cudaSuccess || t->d_plan.ensure(blob) != cudaSuccess)
-        return fail(GACE_ENOMEM, "plan buffers");
-    char *hb = t->h_plan.as<char>();
-    memcpy(hb + o_img, pl.image.data(), pl.image.size());
-    if (!pl.direct.empty()) memcpy(hb + o_dir, pl.direct.data(), pl.direct.size() * sizeof(DirectPair));
-    if (!pl.jobs.empty()) memcpy(hb + o_job, pl.jobs.data(), pl.jobs.size() * sizeof(FinJob));
-    if (!pl.fpreds.empty()) memcpy(hb + o_fp, pl.fpreds.data(), pl.fpreds.size() * sizeof(FinPred));
-    if (!pl.fpairs.empty()) memcpy(hb + o_fq, pl.fpairs.data(), pl.fpairs.size() * sizeof(FinPair));
-    if (!pl.bps.empty()) memcpy(hb + o_bps, pl.bps.data(), pl.bps.size() * sizeof(int64_t));
+    std::string key;
+    key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 8);
+    key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
+    if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
+    if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
+    if (!t->plan || key != t->plan_key) {
+        auto fresh = std::make_shared<Plan>();
+        st = make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh);
+        if (st) return st;
+        const Plan &q = *fresh;
+        // ---- one pinned blob -> one H2D copy: image | direct | jobs | fpreds | fpairs | bps
+        size_t off = 0;
+        t->o_img = off; off = align16(off + q.image.size());
+        t->o_dir = off; off = align16(off + q.direct.size() * sizeof(DirectPair));
+        t->o_job = off; off = align16(off + q.jobs.size() * sizeof(FinJob));
+        t->o_fp = off; off = align16(off + q.fpreds.size() * sizeof(FinPred));
+        t->o_fq = off; off = align16(off + q.fpairs.size() * sizeof(FinPair));
+        t->o_bps = off; off = align16(off + q.bps.size() * sizeof(int64_t));
+        t->blob = std::max<size_t>(off, 16);
+        if (t->h_plan.ensure(t->blob) != cudaSuccess || t->d_plan.ensure(t->blob) != cudaSuccess)
+            return fail(GACE_ENOMEM, "plan buffers");
+        char *hb = t->h_plan.as<char>();
+        memcpy(hb + t->o_img, q.image.data(), q.image.size());
+        if (!q.direct.empty()) memcpy(hb + t->o_dir, q.direct.data(), q.direct.size() * sizeof(DirectPair));
+        if (!q.jobs.empty()) memcpy(hb + t->o_job, q.jobs.data(), q.jobs.size() * sizeof(FinJob));
+        if (!q.fpreds.empty()) memcpy(hb + t->o_fp, q.fpreds.data(), q.fpreds.size() * sizeof(FinPred));
+        if (!q.fpairs.empty()) memcpy(hb + t->o_fq, q.fpairs.data(), q.fpairs.size() * sizeof(FinPair));
+        if (!q.bps.empty()) memcpy(hb + t->o_bps, q.bps.data(), q.bps.size() * sizeof(int64_t));
+        CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, t->blob, cudaMemcpyHostToDevice, t->stream));
+        t->plan = fresh;
+        t->plan_key.swap(key);
+    }
+    const Plan &pl = *static_cast<const Plan *>(t->plan.get());
+    const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
 
     const int grid = t->sms;
     const size_t acc_bytes = std::max<size_t>(8ull * pl.acc_words, 8);
@@ -1103,7 +1121,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
 
     cudaStream_t s = t->stream;
     CUDA_TRY(cudaEventRecord(t->ev[0], s));
-    CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, blob, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemsetAsync(t->d_acc.p, 0, acc_bytes, s));
     CUDA_TRY(cudaMemsetAsync(t->d_nsamp.p, 0, 8, s));
     CUDA_TRY(cudaEventRecord(t->ev[1], s));
