@@ -229,6 +229,7 @@ struct SlotPlan {
     int64_t base = 0, clamp_lo = 0, clamp_hi = 0;
     uint32_t s1 = 0;
     uint8_t fmt = FMT32;               // level-1 cell format (gace_plan.h LutFmt)
+    uint32_t sb = 16;                  // FMT1T: bucket field width of bs
     std::vector<uint32_t> l1;          // level-1 cells in FMT32 encoding (boundary: slot-relative record index)
     std::vector<uint4> l2;             // records and nested blocks (slot-relative indices)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
@@ -303,6 +304,24 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     };
     const uint64_t ncells = (span >> s1) + 1;
     const uint64_t csize = 1ull << s1;
+    if (S.fmt == FMT1T) {      // one in-cell threshold per cell (gace_plan.h FMT1T)
+        auto bs = [&](uint32_t b) { return (b + 1) | (sub_of(b) << S.sb); };
+        for (uint64_t k = 0; k < ncells && ok; ++k) {
+            const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
+            const uint32_t b0 = le(lo), cnt = le(hi) - b0;       // breakpoints in (lo, hi]
+            if (cnt == 0) {
+                S.l1.push_back(bs(b0) - 1);                        // t = 0: always "crossed"
+            } else if (cnt == 1) {
+                const uint32_t t = (uint32_t)(toff[b0] - lo);      // in [1, 2^s1)
+                S.l1.push_back((t << (32 - s1)) | (cuts(b0) ? 1u << (30 - s1) : 0u) | bs(b0));
+            } else {
+                const uint4 e = node(lo, hi, s1);
+                S.l1.push_back(t1_special(s1) | (uint32_t)S.l2.size());   // slot-relative record
+                S.l2.push_back(e);
+            }
+        }
+        return ok;
+    }
     for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
         const uint32_t b0 = le(lo);
@@ -319,6 +338,13 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
 
 size_t lut_bytes(const SlotPlan &S) {
     return (S.fmt == FMT16 ? 2 : 4) * S.l1.size() + 16 * S.l2.size() + 4 * S.lst.size() + 48;
+}
+
+// FMT1T field budget: bucket + 1 in sb bits, the packed sub-bucket above it, and record
+// indices (< 2^14 uint4 in 227 KB) all within the 30 - s1 data bits.
+uint32_t t1_max_s1(const SlotPlan &S, uint32_t nsub) {
+    const uint32_t need = std::max<uint32_t>(S.sb + ceil_log2(nsub), 14);
+    return need >= 29 ? 0 : std::min<uint32_t>(20, 30 - need);
 }
 
 // MurmurHash3 fmix32 (the int32 HLL hash, DESIGN.md §2 step 6) for exact-cell tables.
@@ -362,6 +388,26 @@ struct Plan {
 };
 
 constexpr size_t kSmemBudget = kMaxSmem - 1024;   // keep 1 KB for static shared memory
+
+// Plan summary on stderr (env GACE_PLAN_DUMP; design inspection only).
+void dump_plan(const Plan &pl) {
+    for (size_t i = 0; i < pl.slots.size(); ++i) {
+        const SlotPlan &S = pl.slots[i];
+        size_t special = 0;
+        for (uint32_t c : S.l1) special += (c & (S.fmt == FMT1T ? t1_special(S.s1) : kSpecial)) ? 1 : 0;
+        fprintf(stderr, "slot %zu col %d dt %d mode %d fmt %d s1 %u sb %u nb %u cells %zu special %zu (%.2f%%) l2 %zu lst %zu "
+                "hll %d hist_grp %d prim_b %d span %llu\n", i, S.col, S.dtype, (int)S.mode, (int)S.fmt, S.s1, S.sb, S.nb,
+                S.l1.size(), special, S.l1.empty() ? 0.0 : 100.0 * special / S.l1.size(), S.l2.size(), S.lst.size(),
+                (int)S.has_hll, S.hist_grp, S.prim_b, (unsigned long long)((uint64_t)S.dh - (uint64_t)S.dl));
+    }
+    for (size_t g = 0; g < pl.groups.size(); ++g) {
+        const Group &G = pl.groups[g];
+        fprintf(stderr, "group %zu a %d b %d na %u nbs %u pairs %zu direct %d packed %d\n", g, G.a, G.b, G.na, G.nbs,
+                G.pq.size(), (int)G.direct, (int)G.packed);
+    }
+    fprintf(stderr, "smem %u image %zu acc_words %u hll_bytes %u\n", pl.smem_bytes, pl.image.size(), pl.acc_words,
+            pl.hll_bytes);
+}
 
 gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
                       uint32_t nq, uint64_t hll_mask, Plan &pl) {
@@ -529,14 +575,31 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     // level-1 formats: exact cells (one per key value, HLL info folded in) for small int32
     // domains; 16-bit cells when buckets <= 512 and packed sub-buckets <= 64; else 32-bit
     auto small_subs = [&](const SlotPlan &S) { return S.prim_b < 0 || pl.groups[S.prim_b].nbs <= 64; };
+    auto nsub_of = [&](const SlotPlan &S) -> uint32_t {
+        return S.prim_b < 0 ? 1u : (uint32_t)pl.groups[S.prim_b].TB.size() + 1;
+    };
+    const bool use_t1 = !getenv("GACE_NO_T1");      // design A/B switch (GACE_NO_T1=1: older formats)
     for (size_t i = 0; i < pl.slots.size(); ++i) {
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
         const uint64_t span = span_of(S);
         const bool narrow = S.nb <= 512 && small_subs(S);
+        S.sb = ceil_log2((uint64_t)S.nb + 1);
+        uint32_t t1s = 0;                    // FMT1T level-1 shift: ~64 cells per breakpoint, <= 16K cells
+        {
+            uint64_t target = 64;
+            while (target < 16384 && target < 64ull * S.T.size()) target <<= 1;
+            while (t1s < 31 && (span >> t1s) + 1 > target) ++t1s;
+            t1s = std::max<uint32_t>(t1s, 1);
+            const uint32_t mx = t1_max_s1(S, nsub_of(S));     // finer than the target when the fields force it
+            if (t1s > mx && mx >= 1 && (span >> mx) + 1 <= 16384) t1s = mx;
+        }
         if (narrow && !S.clamp && S.dtype == GACE_I32 && span < 16384) {
             S.fmt = FMTEX;
             s1[i] = 0;
+        } else if (use_t1 && t1s <= t1_max_s1(S, nsub_of(S))) {
+            S.fmt = FMT1T;
+            s1[i] = t1s;
         } else {
             S.fmt = narrow ? FMT16 : FMT32;
             const uint64_t cap = S.fmt == FMT16 ? 16384 : 8192;
@@ -562,6 +625,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (tot <= lut_budget || worst < 0) break;
         SlotPlan &S = pl.slots[worst];
         if (S.fmt == FMTEX) S.fmt = small_subs(S) && S.nb <= 512 ? FMT16 : FMT32;   // exact cells cost too much
+        if (S.fmt == FMT1T && s1[worst] + 1 > t1_max_s1(S, nsub_of(S)))
+            S.fmt = small_subs(S) && S.nb <= 512 ? FMT16 : FMT32;                  // thresholds no longer fit
         // a coarser level 1 roughly halves it; when nested blocks / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
         if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 4 * S.l1.size()) {
@@ -634,7 +699,9 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         for (size_t k = 0; k < S.l1.size(); ++k) {
             const uint32_t c = S.l1[k];
             const uint32_t idx = c & kIdxMask, sub = (c >> kSubShift) & kSubMask;
-            if (S.fmt == FMT16) {
+            if (S.fmt == FMT1T) {
+                img32[S.lut_idx + k] = (c & t1_special(S.s1)) ? t1_special(S.s1) | (S.l2_idx + (c & t1_dmask(S.s1))) : c;
+            } else if (S.fmt == FMT16) {
                 img16[k] = (uint16_t)((c & kSpecial) ? 0x8000u | (S.l2_idx + (c & kRecMask)) : idx | (sub << 9));
             } else if (S.fmt == FMTEX) {                   // cell k is the key base + k
                 uint32_t hidx = 0, rank = 0;
@@ -741,6 +808,9 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     for (uint32_t k = 0; k < dlist.size(); ++k) {
         DEnt &E = dlist[k];
         E.D.acc_idx = direct_idx + k;
+        const Group &G = pl.groups[E.g];
+        if (pl.slots[G.a].fmt == FMT1T) { ++E.D.la; ++E.D.ha; }      // 1-based buckets
+        if (pl.slots[G.b].fmt == FMT1T) { ++E.D.lb; ++E.D.hb; }
         pl.fpairs[E.q].pre = direct_idx + k - pl.acc_idx;
         if (dend[E.g] == 0) dbeg[E.g] = k;
         dend[E.g] = k + 1;
@@ -765,6 +835,16 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.s1 = S.s1;
         Q.lut_w = S.lut_idx;
         Q.fmt = S.fmt;
+        Q.sb = (uint8_t)(S.fmt == FMT1T ? S.sb : 16);
+        Q.bmask = (1u << Q.sb) - 1u;
+        if (S.fmt == FMT1T) {
+            Q.t1_mul = 1u << (32 - S.s1);
+            Q.t1_ones = Q.t1_mul - 1u;
+            Q.t1_dmask = t1_dmask(S.s1);
+            Q.t1_sp = t1_special(S.s1);
+            Q.t1_cutsh = 30 - S.s1 - S.sb;
+        }
+        if (S.fmt == FMT1T && S.hist_w != kNone) Q.hist_addr -= 4;     // 1-based buckets
         if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
         else { Q.clamp_lo = INT64_MIN; Q.clamp_hi = INT64_MAX; }
         if (S.has_preds && S.mode == MODE_LUT && S.clamp) {
@@ -791,6 +871,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         R.nbs = G.nbs;
         R.grid_addr = G.direct ? kNone : 4 * G.grid_w;
         R.map_addr = G.direct ? kNone : 4 * G.map_w;
+        if (!G.direct && pl.slots[G.a].fmt == FMT1T) R.grid_addr -= 4 * G.nbs;   // 1-based A buckets
+        if (!G.direct && pl.slots[G.b].fmt == FMT1T) R.map_addr -= 4;          // 1-based B buckets
     }
     P.ngroups = (uint32_t)pl.groups.size();
     P.clamp = pl.clamp ? 1u : 0u;      // (the specialised kernel bakes this in: set it here)
@@ -801,6 +883,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     P.hll_off = pl.hll_off;
     P.hll_bytes = pl.hll_bytes;
     P.smem_bytes = pl.smem_bytes;
+    if (getenv("GACE_PLAN_DUMP")) dump_plan(pl);
     return GACE_OK;
 }
 
@@ -1110,7 +1193,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
 
     const int grid = t->sms;
-    const size_t acc_bytes = std::max<size_t>(8ull * pl.acc_words, 8);
+    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 16;   // + merged HLL bound registers
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
@@ -1131,6 +1214,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     for (size_t i = 0; i < pl.slots.size(); ++i)
         if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
     P.g_acc = t->d_acc.as<unsigned long long>();
+    P.g_hll_glob = t->d_acc.as<uint32_t>(8ull * pl.acc_words);
     P.g_hll_part = t->d_part.as<uint8_t>();
     P.g_nsamp = t->d_nsamp.as<unsigned long long>();
     P.thr = threshold_of(sample_rate);
@@ -1454,11 +1538,11 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
-            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base);
+            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base, Q.sb);
         } else {
             int64_t x = values[k];
             if (pl.clamp) x = std::min(std::max(x, Q.clamp_lo), Q.clamp_hi);
-            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base));
+            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)((uint64_t)x - (uint64_t)Q.base), Q.sb);
         }
         if (M.oob) return fail(GACE_EUNSUPPORTED, "internal: table read out of range");
         if (b >= S.nb) return fail(GACE_EUNSUPPORTED, "internal: bucket out of range");
@@ -1471,7 +1555,13 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
                                      pl.clamp ? (int32_t)Q.clamp_hi : INT32_MAX) - (uint32_t)Q.base
                 : (uint32_t)((uint64_t)std::min(std::max(values[k], pl.clamp ? Q.clamp_lo : INT64_MIN),
                                                 pl.clamp ? Q.clamp_hi : INT64_MAX) - (uint64_t)Q.base);
-            const uint32_t sub = entry_sub(lut_entry(M, Q.fmt, Q.lut_w, Q.s1, u), u);
+            uint32_t sub;
+            if (Q.fmt == FMT1T) {
+                const uint32_t v = t1_bs(M, Q.lut_w, Q.s1, Q.sb, u);
+                sub = (v & 0x80000000u) ? kNone : v >> Q.sb;
+            } else {
+                sub = entry_sub(lut_entry(M, Q.fmt, Q.lut_w, Q.s1, u), u);
+            }
             const uint32_t want = reinterpret_cast<const uint32_t *>(pl.image.data())[G.map_w + b];
             if (sub != kNone && sub != want) return fail(GACE_EUNSUPPORTED, "internal: packed sub-bucket differs from the map");
         }

@@ -52,6 +52,15 @@ enum LutFmt : uint8_t {
     FMT16 = 1,   // u16: plain = idx (0..8) | sub (9..14);   boundary = 0x8000 | record index (15 bits)
     FMTEX = 2,   // u32, one cell per key value (s1 = 0, never a boundary): idx (0..8) | sub (9..14) |
                  //      HLL register index (15..26) | HLL rank (27..31) of that key (int32 columns)
+    FMT1T = 3,   // u32 with one in-cell threshold (specialised kernel only; 1 <= s1 <= 20):
+                 //   bits [32-s1, 32): t = in-cell offset of the cell's breakpoint (0: none)
+                 //   bit  31-s1      : special (>= 2 breakpoints): low bits = uint4 record index
+                 //   bit  30-s1      : the breakpoint also cuts the packed sub-bucket
+                 //   bits [0, 30-s1) : bs_lo = (bucket + 1) | sub << sb below the breakpoint
+                 //   plain cell: t = 0 and bs_lo = bs - 1, so "offset >= t" always adds the 1 back.
+                 // Decode: c = (u << (32-s1) | ones) >= e;  bs = c ? bs_lo + 1 + cut << sb : bs_lo.
+                 // Buckets are 1-based in this format (the planner shifts the slot's histogram,
+                 // grid and map addresses and its direct-pair intervals by one bucket).
 };
 constexpr uint32_t kRecMask16 = 0x7FFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -76,6 +85,25 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 //     list   : x = kSpecial | kList | n << 24 | first bucket index, y = u32 index of n sorted
 //              breakpoint offsets t; bucket = first + #{t : u >= t} (sub-bucket via the map)
 //
+// Packed sub-bucket of offset u from a DIRECT entry (kNone for a list entry).
+GACE_HD uint32_t entry_sub(const uint4 &e, uint32_t u) {
+    if (e.x & kSpecial) return kNone;
+    return ((e.x >> kSubShift) & kSubMask) + ((u > e.y && (e.x >> kIncShift) & 1u) ? 1u : 0u) +
+           ((u > e.z && (e.x >> (kIncShift + 1)) & 1u) ? 1u : 0u) + ((u > e.w && (e.x >> (kIncShift + 2)) & 1u) ? 1u : 0u);
+}
+
+// Final (direct or list) record reached from record `rec` of a cell of 2^s offsets.
+template <class Mem>
+GACE_HD uint4 rec_walk(const Mem &M, uint32_t rec, uint32_t s, uint32_t u) {
+    uint4 e = M.u4(rec);
+    while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-records (nested)
+        const uint32_t sc = (e.x >> 24) & 63u;
+        e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
+        s = sc;
+    }
+    return e;
+}
+
 // Final (direct or list) record for offset u, walking nested blocks (a plain cell is
 // returned as a direct record without thresholds).  `M` reads the table image:
 // M.u4(i) / M.u32(i) / M.u16(i) (shared memory in the kernel; a bounds-checked copy in
@@ -95,20 +123,12 @@ GACE_HD uint4 lut_entry(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t s1,
         if (!(c & kSpecial)) return make_uint4(c, kNoThr, kNoThr, kNoThr);
         rec = c & kRecMask;
     }
-    uint32_t s = s1;
-    uint4 e = M.u4(rec);
-    while ((e.x & (kSpecial | kList)) == kSpecial) {        // block of sub-records (nested)
-        const uint32_t sc = (e.x >> 24) & 63u;
-        e = M.u4(e.y + ((u & ((1u << s) - 1u)) >> sc));
-        s = sc;
-    }
-    return e;
+    return rec_walk(M, rec, s1, u);
 }
 
-// Bucket index of offset u (full walk).
+// Bucket index of offset u from a final (direct or list) record.
 template <class Mem>
-GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t s1, uint32_t u) {
-    const uint4 e = lut_entry(M, fmt, lut_w, s1, u);
+GACE_HD uint32_t rec_bucket(const Mem &M, const uint4 &e, uint32_t u) {
     uint32_t b = e.x & kIdxMask;
     if (e.x & kList) {
         const uint32_t n = (e.x >> 24) & 63u;
@@ -118,11 +138,28 @@ GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t
     return b + (u > e.y ? 1u : 0u) + (u > e.z ? 1u : 0u) + (u > e.w ? 1u : 0u);
 }
 
-// Packed sub-bucket of offset u from a DIRECT entry (kNone for a list entry).
-GACE_HD uint32_t entry_sub(const uint4 &e, uint32_t u) {
-    if (e.x & kSpecial) return kNone;
-    return ((e.x >> kSubShift) & kSubMask) + ((u > e.y && (e.x >> kIncShift) & 1u) ? 1u : 0u) +
-           ((u > e.z && (e.x >> (kIncShift + 1)) & 1u) ? 1u : 0u) + ((u > e.w && (e.x >> (kIncShift + 2)) & 1u) ? 1u : 0u);
+// FMT1T: field helpers (gace_plan.h LutFmt) and the bs = (bucket + 1) | sub << sb of offset u.
+GACE_HD uint32_t t1_special(uint32_t s1) { return 1u << (31u - s1); }
+GACE_HD uint32_t t1_dmask(uint32_t s1) { return (1u << (30u - s1)) - 1u; }
+template <class Mem>
+GACE_HD uint32_t t1_bs(const Mem &M, uint32_t lut_w, uint32_t s1, uint32_t sb, uint32_t u) {
+    const uint32_t e = M.u32(lut_w + (u >> s1));
+    if (e & t1_special(s1)) {                     // >= 2 breakpoints: walk the cell's record
+        const uint4 r = rec_walk(M, e & t1_dmask(s1), s1, u);
+        const uint32_t b = rec_bucket(M, r, u);
+        const uint32_t sub = entry_sub(r, u);     // kNone for list records (caller maps it)
+        return (b + 1u) | (sub == kNone ? 0u : sub << sb) | (sub == kNone ? 0x80000000u : 0u);
+    }
+    const uint32_t t = e >> (32u - s1), o = u & ((1u << s1) - 1u);
+    const uint32_t lo = e & t1_dmask(s1), cut = (e >> (30u - s1)) & 1u;
+    return o >= t ? lo + 1u + (cut << sb) : lo;
+}
+
+// Bucket index of offset u (full walk).
+template <class Mem>
+GACE_HD uint32_t lut_lookup(const Mem &M, uint32_t fmt, uint32_t lut_w, uint32_t s1, uint32_t u, uint32_t sb = 16) {
+    if (fmt == FMT1T) return (t1_bs(M, lut_w, s1, sb, u) & ((1u << sb) - 1u)) - 1u;
+    return rec_bucket(M, lut_entry(M, fmt, lut_w, s1, u), u);
 }
 
 enum SlotMode : uint8_t { MODE_LUT = 0, MODE_SEARCH = 1, MODE_NOPRED = 2 };
@@ -143,7 +180,15 @@ struct SlotParams {
     uint8_t has_hll;
     int8_t prim_b;          // group whose sub-bucket this column's entries pack, or -1
     uint8_t fmt;            // LutFmt of the level-1 table
-    uint8_t pad[3];
+    uint8_t sb;             // sub-bucket shift inside bs (16, or the FMT1T bucket field width)
+    uint8_t pad[2];
+    uint32_t bmask;         // (1 << sb) - 1: bucket field of bs
+    // FMT1T decode constants (gace_plan.h LutFmt)
+    uint32_t t1_mul;        // 2^(32 - s1)
+    uint32_t t1_ones;       // 2^(32 - s1) - 1
+    uint32_t t1_dmask;      // data bits
+    uint32_t t1_sp;         // special flag
+    uint32_t t1_cutsh;      // cut flag >> t1_cutsh lands on bit sb
 };
 
 struct GroupParams {
@@ -181,6 +226,8 @@ struct ProbeParams {
     unsigned long long *g_acc;             // u64[acc_words], summed over CTAs (and launches)
     uint8_t *g_hll_part;                   // [CTA][hll_bytes] per-CTA register partials
     unsigned long long *g_nsamp;
+    uint32_t *g_hll_glob;                  // u32[hll_bytes]: registers merged across CTAs while the
+                                           // scan runs (max; zeroed per probe) -> HLL skip bound
     uint64_t nrows;                        // rows in this launch
     uint64_t row0;                         // global id of the launch's first row
     uint64_t thr;                          // floor(rate * 2^64)

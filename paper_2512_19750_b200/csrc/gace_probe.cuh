@@ -75,17 +75,34 @@ __device__ __forceinline__ void lds128_if(bool pred, const uint4 *addr, uint4 &r
                  : "r"((uint32_t)pred), "r"(saddr(addr)));
 }
 
-// Warp-cooperative exact minimum of a column's 4096 registers (whole warp active).
-__device__ __noinline__ uint32_t hll_min(uint32_t hll_idx) {
-    const uint4 *R = reinterpret_cast<const uint4 *>(smem32() + hll_idx);
-    const uint32_t lane = threadIdx.x & 31;
+// Lower bound L of the FINAL registers of HLL column slot s (whole warp active).  The
+// CTAs merge their registers into g_hll_glob (max) while the scan runs: this warp pulls
+// its 1/nwarps slice of the merged registers, pushes the CTA's own values where they are
+// higher, and records the slice minimum in s_slmin; L = min over the slice minima.  The
+// merged registers only grow and every value in them came from some CTA's own rows, so a
+// key whose rank is <= L cannot change the final max: skipping it is exact.
+__shared__ uint32_t s_slmin[kMaxSlots][kThreads / 32];
+
+__device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s) {
+    constexpr uint32_t kNw = kThreads / 32, kPer = kHllM / kNw / 32;   // registers per lane
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t i0 = warp * kPer * 32 + lane;
+    const uint32_t *R = smem32() + hll_idx;
+    uint32_t glob[kPer];
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) glob[j] = __ldcg(G + i0 + 32 * j);   // all in flight at once
     uint32_t m = 0xFFFFFFFFu;
-#pragma unroll 8
-    for (int i = 0; i < kHllM / 4 / 32; ++i) {
-        const uint4 v = R[i * 32 + lane];
-        m = min(m, min(min(v.x, v.y), min(v.z, v.w)));
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+        const uint32_t mine = R[i0 + 32 * j];
+        if (mine > glob[j]) atomicMax(G + i0 + 32 * j, mine);
+        m = min(m, max(mine, glob[j]));
     }
-    return __reduce_min_sync(0xFFFFFFFFu, m);
+    m = __reduce_min_sync(0xFFFFFFFFu, m);
+    if (lane == 0) s_slmin[s][warp] = m;
+    __syncwarp();
+    uint32_t L = lane < kNw ? *reinterpret_cast<volatile uint32_t *>(&s_slmin[s][lane]) : 0xFFFFFFFFu;
+    return __reduce_min_sync(0xFFFFFFFFu, L);
 }
 
 // #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback; out of line).
@@ -218,6 +235,18 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
     return b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
 }
 
+// FMT1T cell with >= 2 breakpoints: bs = (bucket + 1) | sub << sb from its record (out of
+// line; list records take the sub-bucket from the packed group's map).
+// (Arguments by value: a reference to the kernel parameters would turn every field read
+// in the callee into a generic-memory load.)
+__device__ __noinline__ uint32_t t1_special_bs(uint32_t lut_w, uint32_t s1, uint32_t sb, uint32_t map_addr,
+                                               uint32_t u) {
+    const uint32_t v = t1_bs(SmemTables{}, lut_w, s1, sb, u);
+    if (!(v & 0x80000000u)) return v;
+    const uint32_t b1 = v & ((1u << sb) - 1u);
+    return b1 | (map_addr != kNone ? *at(map_addr + 4 * b1) << sb : 0u);
+}
+
 // Bucket index | sub-bucket << 16 (bs) of slots [S0, S0 + NB) over one row quad.  One
 // LDS.32 per key and two ALU ops in a plain cell; keys in boundary cells (a few percent)
 // branch to their record; binary-search columns go through the out-of-line search.
@@ -250,7 +279,17 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             // plain cell: bucket | sub-bucket << 16 straight from the level-1 word
-            if (f == FMT32) {
+            if (f == FMT1T) {          // one in-cell threshold: compare, then lo or lo + 1 (+ cut)
+                const SlotParams &S = P.slot[s];
+                const uint32_t x = e[i][k];
+                const uint32_t zz = u[i][k] * S.t1_mul + S.t1_ones;
+                const uint32_t lo = x & S.t1_dmask;
+                const uint32_t hi = lo + 1u + (Sh::packs(P, s) ? (x >> S.t1_cutsh) & (S.bmask + 1u) : 0u);
+                bs[s][k] = zz >= x ? hi : lo;
+                if (x & S.t1_sp)
+                    bs[s][k] = t1_special_bs(S.lut_w, S.s1, S.sb,
+                                             Sh::packs(P, s) ? P.grp[S.prim_b].map_addr : kNone, u[i][k]);
+            } else if (f == FMT32) {
                 bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
                 if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
             } else {
@@ -272,14 +311,14 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
     }
 }
 
-__device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupParams &G, const uint32_t (&bsa)[4],
-                                             const uint32_t (&bsb)[4], uint32_t keep) {
+__device__ __forceinline__ void direct_pairs(const ProbeParams &P, uint32_t ma, uint32_t mb, const GroupParams &G,
+                                             const uint32_t (&bsa)[4], const uint32_t (&bsb)[4], uint32_t keep) {
     for (uint32_t d = G.dbeg; d < G.dend; ++d) {
         const DirectPair D = P.direct[d];
         uint32_t c = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t ba = bsa[k] & 0xFFFFu, bb = bsb[k] & 0xFFFFu;
+            const uint32_t ba = bsa[k] & ma, bb = bsb[k] & mb;
             const uint32_t ina = ((ba >= D.la) & (ba <= D.ha)) ^ D.nega;
             const uint32_t inb = ((bb >= D.lb) & (bb <= D.hb)) ^ D.negb;
             c += ((keep >> k) & 1u) & ina & inb;
@@ -291,13 +330,13 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, const GroupPa
 }
 
 // grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
-__device__ __forceinline__ void grid_add(const GroupParams &G, bool packed, const uint32_t (&bsa)[4],
-                                         const uint32_t (&bsb)[4], uint32_t keep) {
+__device__ __forceinline__ void grid_add(const SlotParams &A, const SlotParams &B, const GroupParams &G, bool packed,
+                                         const uint32_t (&bsa)[4], const uint32_t (&bsb)[4], uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t sub = packed ? bsb[k] >> 16 : *at(G.map_addr + 4 * (bsb[k] & 0xFFFFu));
-            atomicAdd(at(G.grid_addr + 4 * ((bsa[k] & 0xFFFFu) * G.nbs + sub)), 1u);
+            const uint32_t sub = packed ? bsb[k] >> B.sb : *at(G.map_addr + 4 * (bsb[k] & B.bmask));
+            atomicAdd(at(G.grid_addr + 4 * ((bsa[k] & A.bmask) * G.nbs + sub)), 1u);
         }
     }
 }
@@ -331,7 +370,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
         const uint32_t h = P.slot[s].hist_addr;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & 0xFFFFu)), 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & P.slot[s].bmask)), 1u);
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
@@ -340,28 +379,52 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
     for (int s = 0; s < NC; ++s) {
         if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
         uint32_t *R = sm + P.slot[s].hll_idx;
-        if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {   // (index, rank) precomputed per key
+        if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
+            // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
+            // value's contribution once: the first thread to apply it clears the rank in the
+            // cell (a benign race -- every writer stores the same word), so repeats of the
+            // value skip the register entirely.  One test covers the quad.
+            uint32_t any = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                red_max_if(((keep >> k) & 1u) && (ex[s][k] >> 27) > lim_l[s] && !(dbg & 1), R + ((ex[s][k] >> 15) & 0xFFFu),
-                           ex[s][k] >> 27);
+            for (int k = 0; k < 4; ++k) any |= ((keep >> k) & 1u) ? ex[s][k] : 0u;
+            if ((any >> 27) && !(dbg & 1)) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t x = ex[s][k], rank = x >> 27;
+                    if (((keep >> k) & 1u) && rank) {
+                        atomicMax(R + ((x >> 15) & 0xFFFu), rank);
+                        *at(4 * P.slot[s].lut_w + 4 * offset_of<Sh>(P, s, v[s][k])) = x & 0x07FFFFFFu;
+                    }
+                }
+            }
         } else if (Sh::is32(P, s)) {
-            const uint32_t lim = 0xFFFFFFFFu >> lim_l[s];
+            // w32 is even, so clearing bit 0 keeps "w32 <= lim" and puts the non-kept marker ~0 above it
+            const uint32_t lim = (0xFFFFFFFFu >> lim_l[s]) & 0xFFFFFFFEu;
             // clustered column, all four keys equal: one hash covers the quad
             const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
+            uint32_t w32[4], idx[4], wmin = 0xFFFFFFFFu;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (same && k > 0) break;
                 uint32_t h = static_cast<uint32_t>(v[s][k]);
                 h ^= __umulhi(h, 1u << 16);
                 h *= 0x85EBCA6BU;
                 h ^= __umulhi(h, 1u << 19);
                 h *= 0xC2B2AE35U;
                 h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
-                const uint32_t w32 = h * (1u << kHllP) + (1u << (kHllP - 1));
-                const uint32_t idx = __umulhi(h, 1u << kHllP);       // h >> (32 - p)
-                const bool kept_k = same ? keep != 0 : ((keep >> k) & 1u);
-                red_max_if(kept_k && w32 <= lim && !(dbg & 1), R + idx, __clz(w32) + 1);
+                w32[k] = h * (1u << kHllP) + (1u << (kHllP - 1));    // never ~0 (low bits 0x800)
+                idx[k] = __umulhi(h, 1u << kHllP);                   // h >> (32 - p)
+                const bool kept_k = (same && k > 0) ? false : (same ? keep != 0 : ((keep >> k) & 1u));
+                if (!kept_k) w32[k] = 0xFFFFFFFFu;
+                wmin = min(wmin, w32[k]);
+                if (same) break;
+            }
+            // one test for the quad: some key's rank beats the lower bound L
+            if (wmin <= lim && !(dbg & 1)) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    red_max_if(w32[k] <= lim, R + idx[k], __clz(w32[k]) + 1);
+                    if (same) break;
+                }
             }
         } else {
             const uint64_t lim = ~0ull >> lim_l[s];
@@ -380,8 +443,8 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
         for (int g = 0; g < Sh::NG; ++g) {
             const GroupParams &G = P.grp[g];
-            if (Sh::ggrid(g)) grid_add(G, Sh::gpacked(g), bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
-            if (Sh::gdirect(g)) direct_pairs(P, G, bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
+            if (Sh::ggrid(g)) grid_add(P.slot[Sh::ga(g)], P.slot[Sh::gb(g)], G, Sh::gpacked(g), bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
+            if (Sh::gdirect(g)) direct_pairs(P, P.slot[Sh::ga(g)].bmask, P.slot[Sh::gb(g)].bmask, G, bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
         }
     } else {
         for (uint32_t g = 0; g < P.ngroups; ++g) {
@@ -392,8 +455,8 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 ba[k] = pick<NC>(bs, G.a, k);
                 bb[k] = pick<NC>(bs, G.b, k);
             }
-            if (G.has_grid) grid_add(G, G.packed, ba, bb, keep);
-            if (G.dend > G.dbeg) direct_pairs(P, G, ba, bb, keep);
+            if (G.has_grid) grid_add(P.slot[G.a], P.slot[G.b], G, G.packed, ba, bb, keep);
+            if (G.dend > G.dbeg) direct_pairs(P, P.slot[G.a].bmask, P.slot[G.b].bmask, G, ba, bb, keep);
         }
     }
 }
@@ -432,6 +495,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) g_smem[i] = __ldg(P.image + i);
     for (uint32_t i = P.image_u4 + threadIdx.x; i < P.smem_bytes / 16; i += blockDim.x)
         g_smem[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < kMaxSlots * (kThreads / 32)) (&s_slmin[0][0])[threadIdx.x] = 0;
     __syncthreads();
 
     const uint64_t nunits = P.nrows / (4 * U);
@@ -448,11 +512,12 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         Unit<Sh> Xn;
         if (u + stride < nunits) load_unit<Sh>(P, u + stride, Xn);       // prefetch
         if (it == next_refresh) {
-            next_refresh = it + min(it, 128u);
+            next_refresh = it + min(it, 32u);
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
-                    if (Sh::active(P, s) && Sh::hll(P, s)) lim[s] = min(hll_min(P.slot[s].hll_idx), 32u);
+                    if (Sh::active(P, s) && Sh::hll(P, s))
+                        lim[s] = min(hll_bound(P.slot[s].hll_idx, P.g_hll_glob + (P.slot[s].hll_idx - P.hll_off / 4), s), 32u);
             }
         }
 #pragma unroll

@@ -9,7 +9,7 @@ import synth  # noqa: E402
 from paper_2512_19750_b200 import gace  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
-rows = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000
+rows = (int(sys.argv[2]) or None) if len(sys.argv) > 2 else 10_000   # 0: full size
 rate = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
 w = synth.get(name, rows)
 cols = [x.cuda() for x in w.table()]
