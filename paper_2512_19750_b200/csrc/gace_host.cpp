@@ -585,14 +585,14 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         const uint64_t span = span_of(S);
         const bool narrow = S.nb <= 512 && small_subs(S);
         S.sb = ceil_log2((uint64_t)S.nb + 1);
-        uint32_t t1s = 0;                    // FMT1T level-1 shift: ~64 cells per breakpoint, <= 16K cells
+        uint32_t t1s = 0;                    // FMT1T level-1 shift: ~128 cells per breakpoint, <= 32K cells
         {
             uint64_t target = 64;
-            while (target < 16384 && target < 64ull * S.T.size()) target <<= 1;
+            while (target < 32768 && target < 128ull * S.T.size()) target <<= 1;
             while (t1s < 31 && (span >> t1s) + 1 > target) ++t1s;
             t1s = std::max<uint32_t>(t1s, 1);
             const uint32_t mx = t1_max_s1(S, nsub_of(S));     // finer than the target when the fields force it
-            if (t1s > mx && mx >= 1 && (span >> mx) + 1 <= 16384) t1s = mx;
+            if (t1s > mx && mx >= 1 && (span >> mx) + 1 <= 32768) t1s = mx;
         }
         if (narrow && !S.clamp && S.dtype == GACE_I32 && span < 16384) {
             S.fmt = FMTEX;
@@ -1070,6 +1070,51 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
     o += "  __device__ static constexpr bool gpacked(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].packed ? "1" : "0"); }) + "; }\n";
     o += "  __device__ static constexpr bool ggrid(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].has_grid ? "1" : "0"); }) + "; }\n";
     o += "  __device__ static constexpr bool gdirect(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].dend > P.grp[g].dbeg ? "1" : "0"); }) + "; }\n";
+    // plan layout as immediates (the lookup-table contents stay in shared memory)
+    auto u32s = [](uint32_t v) { return std::to_string(v) + "u"; };
+    auto i64s = [](int64_t v) {
+        char b[40];
+        snprintf(b, sizeof b, "(int64_t)%lldLL", (long long)v);
+        if (v == INT64_MIN) snprintf(b, sizeof b, "(int64_t)(-9223372036854775807LL - 1)");
+        return std::string(b);
+    };
+    auto slot_u32 = [&](const char *name, auto f) {
+        o += std::string("  __device__ static constexpr uint32_t ") + name + "(const ProbeParams &, int s) { return " +
+             chain([&](int i) { return u32s(f(P.slot[i])); }, nc) + "; }\n";
+    };
+    auto slot_i64 = [&](const char *name, auto f) {
+        o += std::string("  __device__ static constexpr int64_t ") + name + "(const ProbeParams &, int s) { return " +
+             chain([&](int i) { return i64s(f(P.slot[i])); }, nc) + "; }\n";
+    };
+    auto grp_u32 = [&](const char *name, auto f) {
+        o += std::string("  __device__ static constexpr uint32_t ") + name + "(const ProbeParams &, int g) { return " +
+             gchain([&](uint32_t g) { return u32s(f(P.grp[g])); }) + "; }\n";
+    };
+    o += "  __device__ static constexpr bool sclamp(const ProbeParams &, int s) { return " +
+         chain([&](int i) {
+             const SlotParams &Q = P.slot[i];
+             const bool c = Q.dtype == 0 ? (Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX)
+                                         : (Q.clamp_lo != INT64_MIN || Q.clamp_hi != INT64_MAX);
+             return std::string(c ? "1" : "0");
+         }, nc) + "; }\n";
+    slot_i64("base", [](const SlotParams &Q) { return Q.base; });
+    slot_i64("clo", [](const SlotParams &Q) { return Q.clamp_lo; });
+    slot_i64("chi", [](const SlotParams &Q) { return Q.clamp_hi; });
+    slot_u32("s1", [](const SlotParams &Q) { return Q.s1; });
+    slot_u32("lutb", [](const SlotParams &Q) { return 4 * Q.lut_w; });
+    slot_u32("histb", [](const SlotParams &Q) { return Q.hist_addr; });
+    slot_u32("hllw", [](const SlotParams &Q) { return Q.hll_idx; });
+    slot_u32("sb", [](const SlotParams &Q) { return (uint32_t)Q.sb; });
+    slot_u32("bmask", [](const SlotParams &Q) { return Q.bmask; });
+    slot_u32("t1mul", [](const SlotParams &Q) { return Q.t1_mul; });
+    slot_u32("t1ones", [](const SlotParams &Q) { return Q.t1_ones; });
+    slot_u32("t1dmask", [](const SlotParams &Q) { return Q.t1_dmask; });
+    slot_u32("t1sp", [](const SlotParams &Q) { return Q.t1_sp; });
+    slot_u32("t1cutsh", [](const SlotParams &Q) { return Q.t1_cutsh; });
+    slot_u32("mapb", [&](const SlotParams &Q) { return Q.prim_b >= 0 ? P.grp[Q.prim_b].map_addr : kNone; });
+    grp_u32("ggridb", [](const GroupParams &G) { return G.grid_addr; });
+    grp_u32("gnbs", [](const GroupParams &G) { return G.nbs; });
+    grp_u32("gmapb", [](const GroupParams &G) { return G.map_addr; });
     o += "};\n}  // namespace gace\n";
     return o;
 }

@@ -84,18 +84,22 @@ __device__ __forceinline__ void lds128_if(bool pred, const uint4 *addr, uint4 &r
 __shared__ uint32_t s_slmin[kMaxSlots][kThreads / 32];
 
 __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s) {
-    constexpr uint32_t kNw = kThreads / 32, kPer = kHllM / kNw / 32;   // registers per lane
+    // this warp's registers: i = warp * 32 + lane + j * kThreads (the warps cover all 4096)
+    constexpr uint32_t kNw = kThreads / 32, kPer = (kHllM + kThreads - 1) / kThreads;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t i0 = warp * kPer * 32 + lane;
+    const uint32_t i0 = warp * 32 + lane;
     const uint32_t *R = smem32() + hll_idx;
     uint32_t glob[kPer];
 #pragma unroll
-    for (uint32_t j = 0; j < kPer; ++j) glob[j] = __ldcg(G + i0 + 32 * j);   // all in flight at once
+    for (uint32_t j = 0; j < kPer; ++j)                  // all loads in flight at once
+        glob[j] = i0 + j * kThreads < kHllM ? __ldcg(G + i0 + j * kThreads) : 0xFFFFFFFFu;
     uint32_t m = 0xFFFFFFFFu;
 #pragma unroll
     for (uint32_t j = 0; j < kPer; ++j) {
-        const uint32_t mine = R[i0 + 32 * j];
-        if (mine > glob[j]) atomicMax(G + i0 + 32 * j, mine);
+        const uint32_t i = i0 + j * kThreads;
+        if (i >= kHllM) break;
+        const uint32_t mine = R[i];
+        if (mine > glob[j]) atomicMax(G + i, mine);
         m = min(m, max(mine, glob[j]));
     }
     m = __reduce_min_sync(0xFFFFFFFFu, m);
@@ -159,6 +163,28 @@ struct RtShape {
     __device__ static constexpr int gb(int) { return 0; }
     __device__ static constexpr bool ggrid(int) { return false; }
     __device__ static constexpr bool gdirect(int) { return false; }
+    // plan layout (read from the parameters; JitShape bakes them in as immediates)
+    __device__ static bool sclamp(const ProbeParams &P, int) { return P.clamp; }
+    __device__ static int64_t base(const ProbeParams &P, int s) { return P.slot[s].base; }
+    __device__ static int64_t clo(const ProbeParams &P, int s) { return P.slot[s].clamp_lo; }
+    __device__ static int64_t chi(const ProbeParams &P, int s) { return P.slot[s].clamp_hi; }
+    __device__ static uint32_t s1(const ProbeParams &P, int s) { return P.slot[s].s1; }
+    __device__ static uint32_t lutb(const ProbeParams &P, int s) { return 4 * P.slot[s].lut_w; }
+    __device__ static uint32_t histb(const ProbeParams &P, int s) { return P.slot[s].hist_addr; }
+    __device__ static uint32_t hllw(const ProbeParams &P, int s) { return P.slot[s].hll_idx; }
+    __device__ static uint32_t sb(const ProbeParams &P, int s) { return P.slot[s].sb; }
+    __device__ static uint32_t bmask(const ProbeParams &P, int s) { return P.slot[s].bmask; }
+    __device__ static uint32_t t1mul(const ProbeParams &P, int s) { return P.slot[s].t1_mul; }
+    __device__ static uint32_t t1ones(const ProbeParams &P, int s) { return P.slot[s].t1_ones; }
+    __device__ static uint32_t t1dmask(const ProbeParams &P, int s) { return P.slot[s].t1_dmask; }
+    __device__ static uint32_t t1sp(const ProbeParams &P, int s) { return P.slot[s].t1_sp; }
+    __device__ static uint32_t t1cutsh(const ProbeParams &P, int s) { return P.slot[s].t1_cutsh; }
+    __device__ static uint32_t mapb(const ProbeParams &P, int s) {      // packed group's map, or kNone
+        return P.slot[s].prim_b >= 0 ? P.grp[P.slot[s].prim_b].map_addr : kNone;
+    }
+    __device__ static uint32_t ggridb(const ProbeParams &P, int g) { return P.grp[g].grid_addr; }
+    __device__ static uint32_t gnbs(const ProbeParams &P, int g) { return P.grp[g].nbs; }
+    __device__ static uint32_t gmapb(const ProbeParams &P, int g) { return P.grp[g].map_addr; }
 };
 
 // ------------------------------------------------------------------ row units
@@ -207,15 +233,15 @@ __device__ __forceinline__ void decode(const ProbeParams &P, int s, const int4 (
 // Offset u = key - base of a lookup-table column (with the optional clamp).
 template <class Sh>
 __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<Sh> xk) {
-    const SlotParams &S = P.slot[s];
     if (Sh::is32(P, s)) {
         int32_t y = static_cast<int32_t>(xk);
-        if (Sh::clamp(P)) y = min(max(y, static_cast<int32_t>(S.clamp_lo)), static_cast<int32_t>(S.clamp_hi));
-        return static_cast<uint32_t>(y) - static_cast<uint32_t>(S.base);
+        if (Sh::sclamp(P, s))
+            y = min(max(y, static_cast<int32_t>(Sh::clo(P, s))), static_cast<int32_t>(Sh::chi(P, s)));
+        return static_cast<uint32_t>(y) - static_cast<uint32_t>(Sh::base(P, s));
     }
     int64_t x = xk;
-    if (Sh::clamp(P)) x = min(max(x, S.clamp_lo), S.clamp_hi);
-    return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(S.base));
+    if (Sh::sclamp(P, s)) x = min(max(x, Sh::clo(P, s)), Sh::chi(P, s));
+    return static_cast<uint32_t>(static_cast<uint64_t>(x) - static_cast<uint64_t>(Sh::base(P, s)));
 }
 
 // Bucket | sub-bucket << 16 of a key in a boundary cell: its 16-byte record (<= 3
@@ -231,8 +257,8 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
                   (c3 & (r.x >> (kIncShift + 2)))) << 16;
         return b;
     }
-    const uint32_t b = lut_bucket(Sh::fmt(P, s), P.slot[s].lut_w, P.slot[s].s1, u);
-    return b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
+    const uint32_t b = lut_bucket(Sh::fmt(P, s), Sh::lutb(P, s) / 4, Sh::s1(P, s), u);
+    return b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << 16 : 0u);
 }
 
 // FMT1T cell with >= 2 breakpoints: bs = (bucket + 1) | sub << sb from its record (out of
@@ -258,13 +284,13 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
         const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
-        const uint32_t base = 4 * P.slot[s].lut_w;
+        const uint32_t base = Sh::lutb(P, s);
         const int f = Sh::fmt(P, s);
         const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            const uint32_t cell = f == FMTEX ? u[i][k] : u[i][k] >> P.slot[s].s1;
+            const uint32_t cell = f == FMTEX ? u[i][k] : u[i][k] >> Sh::s1(P, s);
             if (!lut || (k > 0 && same)) e[i][k] = 0u;
             else if (f == FMT16) e[i][k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
             else e[i][k] = *at(base + 4 * cell);
@@ -280,15 +306,14 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
         for (int k = 0; k < 4; ++k) {
             // plain cell: bucket | sub-bucket << 16 straight from the level-1 word
             if (f == FMT1T) {          // one in-cell threshold: compare, then lo or lo + 1 (+ cut)
-                const SlotParams &S = P.slot[s];
                 const uint32_t x = e[i][k];
-                const uint32_t zz = u[i][k] * S.t1_mul + S.t1_ones;
-                const uint32_t lo = x & S.t1_dmask;
-                const uint32_t hi = lo + 1u + (Sh::packs(P, s) ? (x >> S.t1_cutsh) & (S.bmask + 1u) : 0u);
+                const uint32_t zz = u[i][k] * Sh::t1mul(P, s) + Sh::t1ones(P, s);
+                const uint32_t lo = x & Sh::t1dmask(P, s);
+                const uint32_t hi = lo + 1u + (Sh::packs(P, s) ? (x >> Sh::t1cutsh(P, s)) & (Sh::bmask(P, s) + 1u) : 0u);
                 bs[s][k] = zz >= x ? hi : lo;
-                if (x & S.t1_sp)
-                    bs[s][k] = t1_special_bs(S.lut_w, S.s1, S.sb,
-                                             Sh::packs(P, s) ? P.grp[S.prim_b].map_addr : kNone, u[i][k]);
+                if (x & Sh::t1sp(P, s))
+                    bs[s][k] = t1_special_bs(Sh::lutb(P, s) / 4, Sh::s1(P, s), Sh::sb(P, s),
+                                             Sh::packs(P, s) ? Sh::mapb(P, s) : kNone, u[i][k]);
             } else if (f == FMT32) {
                 bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
                 if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
@@ -305,7 +330,7 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t b = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
-                bs[s][k] = b | (Sh::packs(P, s) ? *at(P.grp[P.slot[s].prim_b].map_addr + 4 * b) << 16 : 0u);
+                bs[s][k] = b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << 16 : 0u);
             }
         }
     }
@@ -330,13 +355,14 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, uint32_t ma, 
 }
 
 // grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
-__device__ __forceinline__ void grid_add(const SlotParams &A, const SlotParams &B, const GroupParams &G, bool packed,
-                                         const uint32_t (&bsa)[4], const uint32_t (&bsb)[4], uint32_t keep) {
+__device__ __forceinline__ void grid_add(uint32_t amask, uint32_t bsh, uint32_t bmask, uint32_t grid, uint32_t nbs,
+                                         uint32_t map, bool packed, const uint32_t (&bsa)[4], const uint32_t (&bsb)[4],
+                                         uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t sub = packed ? bsb[k] >> B.sb : *at(G.map_addr + 4 * (bsb[k] & B.bmask));
-            atomicAdd(at(G.grid_addr + 4 * ((bsa[k] & A.bmask) * G.nbs + sub)), 1u);
+            const uint32_t sub = packed ? bsb[k] >> bsh : *at(map + 4 * (bsb[k] & bmask));
+            atomicAdd(at(grid + 4 * ((bsa[k] & amask) * nbs + sub)), 1u);
         }
     }
 }
@@ -367,10 +393,10 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
         if (!Sh::active(P, s) || !Sh::ownh(P, s) || (dbg & 2)) continue;
-        const uint32_t h = P.slot[s].hist_addr;
+        const uint32_t h = Sh::histb(P, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & P.slot[s].bmask)), 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & Sh::bmask(P, s))), 1u);
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
@@ -378,7 +404,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
     for (int s = 0; s < NC; ++s) {
         if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
-        uint32_t *R = sm + P.slot[s].hll_idx;
+        uint32_t *R = sm + Sh::hllw(P, s);
         if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
             // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
             // value's contribution once: the first thread to apply it clears the rank in the
@@ -393,7 +419,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                     const uint32_t x = ex[s][k], rank = x >> 27;
                     if (((keep >> k) & 1u) && rank) {
                         atomicMax(R + ((x >> 15) & 0xFFFu), rank);
-                        *at(4 * P.slot[s].lut_w + 4 * offset_of<Sh>(P, s, v[s][k])) = x & 0x07FFFFFFu;
+                        *at(Sh::lutb(P, s) + 4 * offset_of<Sh>(P, s, v[s][k])) = x & 0x07FFFFFFu;
                     }
                 }
             }
@@ -443,8 +469,11 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
 #pragma unroll
         for (int g = 0; g < Sh::NG; ++g) {
             const GroupParams &G = P.grp[g];
-            if (Sh::ggrid(g)) grid_add(P.slot[Sh::ga(g)], P.slot[Sh::gb(g)], G, Sh::gpacked(g), bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
-            if (Sh::gdirect(g)) direct_pairs(P, P.slot[Sh::ga(g)].bmask, P.slot[Sh::gb(g)].bmask, G, bs[Sh::ga(g)], bs[Sh::gb(g)], keep);
+            const int a = Sh::ga(g), b = Sh::gb(g);
+            if (Sh::ggrid(g))
+                grid_add(Sh::bmask(P, a), Sh::sb(P, b), Sh::bmask(P, b), Sh::ggridb(P, g), Sh::gnbs(P, g),
+                         Sh::gmapb(P, g), Sh::gpacked(g), bs[a], bs[b], keep);
+            if (Sh::gdirect(g)) direct_pairs(P, Sh::bmask(P, a), Sh::bmask(P, b), G, bs[a], bs[b], keep);
         }
     } else {
         for (uint32_t g = 0; g < P.ngroups; ++g) {
@@ -455,7 +484,9 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 ba[k] = pick<NC>(bs, G.a, k);
                 bb[k] = pick<NC>(bs, G.b, k);
             }
-            if (G.has_grid) grid_add(P.slot[G.a], P.slot[G.b], G, G.packed, ba, bb, keep);
+            if (G.has_grid)
+                grid_add(P.slot[G.a].bmask, P.slot[G.b].sb, P.slot[G.b].bmask, G.grid_addr, G.nbs, G.map_addr, G.packed,
+                         ba, bb, keep);
             if (G.dend > G.dbeg) direct_pairs(P, P.slot[G.a].bmask, P.slot[G.b].bmask, G, ba, bb, keep);
         }
     }
@@ -517,7 +548,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
                     if (Sh::active(P, s) && Sh::hll(P, s))
-                        lim[s] = min(hll_bound(P.slot[s].hll_idx, P.g_hll_glob + (P.slot[s].hll_idx - P.hll_off / 4), s), 32u);
+                        lim[s] = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 32u);
             }
         }
 #pragma unroll
