@@ -835,14 +835,20 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.s1 = S.s1;
         Q.lut_w = S.lut_idx;
         Q.fmt = S.fmt;
-        Q.sb = (uint8_t)(S.fmt == FMT1T ? S.sb : 16);
+        // bs layout per format: the plain level-1 word is used as bs directly
+        const bool lutm = S.has_preds && S.mode == MODE_LUT;
+        Q.sb = (uint8_t)(!lutm ? 16 : S.fmt == FMT1T ? S.sb : S.fmt == FMT32 ? kSubShift : 9);
         Q.bmask = (1u << Q.sb) - 1u;
+        Q.submask = !lutm || S.fmt == FMT1T ? 0xFFFFFFFFu : S.fmt == FMT32 ? kSubMask : 63u;
+        Q.sub_mul = 1u << (32 - Q.sb);
+        Q.cell_mul = S.s1 >= 1 ? 1u << (32 - S.s1) : 0u;
         if (S.fmt == FMT1T) {
             Q.t1_mul = 1u << (32 - S.s1);
             Q.t1_ones = Q.t1_mul - 1u;
             Q.t1_dmask = t1_dmask(S.s1);
             Q.t1_sp = t1_special(S.s1);
             Q.t1_cutsh = 30 - S.s1 - S.sb;
+            Q.t1_cutmul = Q.t1_cutsh ? 1u << (32 - Q.t1_cutsh) : 0u;
         }
         if (S.fmt == FMT1T && S.hist_w != kNone) Q.hist_addr -= 4;     // 1-based buckets
         if (S.dtype == GACE_I32) { Q.clamp_lo = INT32_MIN; Q.clamp_hi = INT32_MAX; }
@@ -875,6 +881,9 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (!G.direct && pl.slots[G.b].fmt == FMT1T) R.map_addr -= 4;          // 1-based B buckets
     }
     P.ngroups = (uint32_t)pl.groups.size();
+    P.c1 = 1;
+    P.c4 = 4;
+    P.c_hll = 1u << kHllP;
     P.clamp = pl.clamp ? 1u : 0u;      // (the specialised kernel bakes this in: set it here)
     P.ndirect = (uint32_t)pl.direct.size();
     P.image_u4 = image_words / 4;
@@ -1111,6 +1120,10 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
     slot_u32("t1dmask", [](const SlotParams &Q) { return Q.t1_dmask; });
     slot_u32("t1sp", [](const SlotParams &Q) { return Q.t1_sp; });
     slot_u32("t1cutsh", [](const SlotParams &Q) { return Q.t1_cutsh; });
+    slot_u32("t1cutmul", [](const SlotParams &Q) { return Q.t1_cutmul; });
+    slot_u32("submask", [](const SlotParams &Q) { return Q.submask; });
+    slot_u32("submul", [](const SlotParams &Q) { return Q.sub_mul; });
+    slot_u32("cellmul", [](const SlotParams &Q) { return Q.cell_mul; });
     slot_u32("mapb", [&](const SlotParams &Q) { return Q.prim_b >= 0 ? P.grp[Q.prim_b].map_addr : kNone; });
     grp_u32("ggridb", [](const GroupParams &G) { return G.grid_addr; });
     grp_u32("gnbs", [](const GroupParams &G) { return G.nbs; });

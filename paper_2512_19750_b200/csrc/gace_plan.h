@@ -183,12 +183,16 @@ struct SlotParams {
     uint8_t sb;             // sub-bucket shift inside bs (16, or the FMT1T bucket field width)
     uint8_t pad[2];
     uint32_t bmask;         // (1 << sb) - 1: bucket field of bs
+    uint32_t submask;       // sub-bucket field of bs >> sb (FMT16/FMTEX: 63, FMT32: 127)
+    uint32_t sub_mul;       // 2^(32 - sb): bs >> sb as a high multiply (FMA pipe)
+    uint32_t cell_mul;      // 2^(32 - s1) (s1 >= 1): level-1 cell u >> s1 as a high multiply
     // FMT1T decode constants (gace_plan.h LutFmt)
     uint32_t t1_mul;        // 2^(32 - s1)
     uint32_t t1_ones;       // 2^(32 - s1) - 1
     uint32_t t1_dmask;      // data bits
     uint32_t t1_sp;         // special flag
     uint32_t t1_cutsh;      // cut flag >> t1_cutsh lands on bit sb
+    uint32_t t1_cutmul;     // 2^(32 - t1_cutsh), or 0 when t1_cutsh = 0
 };
 
 struct GroupParams {
@@ -235,6 +239,8 @@ struct ProbeParams {
     uint32_t sample_all;                   // rate == 1
     uint32_t part_merge;                   // 1: max-merge into existing per-CTA partials (later chunk launches)
     uint32_t clamp;                        // clamp keys into each slot's [clamp_lo, clamp_hi]
+    uint32_t c1, c4, c_hll;                // 1, 4, 2^p: multipliers the compiler cannot see, so that
+                                           // u * 4 + base etc. stay IMADs (FMA pipe) instead of LEA/SHF
     uint32_t dbg;                          // ablation bits (env GACE_ABLATE; 0 in production):
                                            // 1 no HLL raise, 2 no histogram adds, 4 no grid adds, 8 no HLL
 };

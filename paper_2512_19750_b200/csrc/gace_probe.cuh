@@ -81,7 +81,11 @@ __device__ __forceinline__ void lds128_if(bool pred, const uint4 *addr, uint4 &r
 // higher, and records the slice minimum in s_slmin; L = min over the slice minima.  The
 // merged registers only grow and every value in them came from some CTA's own rows, so a
 // key whose rank is <= L cannot change the final max: skipping it is exact.
-__shared__ uint32_t s_slmin[kMaxSlots][kThreads / 32];
+__shared__ uint8_t s_slmin[kMaxSlots][kThreads / 32];   // register values are < 64
+// Per-warp skip limit ~0 >> L (bit 0 cleared) of each HLL slot; row kThreads/32 stays ~1
+// (no skipping) for the tail rows.  Kept in shared memory (a broadcast load per use)
+// rather than in registers, which the hot loop needs for its keys.
+__shared__ uint32_t s_wlim[kThreads / 32 + 1][kMaxSlots];
 
 __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s) {
     // this warp's registers: i = warp * 32 + lane + j * kThreads (the warps cover all 4096)
@@ -103,9 +107,9 @@ __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s)
         m = min(m, max(mine, glob[j]));
     }
     m = __reduce_min_sync(0xFFFFFFFFu, m);
-    if (lane == 0) s_slmin[s][warp] = m;
+    if (lane == 0) s_slmin[s][warp] = (uint8_t)min(m, 255u);
     __syncwarp();
-    uint32_t L = lane < kNw ? *reinterpret_cast<volatile uint32_t *>(&s_slmin[s][lane]) : 0xFFFFFFFFu;
+    uint32_t L = lane < kNw ? *reinterpret_cast<volatile uint8_t *>(&s_slmin[s][lane]) : 0xFFFFFFFFu;
     return __reduce_min_sync(0xFFFFFFFFu, L);
 }
 
@@ -179,6 +183,10 @@ struct RtShape {
     __device__ static uint32_t t1dmask(const ProbeParams &P, int s) { return P.slot[s].t1_dmask; }
     __device__ static uint32_t t1sp(const ProbeParams &P, int s) { return P.slot[s].t1_sp; }
     __device__ static uint32_t t1cutsh(const ProbeParams &P, int s) { return P.slot[s].t1_cutsh; }
+    __device__ static uint32_t t1cutmul(const ProbeParams &P, int s) { return P.slot[s].t1_cutmul; }
+    __device__ static uint32_t submask(const ProbeParams &P, int s) { return P.slot[s].submask; }
+    __device__ static uint32_t submul(const ProbeParams &P, int s) { return P.slot[s].sub_mul; }
+    __device__ static uint32_t cellmul(const ProbeParams &P, int s) { return P.slot[s].cell_mul; }
     __device__ static uint32_t mapb(const ProbeParams &P, int s) {      // packed group's map, or kNone
         return P.slot[s].prim_b >= 0 ? P.grp[P.slot[s].prim_b].map_addr : kNone;
     }
@@ -254,11 +262,11 @@ __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s,
         uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
         if (Sh::packs(P, s))
             b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) + (c2 & (r.x >> (kIncShift + 1))) +
-                  (c3 & (r.x >> (kIncShift + 2)))) << 16;
+                  (c3 & (r.x >> (kIncShift + 2)))) << Sh::sb(P, s);
         return b;
     }
     const uint32_t b = lut_bucket(Sh::fmt(P, s), Sh::lutb(P, s) / 4, Sh::s1(P, s), u);
-    return b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << 16 : 0u);
+    return b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << Sh::sb(P, s) : 0u);
 }
 
 // FMT1T cell with >= 2 breakpoints: bs = (bucket + 1) | sub << sb from its record (out of
@@ -273,9 +281,12 @@ __device__ __noinline__ uint32_t t1_special_bs(uint32_t lut_w, uint32_t s1, uint
     return b1 | (map_addr != kNone ? *at(map_addr + 4 * b1) << sb : 0u);
 }
 
-// Bucket index | sub-bucket << 16 (bs) of slots [S0, S0 + NB) over one row quad.  One
-// LDS.32 per key and two ALU ops in a plain cell; keys in boundary cells (a few percent)
-// branch to their record; binary-search columns go through the out-of-line search.
+// bs = bucket | sub-bucket << sb of slots [S0, S0 + NB) over one row quad (the layout of the
+// slot's plain level-1 word, so a plain cell is used as is; FMT1T buckets are 1-based).
+// One LDS per key; cells with breakpoints resolve inline (FMT1T: one threshold) or, for the
+// rare special cells, through one test per column quad and an out-of-line record walk.
+// Multiplies by 2^k use opaque multipliers (P.c4, P.slot[].t1_mul) or high multiplies so
+// that they run on the FMA pipe, which the rest of the loop leaves half idle.
 template <class Sh, int S0, int NB>
 __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
                                         uint32_t (&bs)[Sh::NC][4], uint32_t (&ex)[Sh::NC][4]) {
@@ -290,10 +301,15 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            const uint32_t cell = f == FMTEX ? u[i][k] : u[i][k] >> Sh::s1(P, s);
-            if (!lut || (k > 0 && same)) e[i][k] = 0u;
-            else if (f == FMT16) e[i][k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
-            else e[i][k] = *at(base + 4 * cell);
+            if (!lut || (k > 0 && same)) {
+                e[i][k] = 0u;
+            } else if (f == FMT16) {
+                const uint32_t cell = u[i][k] >> Sh::s1(P, s);
+                e[i][k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
+            } else {
+                const uint32_t cell = f == FMTEX ? u[i][k] : (Sh::s1(P, s) ? __umulhi(u[i][k], Sh::cellmul(P, s)) : u[i][k]);
+                e[i][k] = *at(cell * P.c4 + base);
+            }
             if (k > 0 && same) e[i][k] = e[i][0];
         }
         ex[s][0] = e[i][0]; ex[s][1] = e[i][1]; ex[s][2] = e[i][2]; ex[s][3] = e[i][3];
@@ -302,25 +318,51 @@ __device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v
     for (int i = 0; i < NB; ++i) {
         const int s = S0 + i;
         const int f = Sh::fmt(P, s);
+        if (f == FMT1T) {              // one in-cell threshold: c ? lo + inc : lo, inc = 1 or 1 + 2^sb
+            const uint32_t sp = Sh::t1sp(P, s);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            // plain cell: bucket | sub-bucket << 16 straight from the level-1 word
-            if (f == FMT1T) {          // one in-cell threshold: compare, then lo or lo + 1 (+ cut)
+            for (int k = 0; k < 4; ++k) {
                 const uint32_t x = e[i][k];
-                const uint32_t zz = u[i][k] * Sh::t1mul(P, s) + Sh::t1ones(P, s);
+                const uint32_t zz = u[i][k] * P.slot[s].t1_mul + Sh::t1ones(P, s);
                 const uint32_t lo = x & Sh::t1dmask(P, s);
-                const uint32_t hi = lo + 1u + (Sh::packs(P, s) ? (x >> Sh::t1cutsh(P, s)) & (Sh::bmask(P, s) + 1u) : 0u);
-                bs[s][k] = zz >= x ? hi : lo;
-                if (x & Sh::t1sp(P, s))
-                    bs[s][k] = t1_special_bs(Sh::lutb(P, s) / 4, Sh::s1(P, s), Sh::sb(P, s),
-                                             Sh::packs(P, s) ? Sh::mapb(P, s) : kNone, u[i][k]);
-            } else if (f == FMT32) {
-                bs[s][k] = (e[i][k] & kIdxMask) | (Sh::packs(P, s) ? (e[i][k] << (16 - kSubShift)) & (kSubMask << 16) : 0u);
-                if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
-            } else {
-                bs[s][k] = (e[i][k] & 0x1FFu) | (Sh::packs(P, s) ? (e[i][k] << 7) & (63u << 16) : 0u);
-                if (f == FMT16 && (e[i][k] & 0x8000u)) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask16, u[i][k]);
+                uint32_t inc = 1u;
+                if (Sh::packs(P, s))
+                    inc = ((Sh::t1cutsh(P, s) ? __umulhi(x, Sh::t1cutmul(P, s)) : x) & (Sh::bmask(P, s) + 1u)) | 1u;
+                bs[s][k] = zz >= x ? lo * P.c1 + inc : lo;
             }
+            if ((e[i][0] | e[i][1] | e[i][2] | e[i][3]) & sp) {      // >= 2 breakpoints in some cell
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!(e[i][k] & sp)) continue;
+                    const uint4 r = g_smem[e[i][k] & Sh::t1dmask(P, s)];
+                    if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
+                        const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
+                        uint32_t b = (r.x & kIdxMask) + 1u + c1 + c2 + c3;
+                        if (Sh::packs(P, s))
+                            b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) +
+                                  (c2 & (r.x >> (kIncShift + 1))) + (c3 & (r.x >> (kIncShift + 2)))) << Sh::sb(P, s);
+                        bs[s][k] = b;
+                    } else {                   // nested block or list: out-of-line walk
+                        bs[s][k] = t1_special_bs(Sh::lutb(P, s) / 4, Sh::s1(P, s), Sh::sb(P, s),
+                                                 Sh::packs(P, s) ? Sh::mapb(P, s) : kNone, u[i][k]);
+                    }
+                }
+            }
+        } else if (f == FMT32) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bs[s][k] = e[i][k];
+                if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
+            }
+        } else if (f == FMT16) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bs[s][k] = e[i][k];
+                if (e[i][k] & 0x8000u) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask16, u[i][k]);
+            }
+        } else {                       // FMTEX: exact cells, never a boundary
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bs[s][k] = e[i][k];
         }
     }
 #pragma unroll
@@ -355,14 +397,14 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, uint32_t ma, 
 }
 
 // grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
-__device__ __forceinline__ void grid_add(uint32_t amask, uint32_t bsh, uint32_t bmask, uint32_t grid, uint32_t nbs,
-                                         uint32_t map, bool packed, const uint32_t (&bsa)[4], const uint32_t (&bsb)[4],
-                                         uint32_t keep) {
+__device__ __forceinline__ void grid_add(uint32_t c4, uint32_t amask, uint32_t submul, uint32_t submask, uint32_t bmask,
+                                         uint32_t grid, uint32_t nbs, uint32_t map, bool packed,
+                                         const uint32_t (&bsa)[4], const uint32_t (&bsb)[4], uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t sub = packed ? bsb[k] >> bsh : *at(map + 4 * (bsb[k] & bmask));
-            atomicAdd(at(grid + 4 * ((bsa[k] & amask) * nbs + sub)), 1u);
+            const uint32_t sub = packed ? __umulhi(bsb[k], submul) & submask : *at(map + 4 * (bsb[k] & bmask));
+            atomicAdd(at(((bsa[k] & amask) * nbs + sub) * c4 + grid), 1u);
         }
     }
 }
@@ -378,7 +420,7 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NC][4], uint32_t s,
 // Everything one row quad contributes.  keep: one bit per row.
 template <class Sh>
 __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
-                                          uint32_t keep, const uint32_t (&lim_l)[Sh::NC]) {
+                                          uint32_t keep, const uint32_t *wlim) {
     constexpr int NC = Sh::NC;
     uint32_t *sm = smem32();
     const uint32_t dbg = P.dbg;
@@ -425,7 +467,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             }
         } else if (Sh::is32(P, s)) {
             // w32 is even, so clearing bit 0 keeps "w32 <= lim" and puts the non-kept marker ~0 above it
-            const uint32_t lim = (0xFFFFFFFFu >> lim_l[s]) & 0xFFFFFFFEu;
+            const uint32_t lim = wlim[s];
             // clustered column, all four keys equal: one hash covers the quad
             const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
             uint32_t w32[4], idx[4], wmin = 0xFFFFFFFFu;
@@ -437,7 +479,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 h ^= __umulhi(h, 1u << 19);
                 h *= 0xC2B2AE35U;
                 h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
-                w32[k] = h * (1u << kHllP) + (1u << (kHllP - 1));    // never ~0 (low bits 0x800)
+                w32[k] = h * P.c_hll + (1u << (kHllP - 1));          // never ~0 (low bits 0x800)
                 idx[k] = __umulhi(h, 1u << kHllP);                   // h >> (32 - p)
                 const bool kept_k = (same && k > 0) ? false : (same ? keep != 0 : ((keep >> k) & 1u));
                 if (!kept_k) w32[k] = 0xFFFFFFFFu;
@@ -453,7 +495,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 }
             }
         } else {
-            const uint64_t lim = ~0ull >> lim_l[s];
+            const uint64_t lim = ~0ull >> (32 - __popc(wlim[s] | 1u));     // L from the 32-bit limit
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
@@ -471,8 +513,8 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             const GroupParams &G = P.grp[g];
             const int a = Sh::ga(g), b = Sh::gb(g);
             if (Sh::ggrid(g))
-                grid_add(Sh::bmask(P, a), Sh::sb(P, b), Sh::bmask(P, b), Sh::ggridb(P, g), Sh::gnbs(P, g),
-                         Sh::gmapb(P, g), Sh::gpacked(g), bs[a], bs[b], keep);
+                grid_add(P.c4, Sh::bmask(P, a), Sh::submul(P, b), Sh::submask(P, b), Sh::bmask(P, b), Sh::ggridb(P, g),
+                         Sh::gnbs(P, g), Sh::gmapb(P, g), Sh::gpacked(g), bs[a], bs[b], keep);
             if (Sh::gdirect(g)) direct_pairs(P, Sh::bmask(P, a), Sh::bmask(P, b), G, bs[a], bs[b], keep);
         }
     } else {
@@ -485,8 +527,8 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                 bb[k] = pick<NC>(bs, G.b, k);
             }
             if (G.has_grid)
-                grid_add(P.slot[G.a].bmask, P.slot[G.b].sb, P.slot[G.b].bmask, G.grid_addr, G.nbs, G.map_addr, G.packed,
-                         ba, bb, keep);
+                grid_add(P.c4, P.slot[G.a].bmask, P.slot[G.b].sub_mul, P.slot[G.b].submask, P.slot[G.b].bmask,
+                         G.grid_addr, G.nbs, G.map_addr, G.packed, ba, bb, keep);
             if (G.dend > G.dbeg) direct_pairs(P, P.slot[G.a].bmask, P.slot[G.b].bmask, G, ba, bb, keep);
         }
     }
@@ -511,10 +553,7 @@ __device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
             rj[s][Sh::I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
         }
     }
-    uint32_t zero[Sh::NC];
-#pragma unroll
-    for (int s = 0; s < Sh::NC; ++s) zero[s] = 0;
-    quad_work<Sh>(P, rj, 1u, zero);
+    quad_work<Sh>(P, rj, 1u, s_wlim[kThreads / 32]);
     return 1;
 }
 
@@ -527,14 +566,13 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     for (uint32_t i = P.image_u4 + threadIdx.x; i < P.smem_bytes / 16; i += blockDim.x)
         g_smem[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x < kMaxSlots * (kThreads / 32)) (&s_slmin[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxSlots * (kThreads / 32 + 1)) (&s_wlim[0][0])[threadIdx.x] = 0xFFFFFFFEu;
     __syncthreads();
 
     const uint64_t nunits = P.nrows / (4 * U);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t kept = 0;
-    uint32_t lim[NC];            // per-column lower bound L of the CTA's HLL registers
-#pragma unroll
-    for (int s = 0; s < NC; ++s) lim[s] = 0;
+    uint32_t *wlim = s_wlim[threadIdx.x >> 5];
     uint32_t it = 0, next_refresh = 4;
     uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     Unit<Sh> X;
@@ -547,8 +585,11 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
-                    if (Sh::active(P, s) && Sh::hll(P, s))
-                        lim[s] = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 32u);
+                    if (Sh::active(P, s) && Sh::hll(P, s)) {
+                        const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 31u);
+                        if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
+                    }
+                __syncwarp();
             }
         }
 #pragma unroll
@@ -568,7 +609,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 rj[s][0] = X.r[s][j][0];
                 if (Sh::I64) rj[s][Sh::I64 ? 1 : 0] = X.r[s][j][Sh::I64 ? 1 : 0];
             }
-            quad_work<Sh>(P, rj, keep, lim);
+            quad_work<Sh>(P, rj, keep, wlim);
         }
         X = Xn;
     }
