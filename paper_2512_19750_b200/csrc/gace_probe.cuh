@@ -281,100 +281,98 @@ __device__ __noinline__ uint32_t t1_special_bs(uint32_t lut_w, uint32_t s1, uint
     return b1 | (map_addr != kNone ? *at(map_addr + 4 * b1) << sb : 0u);
 }
 
-// bs = bucket | sub-bucket << sb of slots [S0, S0 + NB) over one row quad (the layout of the
-// slot's plain level-1 word, so a plain cell is used as is; FMT1T buckets are 1-based).
-// One LDS per key; cells with breakpoints resolve inline (FMT1T: one threshold) or, for the
-// rare special cells, through one test per column quad and an out-of-line record walk.
-// Multiplies by 2^k use opaque multipliers (P.c4, P.slot[].t1_mul) or high multiplies so
-// that they run on the FMA pipe, which the rest of the loop leaves half idle.
-template <class Sh, int S0, int NB>
-__device__ __forceinline__ void buckets(const ProbeParams &P, const KeyT<Sh> (&v)[Sh::NC][4],
-                                        uint32_t (&bs)[Sh::NC][4], uint32_t (&ex)[Sh::NC][4]) {
-    uint32_t u[NB][4], e[NB][4];
+// bs = bucket | sub-bucket << sb of slot s over one row quad (the layout of the slot's plain
+// level-1 word, so a plain cell is used as is; FMT1T buckets are 1-based).  One LDS per key
+// (one per quad for a clustered column whose four keys are equal); cells with breakpoints
+// resolve inline (FMT1T: one threshold) or, for the rare special cells, through one test
+// per column quad and a record walk.  Multiplies by 2^k use opaque multipliers (P.c4,
+// P.slot[].t1_mul) or high multiplies so that they run on the FMA pipe.
+template <class Sh>
+__device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, bool same, const KeyT<Sh> (&v)[4],
+                                           uint32_t (&bs)[4], uint32_t (&e)[4]) {
+    const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
+    const uint32_t base = Sh::lutb(P, s);
+    const int f = Sh::fmt(P, s);
+    const int nk = same ? 1 : 4;
+    uint32_t u[4];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const int s = S0 + i;
-        const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
-        const uint32_t base = Sh::lutb(P, s);
-        const int f = Sh::fmt(P, s);
-        const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
+    for (int k = 0; k < 4; ++k) {
+        u[k] = 0u;
+        e[k] = 0u;
+        if (k >= nk || !lut) continue;
+        u[k] = offset_of<Sh>(P, s, v[k]);
+        if (f == FMT16) {
+            const uint32_t cell = u[k] >> Sh::s1(P, s);
+            e[k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
+        } else {
+            const uint32_t cell = f == FMTEX ? u[k] : (Sh::s1(P, s) ? __umulhi(u[k], Sh::cellmul(P, s)) : u[k]);
+            e[k] = *at(cell * P.c4 + base);
+        }
+    }
+    if (lut && f == FMT1T) {           // one in-cell threshold: c ? lo + inc : lo, inc = 1 or 1 + 2^sb
+        const uint32_t sp = Sh::t1sp(P, s);
+        uint32_t any = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            u[i][k] = lut ? offset_of<Sh>(P, s, v[s][k]) : 0u;
-            if (!lut || (k > 0 && same)) {
-                e[i][k] = 0u;
-            } else if (f == FMT16) {
-                const uint32_t cell = u[i][k] >> Sh::s1(P, s);
-                e[i][k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
-            } else {
-                const uint32_t cell = f == FMTEX ? u[i][k] : (Sh::s1(P, s) ? __umulhi(u[i][k], Sh::cellmul(P, s)) : u[i][k]);
-                e[i][k] = *at(cell * P.c4 + base);
-            }
-            if (k > 0 && same) e[i][k] = e[i][0];
+            if (k >= nk) continue;
+            const uint32_t x = e[k];
+            const uint32_t zz = u[k] * P.slot[s].t1_mul + Sh::t1ones(P, s);
+            const uint32_t lo = x & Sh::t1dmask(P, s);
+            uint32_t inc = 1u;
+            if (Sh::packs(P, s))
+                inc = ((Sh::t1cutsh(P, s) ? __umulhi(x, Sh::t1cutmul(P, s)) : x) & (Sh::bmask(P, s) + 1u)) | 1u;
+            bs[k] = zz >= x ? lo * P.c1 + inc : lo;
+            any |= x;
         }
-        ex[s][0] = e[i][0]; ex[s][1] = e[i][1]; ex[s][2] = e[i][2]; ex[s][3] = e[i][3];
-    }
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const int s = S0 + i;
-        const int f = Sh::fmt(P, s);
-        if (f == FMT1T) {              // one in-cell threshold: c ? lo + inc : lo, inc = 1 or 1 + 2^sb
-            const uint32_t sp = Sh::t1sp(P, s);
+        if (any & sp) {                // >= 2 breakpoints in some cell
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t x = e[i][k];
-                const uint32_t zz = u[i][k] * P.slot[s].t1_mul + Sh::t1ones(P, s);
-                const uint32_t lo = x & Sh::t1dmask(P, s);
-                uint32_t inc = 1u;
-                if (Sh::packs(P, s))
-                    inc = ((Sh::t1cutsh(P, s) ? __umulhi(x, Sh::t1cutmul(P, s)) : x) & (Sh::bmask(P, s) + 1u)) | 1u;
-                bs[s][k] = zz >= x ? lo * P.c1 + inc : lo;
-            }
-            if ((e[i][0] | e[i][1] | e[i][2] | e[i][3]) & sp) {      // >= 2 breakpoints in some cell
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (!(e[i][k] & sp)) continue;
-                    const uint4 r = g_smem[e[i][k] & Sh::t1dmask(P, s)];
-                    if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
-                        const uint32_t c1 = u[i][k] > r.y, c2 = u[i][k] > r.z, c3 = u[i][k] > r.w;
-                        uint32_t b = (r.x & kIdxMask) + 1u + c1 + c2 + c3;
-                        if (Sh::packs(P, s))
-                            b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) +
-                                  (c2 & (r.x >> (kIncShift + 1))) + (c3 & (r.x >> (kIncShift + 2)))) << Sh::sb(P, s);
-                        bs[s][k] = b;
-                    } else {                   // nested block or list: out-of-line walk
-                        bs[s][k] = t1_special_bs(Sh::lutb(P, s) / 4, Sh::s1(P, s), Sh::sb(P, s),
-                                                 Sh::packs(P, s) ? Sh::mapb(P, s) : kNone, u[i][k]);
-                    }
+                if (k >= nk || !(e[k] & sp)) continue;
+                const uint4 r = g_smem[e[k] & Sh::t1dmask(P, s)];
+                if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
+                    const uint32_t c1 = u[k] > r.y, c2 = u[k] > r.z, c3 = u[k] > r.w;
+                    uint32_t b = (r.x & kIdxMask) + 1u + c1 + c2 + c3;
+                    if (Sh::packs(P, s))
+                        b |= (((r.x >> kSubShift) & kSubMask) + (c1 & (r.x >> kIncShift)) +
+                              (c2 & (r.x >> (kIncShift + 1))) + (c3 & (r.x >> (kIncShift + 2)))) << Sh::sb(P, s);
+                    bs[k] = b;
+                } else {                   // nested block or list: out-of-line walk
+                    bs[k] = t1_special_bs(Sh::lutb(P, s) / 4, Sh::s1(P, s), Sh::sb(P, s),
+                                          Sh::packs(P, s) ? Sh::mapb(P, s) : kNone, u[k]);
                 }
             }
-        } else if (f == FMT32) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                bs[s][k] = e[i][k];
-                if (e[i][k] & kSpecial) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask, u[i][k]);
-            }
-        } else if (f == FMT16) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                bs[s][k] = e[i][k];
-                if (e[i][k] & 0x8000u) bs[s][k] = boundary_bucket<Sh>(P, s, e[i][k] & kRecMask16, u[i][k]);
-            }
-        } else {                       // FMTEX: exact cells, never a boundary
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bs[s][k] = e[i][k];
         }
+    } else if (lut && f == FMT32) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= nk) continue;
+            bs[k] = e[k];
+            if (e[k] & kSpecial) bs[k] = boundary_bucket<Sh>(P, s, e[k] & kRecMask, u[k]);
+        }
+    } else if (lut && f == FMT16) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= nk) continue;
+            bs[k] = e[k];
+            if (e[k] & 0x8000u) bs[k] = boundary_bucket<Sh>(P, s, e[k] & kRecMask16, u[k]);
+        }
+    } else if (lut) {                  // FMTEX: exact cells, never a boundary
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bs[k] = e[k];
+    } else if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {      // binary-search fallback column
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= nk) continue;
+            const uint32_t b = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[k]);
+            bs[k] = b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << 16 : 0u);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bs[k] = 0u;
     }
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const int s = S0 + i;
-        if (Sh::active(P, s) && Sh::mode(P, s) == MODE_SEARCH) {      // binary-search fallback column
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t b = search_bucket(P.slot[s].bps, P.slot[s].nbp, v[s][k]);
-                bs[s][k] = b | (Sh::packs(P, s) ? *at(Sh::mapb(P, s) + 4 * b) << 16 : 0u);
-            }
-        }
+    if (same) {
+        bs[1] = bs[2] = bs[3] = bs[0];
+        e[1] = e[2] = e[3] = e[0];
     }
 }
 
@@ -417,35 +415,23 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NC][4], uint32_t s,
     return r;
 }
 
-// Everything one row quad contributes.  keep: one bit per row.
+// Own bucket histogram (columns that are no grid's full-resolution side) and HLL of one
+// column of a row quad.
 template <class Sh>
-__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
-                                          uint32_t keep, const uint32_t *wlim) {
-    constexpr int NC = Sh::NC;
+__device__ __forceinline__ void column_tail(const ProbeParams &P, int s, bool same, uint32_t keep, const uint32_t *wlim,
+                                            const KeyT<Sh> (&v)[4], const uint32_t (&bs)[4], const uint32_t (&ex)[4]) {
     uint32_t *sm = smem32();
     const uint32_t dbg = P.dbg;
-    KeyT<Sh> v[NC][4];
-#pragma unroll
-    for (int s = 0; s < NC; ++s)
-        if (Sh::active(P, s)) decode<Sh>(P, s, r[s], v[s]);
-    uint32_t bs[NC][4], ex[NC][4];
-    buckets<Sh, 0, (NC < 4 ? NC : 4)>(P, v, bs, ex);
-    if (NC > 4) buckets<Sh, (NC > 4 ? 4 : 0), (NC > 4 ? NC - 4 : 1)>(P, v, bs, ex);
-    // own bucket histograms (columns that are no grid's full-resolution side)
-#pragma unroll
-    for (int s = 0; s < NC; ++s) {
-        if (!Sh::active(P, s) || !Sh::ownh(P, s) || (dbg & 2)) continue;
+    if (Sh::ownh(P, s) && !(dbg & 2)) {
         const uint32_t h = Sh::histb(P, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[s][k] & Sh::bmask(P, s))), 1u);
+            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[k] & Sh::bmask(P, s))), 1u);
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
     // which the rest of the loop leaves idle); survivors do a predicated ATOMS.MAX.
-#pragma unroll
-    for (int s = 0; s < NC; ++s) {
-        if (!Sh::active(P, s) || !Sh::hll(P, s) || (dbg & 8)) continue;
+    if (Sh::hll(P, s) && !(dbg & 8)) {
         uint32_t *R = sm + Sh::hllw(P, s);
         if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
             // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
@@ -454,26 +440,24 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             // value skip the register entirely.  One test covers the quad.
             uint32_t any = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) any |= ((keep >> k) & 1u) ? ex[s][k] : 0u;
+            for (int k = 0; k < 4; ++k) any |= ((keep >> k) & 1u) ? ex[k] : 0u;
             if ((any >> 27) && !(dbg & 1)) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const uint32_t x = ex[s][k], rank = x >> 27;
+                    const uint32_t x = ex[k], rank = x >> 27;
                     if (((keep >> k) & 1u) && rank) {
                         atomicMax(R + ((x >> 15) & 0xFFFu), rank);
-                        *at(Sh::lutb(P, s) + 4 * offset_of<Sh>(P, s, v[s][k])) = x & 0x07FFFFFFu;
+                        *at(Sh::lutb(P, s) + 4 * offset_of<Sh>(P, s, v[k])) = x & 0x07FFFFFFu;
                     }
                 }
             }
         } else if (Sh::is32(P, s)) {
             // w32 is even, so clearing bit 0 keeps "w32 <= lim" and puts the non-kept marker ~0 above it
             const uint32_t lim = wlim[s];
-            // clustered column, all four keys equal: one hash covers the quad
-            const bool same = Sh::clust(P, s) && v[s][0] == v[s][1] && v[s][1] == v[s][2] && v[s][2] == v[s][3];
             uint32_t w32[4], idx[4], wmin = 0xFFFFFFFFu;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                uint32_t h = static_cast<uint32_t>(v[s][k]);
+                uint32_t h = static_cast<uint32_t>(v[k]);
                 h ^= __umulhi(h, 1u << 16);
                 h *= 0x85EBCA6BU;
                 h ^= __umulhi(h, 1u << 19);
@@ -498,15 +482,19 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             const uint64_t lim = ~0ull >> (32 - __popc(wlim[s] | 1u));     // L from the 32-bit limit
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint64_t h = mix64(static_cast<uint64_t>(v[s][k]) + GACE_GAMMA);
+                const uint64_t h = mix64(static_cast<uint64_t>(v[k]) + GACE_GAMMA);
                 const uint64_t w64 = (h << kHllP) | (1ull << (kHllP - 1));
                 const uint32_t idx = static_cast<uint32_t>(h >> (64 - kHllP));
                 red_max_if(((keep >> k) & 1u) && w64 <= lim && !(dbg & 1), R + idx, __clzll(w64) + 1);
             }
         }
     }
-    // pairs
-    if (dbg & 4) return;
+}
+
+// Pair grids / per-row pairs of one row quad.
+template <class Sh>
+__device__ __forceinline__ void pair_work(const ProbeParams &P, uint32_t keep, const uint32_t (&bs)[Sh::NC][4]) {
+    constexpr int NC = Sh::NC;
     if (Sh::STATIC) {
 #pragma unroll
         for (int g = 0; g < Sh::NG; ++g) {
@@ -532,6 +520,35 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             if (G.dend > G.dbeg) direct_pairs(P, P.slot[G.a].bmask, P.slot[G.b].bmask, G, ba, bb, keep);
         }
     }
+}
+
+// Everything one row quad contributes.  keep: one bit per row.
+template <class Sh>
+__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
+                                          uint32_t keep, const uint32_t *wlim) {
+    constexpr int NC = Sh::NC;
+    uint32_t *sm = smem32();
+    const uint32_t dbg = P.dbg;
+    uint32_t bs[NC][4];
+    // one column at a time (bucket, own histogram, HLL): only that column's keys and lookup
+    // words are live next to the quad's bucket words
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        if (!Sh::active(P, s)) {
+            bs[s][0] = bs[s][1] = bs[s][2] = bs[s][3] = 0u;
+            continue;
+        }
+        KeyT<Sh> v[4];
+        decode<Sh>(P, s, r[s], v);
+        // clustered column, all four keys equal: one lookup and one hash cover the quad
+        const bool same = Sh::clust(P, s) && v[0] == v[1] && v[1] == v[2] && v[2] == v[3];
+        uint32_t ex[4];
+        bucket_col<Sh>(P, s, same, v, bs[s], ex);
+        column_tail<Sh>(P, s, same, keep, wlim, v, bs[s], ex);
+    }
+    // pairs
+    if (dbg & 4) return;
+    pair_work<Sh>(P, keep, bs);
 }
 
 // One row past the last full unit (scalar loads; out of line: cold code).
