@@ -1287,7 +1287,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
 
     // rows per launch: keep every CTA's u32 bins below 2^31
-    const uint64_t max_rows = (uint64_t)grid * kThreads * (1ull << 19);
+    // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
+    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
     uint64_t launches = 0;
     double h2d_ms = 0;
     // specialised (NVRTC) kernel for large launches, generic precompiled kernel otherwise

@@ -206,19 +206,19 @@ struct Unit {
 };
 
 template <class Sh>
-__device__ __forceinline__ void load_unit(const ProbeParams &P, uint64_t u, Unit<Sh> &X) {
+__device__ __forceinline__ void load_unit(const ProbeParams &P, uint32_t u, Unit<Sh> &X) {
 #pragma unroll
     for (int s = 0; s < Sh::NC; ++s) {
         if (!Sh::active(P, s)) continue;
         const char *base = static_cast<const char *>(P.slot[s].ptr);
         if (Sh::is32(P, s)) {
 #pragma unroll
-            for (int j = 0; j < Sh::U; ++j) X.r[s][j][0] = ld_stream(base + (u * Sh::U + j) * 16);
+            for (int j = 0; j < Sh::U; ++j) X.r[s][j][0] = ld_stream(base + ((uint64_t)u * Sh::U + j) * 16);
         } else {
 #pragma unroll
             for (int j = 0; j < Sh::U; ++j) {
-                X.r[s][j][0] = ld_stream(base + (u * Sh::U + j) * 32);
-                X.r[s][j][Sh::I64 ? 1 : 0] = ld_stream(base + (u * Sh::U + j) * 32 + 16);
+                X.r[s][j][0] = ld_stream(base + ((uint64_t)u * Sh::U + j) * 32);
+                X.r[s][j][Sh::I64 ? 1 : 0] = ld_stream(base + ((uint64_t)u * Sh::U + j) * 32 + 16);
             }
         }
     }
@@ -586,17 +586,13 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     if (threadIdx.x < kMaxSlots * (kThreads / 32 + 1)) (&s_wlim[0][0])[threadIdx.x] = 0xFFFFFFFEu;
     __syncthreads();
 
-    const uint64_t nunits = P.nrows / (4 * U);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // unit indices fit 32 bits: the host caps a launch at 2^31 units
+    const uint32_t nunits = static_cast<uint32_t>(P.nrows / (4 * U));
+    const uint32_t stride = gridDim.x * blockDim.x;
     uint32_t kept = 0;
     uint32_t *wlim = s_wlim[threadIdx.x >> 5];
     uint32_t it = 0, next_refresh = 4;
-    uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    Unit<Sh> X;
-    if (u < nunits) load_unit<Sh>(P, u, X);
-    for (; u < nunits; u += stride, ++it) {
-        Unit<Sh> Xn;
-        if (u + stride < nunits) load_unit<Sh>(P, u + stride, Xn);       // prefetch
+    auto body = [&](const Unit<Sh> &X, uint32_t u) {
         if (it == next_refresh) {
             next_refresh = it + min(it, 32u);
             if (__activemask() == 0xFFFFFFFFu) {
@@ -613,7 +609,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         for (int j = 0; j < U; ++j) {
             uint32_t keep = 0xFu;
             if (Sh::SAMPLE) {
-                const uint64_t g0 = P.row0 + (u * U + j) * 4;
+                const uint64_t g0 = P.row0 + ((uint64_t)u * U + j) * 4;
                 keep = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) keep |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
@@ -628,6 +624,15 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             }
             quad_work<Sh>(P, rj, keep, wlim);
         }
+        ++it;
+    };
+    uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    Unit<Sh> X;
+    if (u < nunits) load_unit<Sh>(P, u, X);
+    for (; u < nunits; u += stride) {
+        Unit<Sh> Xn;
+        if (u + stride < nunits) load_unit<Sh>(P, u + stride, Xn);       // prefetch
+        body(X, u);
         X = Xn;
     }
     if (!Sh::SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed
