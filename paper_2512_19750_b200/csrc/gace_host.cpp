@@ -549,9 +549,12 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             S.base = S.dl;
             S.clamp = true;
             S.clamp_lo = S.clamp_hi = S.dl;
-        } else if ((uint64_t)S.dh - (uint64_t)S.dl < (1ull << 32) && !t->host) {
+        } else if ((uint64_t)S.dh - (uint64_t)S.dl < (1ull << 32) && !t->host &&
+                   ((uint64_t)S.T.back() - ((uint64_t)S.T.front() - 1)) * 4 > (uint64_t)S.dh - (uint64_t)S.dl) {
             S.base = S.dl;                       // domain cover, values never leave it
         } else if ((uint64_t)S.T.back() - ((uint64_t)S.T.front() - 1) < (1ull << 32)) {
+            // breakpoint-span cover (host tables, or breakpoints in a small part of the domain:
+            // much finer cells for two extra ops per key), keys clamped into it
             S.base = S.T.front() - 1;            // breakpoint-span cover, clamp into it
             S.clamp = true;
             S.clamp_lo = S.base;

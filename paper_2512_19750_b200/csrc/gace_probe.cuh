@@ -472,9 +472,18 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, bool sa
             }
             // one test for the quad: some key's rank beats the lower bound L
             if (wmin <= lim && !(dbg & 1)) {
+                // exact test against the CTA's register first (all loads issued, then the
+                // compares): a frequent value whose rank is already in (a skewed column's
+                // head, e.g. fmix32(0) = 0 -> rank 21) never reaches the atomic
+                uint32_t cur[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    red_max_if(w32[k] <= lim, R + idx[k], __clz(w32[k]) + 1);
+                    cur[k] = w32[k] <= lim ? R[idx[k]] : 64u;
+                    if (same) break;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    red_max_if(__clz(w32[k]) + 1 > cur[k], R + idx[k], __clz(w32[k]) + 1);
                     if (same) break;
                 }
             }

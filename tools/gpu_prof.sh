@@ -5,7 +5,7 @@ C=${1:-C5}; TAG=${2:-r01}
 mkdir -p gpurun_out
 B="python bench.py --config $C --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
 $B > gpurun_out/plain_$TAG.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'gace|fin_|probe|minmax|sample' -c 200 --csv \
     --log-file gpurun_out/launches_${C}_$TAG.csv $B > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
 G="python tools/gpu_debug.py $C 0"
