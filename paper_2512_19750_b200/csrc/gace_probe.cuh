@@ -60,6 +60,24 @@ __device__ __forceinline__ uint32_t *at(uint32_t a) {
     return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(g_smem) + a);
 }
 
+// Hot-path shared-memory accesses by byte offset from the dynamic shared memory: the
+// window base is a uniform value the compiler folds into the address operand
+// (LDS [R + UR]), instead of materialising generic pointers per access.
+__device__ __forceinline__ uint32_t sbase() { return static_cast<uint32_t>(__cvta_generic_to_shared(g_smem)); }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t off) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase() + off));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t off) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(sbase() + off));
+    return v;
+}
+__device__ __forceinline__ void red_add1(uint32_t off) {
+    asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(sbase() + off) : "memory");
+}
+
 // Predicated shared-memory ops as single instructions (a C++ `if` around them becomes a
 // branch with reconvergence barriers on every key).
 __device__ __forceinline__ uint32_t saddr(const void *p) {
@@ -303,10 +321,10 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, bool sam
         u[k] = offset_of<Sh>(P, s, v[k]);
         if (f == FMT16) {
             const uint32_t cell = u[k] >> Sh::s1(P, s);
-            e[k] = *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(g_smem) + base + 2 * cell);
+            e[k] = lds_u16(base + 2 * cell);
         } else {
             const uint32_t cell = f == FMTEX ? u[k] : (Sh::s1(P, s) ? __umulhi(u[k], Sh::cellmul(P, s)) : u[k]);
-            e[k] = *at(cell * P.c4 + base);
+            e[k] = lds_u32(cell * P.c4 + base);
         }
     }
     if (lut && f == FMT1T) {           // one in-cell threshold: c ? lo + inc : lo, inc = 1 or 1 + 2^sb
@@ -402,7 +420,7 @@ __device__ __forceinline__ void grid_add(uint32_t c4, uint32_t amask, uint32_t s
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
             const uint32_t sub = packed ? __umulhi(bsb[k], submul) & submask : *at(map + 4 * (bsb[k] & bmask));
-            atomicAdd(at(((bsa[k] & amask) * nbs + sub) * c4 + grid), 1u);
+            red_add1(((bsa[k] & amask) * nbs + sub) * c4 + grid);
         }
     }
 }
@@ -426,7 +444,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, bool sa
         const uint32_t h = Sh::histb(P, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) atomicAdd(at(h + 4 * (bs[k] & Sh::bmask(P, s))), 1u);
+            if ((keep >> k) & 1u) red_add1(h + 4 * (bs[k] & Sh::bmask(P, s)));
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
