@@ -216,7 +216,7 @@ static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
     auto k = probe_kernel<NC, SAMPLE, I64>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 2048);
         if (e != cudaSuccess) return e;
         configured = true;
     }

@@ -35,7 +35,7 @@ constexpr int kMaxSlots = 8;           // GACE_MAX_PROBED_COLS
 constexpr int kMaxGroups = 28;         // unordered slot pairs
 constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
-constexpr int kThreads = 768;          // probe CTA size (one CTA per SM, <= 80 registers)
+constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM, <= 64 registers)
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
 constexpr uint32_t kSpecial = 0x80000000u;  // entry is a nested block or a list
 constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list

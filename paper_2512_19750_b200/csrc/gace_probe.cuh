@@ -18,6 +18,10 @@
 #pragma once
 #include "gace_plan.h"
 
+#ifndef GACE_PREFETCH
+#define GACE_PREFETCH 0
+#endif
+
 namespace gace {
 
 #define GACE_GAMMA 0x9E3779B97F4A7C15ULL
@@ -654,6 +658,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         ++it;
     };
     uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+#if GACE_PREFETCH
     Unit<Sh> X;
     if (u < nunits) load_unit<Sh>(P, u, X);
     for (; u < nunits; u += stride) {
@@ -662,6 +667,15 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         body(X, u);
         X = Xn;
     }
+#else
+    // no register prefetch: the 24 warps of the SM keep enough loads in flight, and the
+    // registers go to the lookup / hash work instead
+    for (; u < nunits; u += stride) {
+        Unit<Sh> X;
+        load_unit<Sh>(P, u, X);
+        body(X, u);
+    }
+#endif
     if (!Sh::SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed
     // tail rows [nunits * 4U, nrows): one row per thread of the last CTA
     const uint64_t tail0 = nunits * 4 * U;
