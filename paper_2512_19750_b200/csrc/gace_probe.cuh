@@ -309,13 +309,14 @@ __device__ __noinline__ uint32_t t1_special_bs(uint32_t lut_w, uint32_t s1, uint
 // resolve inline (FMT1T: one threshold) or, for the rare special cells, through one test
 // per column quad and a record walk.  Multiplies by 2^k use opaque multipliers (P.c4,
 // P.slot[].t1_mul) or high multiplies so that they run on the FMA pipe.
-template <class Sh>
-__device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, bool same, const KeyT<Sh> (&v)[4],
+template <class Sh, int NK>
+__device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const KeyT<Sh> (&v)[4],
                                            uint32_t (&bs)[4], uint32_t (&e)[4]) {
     const bool lut = Sh::active(P, s) && Sh::mode(P, s) == MODE_LUT;
     const uint32_t base = Sh::lutb(P, s);
     const int f = Sh::fmt(P, s);
-    const int nk = same ? 1 : 4;
+    constexpr int nk = NK;
+    constexpr bool same = NK == 1;
     uint32_t u[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -439,9 +440,10 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NC][4], uint32_t s,
 
 // Own bucket histogram (columns that are no grid's full-resolution side) and HLL of one
 // column of a row quad.
-template <class Sh>
-__device__ __forceinline__ void column_tail(const ProbeParams &P, int s, bool same, uint32_t keep, const uint32_t *wlim,
+template <class Sh, int NK>
+__device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_t keep, const uint32_t *wlim,
                                             const KeyT<Sh> (&v)[4], const uint32_t (&bs)[4], const uint32_t (&ex)[4]) {
+    constexpr bool same = NK == 1;
     uint32_t *sm = smem32();
     const uint32_t dbg = P.dbg;
     if (Sh::ownh(P, s) && !(dbg & 2)) {
@@ -572,10 +574,14 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
         KeyT<Sh> v[4];
         decode<Sh>(P, s, r[s], v);
         // clustered column, all four keys equal: one lookup and one hash cover the quad
-        const bool same = Sh::clust(P, s) && v[0] == v[1] && v[1] == v[2] && v[2] == v[3];
         uint32_t ex[4];
-        bucket_col<Sh>(P, s, same, v, bs[s], ex);
-        column_tail<Sh>(P, s, same, keep, wlim, v, bs[s], ex);
+        if (Sh::clust(P, s) && v[0] == v[1] && v[1] == v[2] && v[2] == v[3]) {
+            bucket_col<Sh, 1>(P, s, v, bs[s], ex);
+            column_tail<Sh, 1>(P, s, keep, wlim, v, bs[s], ex);
+        } else {
+            bucket_col<Sh, 4>(P, s, v, bs[s], ex);
+            column_tail<Sh, 4>(P, s, keep, wlim, v, bs[s], ex);
+        }
     }
     // pairs
     if (dbg & 4) return;
