@@ -103,8 +103,13 @@ typedef struct gace_table gace_table;   /* opaque */
  *   dist             NULL = single GPU, row_offset 0; else gace_dist above (collective:
  *                    every rank calls attach; NCCL comm created here if an id is given).
  *   device           CUDA device ordinal.
- *   cuda_stream      cudaStream_t all work is issued on (NULL = a library-owned stream).
- * One-time work: a min/max pass per column (the table is immutable while attached).
+ *   cuda_stream      cudaStream_t all work is issued on, including the attach-time pass
+ *                    below: pass the stream that produced the columns (NULL = a
+ *                    library-owned stream, which is NOT ordered after other streams -- the
+ *                    caller must then have synchronised the columns before attach).
+ * One-time work: a min/max pass per column (the table is immutable while attached); the
+ * lookup tables are built over that domain, so columns still being written at attach
+ * give wrong results, not an error.
  */
 gace_status gace_table_attach(const void *const *col_dev_ptrs, const gace_dtype *dtypes,
                               uint32_t ncols, uint64_t nrows_local, const gace_dist *dist,

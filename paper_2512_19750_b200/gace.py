@@ -239,8 +239,18 @@ class Table:
                       ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None, dist.comm)
         self.row_offset = dist.row_offset if dist else 0
         s = None
+        if stream is None and not host:
+            # the attach-time domain scan (and every probe) must see the finished columns:
+            # work on the caller's current torch stream, or -- for the legacy default stream,
+            # handle 0, which the C-ABI reads as "library stream" -- wait for it here
+            import torch
+            stream = torch.cuda.current_stream(device)
         if stream is not None:
             s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+            if not s:
+                if hasattr(stream, "synchronize"):
+                    stream.synchronize()
+                s = None
         h = ctypes.c_void_p()
         fn = L.gace_table_attach_host if host else L.gace_table_attach
         _check(fn(arr_p, arr_t, self.ncols, nrows, ctypes.byref(d) if d is not None else None,

@@ -318,3 +318,87 @@ def test_clustered_columns(G, oracle, force_jit):
     Q = np.array([(0, 3), (1, 3), (2, 3), (4, 3)], dtype=synth.PAIR_DTYPE)
     for rate in (1.0, 0.4):
         _check(G, oracle, [ok, other], P, Q, rate, 5, [0, 1])
+
+
+# ------------------------------------------------------------------ scale: many iterations per thread
+# Small tables give each of the 148 x 1024 threads less than one row unit, so the HLL skip
+# bound (refreshed at iterations 4, 8, 16, then every 32, from registers merged across
+# CTAs) and the long-run paths never run.  These sizes give every thread 8..60 iterations.
+
+@pytest.mark.parametrize("name,nrows,rate", [
+    ("C5", 40_000_003, 1.0), ("C4", 24_000_001, 1.0), ("C3", 30_000_002, 1.0), ("C5_i64", 20_000_001, 1.0),
+    ("C5", 36_000_000, 0.5),
+])
+def test_scale_many_iterations(G, oracle, name, nrows, rate):
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, 11, w.hll_cols)
+
+
+def test_fmt1t_special_cells(G, oracle):
+    """Level-1 cells holding 2, 3, 4..8 and dozens of breakpoints (direct records, lists and
+    nested blocks behind the one-threshold format), on both sides of packed pair grids."""
+    g = np.random.default_rng(41)
+    n = 3_000_001
+    a = g.integers(0, 1_000_000, size=n).astype(np.int32)
+    b = g.integers(0, 1_000_000, size=n).astype(np.int32)
+    # keys concentrated where the breakpoints are dense
+    a[: n // 3] = g.integers(500_000, 500_400, size=n // 3)
+    b[: n // 4] = g.integers(10, 90, size=n // 4)
+    rows = []
+    for v in range(500_000, 500_200, 3):                      # dense EQ binds: nested / list cells
+        rows.append((0, 0, 0, v, 0))
+    for lo in (100, 5_000, 77_777, 500_100, 900_000):        # narrow BETWEENs: 2 breakpoints per cell
+        rows += [(0, 5, 0, lo, lo + 1), (0, 5, 1, lo + 2, lo + 9), (0, 5, 0, lo, lo + 30_000)]
+    for v in range(10, 90, 7):                                # b: clustered EQs and ranges
+        rows += [(1, 0, 0, v, 0), (1, 5, 0, v, v + 3)]
+    rows += [(1, 1, 0, 500_000, 0), (1, 4, 1, 999_000, 0), (1, 5, 0, 0, 999_999)]
+    P = np.array(rows, dtype=synth.PRED_DTYPE)
+    na = sum(1 for r in rows if r[0] == 0)
+    Q = np.array([(i, na + j) for i in range(0, na, 5) for j in range(0, len(rows) - na, 4)][:300],
+                 dtype=synth.PAIR_DTYPE)
+    for rate in (1.0, 0.45):
+        _check(G, oracle, [a, b], P, Q, rate, 21, [0, 1])
+
+
+def test_fmt1t_special_cells_specialised(G, oracle, force_jit):
+    test_fmt1t_special_cells(G, oracle)
+
+
+@pytest.mark.slow
+def test_full_size_shard_invariance(G):
+    """At BASELINE's full C5 size (the bench configuration): the whole-table probe equals the
+    sum / max merge of two row shards probed with their global row offsets, and the count
+    invariants hold (predicate + complement = n_sampled, joint <= both marginals)."""
+    w = synth.get("C5")
+    cols = [c.cuda() for c in w.table(device="cuda")]
+    N = w.nrows
+    t = G.Table(cols)
+    try:
+        for rate, seed in ((1.0, 0), (0.01, 0x5EED)):
+            whole = t.probe(w.preds, w.pairs, rate, seed, w.hll_cols)
+            info = (t.last_timing(), G.lib().gace_last_error())
+            cut = (N // 2 + 12345) & ~3                  # 16-byte aligned shard start
+            parts = []
+            for s, e in ((0, cut), (cut, N)):
+                tp = G.Table([c[s:e] for c in cols], dist=G.DistInfo(0, 1, s, N))
+                try:
+                    parts.append(tp.probe(w.preds, w.pairs, rate, seed, w.hll_cols))
+                finally:
+                    tp.detach()
+            assert whole.n_sampled == sum(p.n_sampled for p in parts)
+            bad = np.nonzero(whole.counts != parts[0].counts + parts[1].counts)[0]
+            assert len(bad) == 0, (info, rate, sorted(set(int(w.preds["col"][i]) for i in bad)), bad[:8],
+                                   whole.counts[bad[:4]], parts[0].counts[bad[:4]], parts[1].counts[bad[:4]])
+            np.testing.assert_array_equal(whole.joints, sum(p.joints for p in parts))
+            np.testing.assert_array_equal(whole.regs, np.maximum(parts[0].regs, parts[1].regs))
+            P = w.preds
+            assert np.all(whole.counts <= whole.n_sampled)
+            for q, (i, j) in enumerate(zip(w.pairs["i"], w.pairs["j"])):
+                assert whole.joints[q] <= min(whole.counts[i], whole.counts[j])
+            neg = P.copy()
+            neg["flags"] ^= 1
+            comp = t.probe(neg, None, rate, seed, [])
+            np.testing.assert_array_equal(whole.counts + comp.counts, np.full(len(P), whole.n_sampled, np.uint64))
+    finally:
+        t.detach()
