@@ -1102,6 +1102,11 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
         o += std::string("  __device__ static constexpr uint32_t ") + name + "(const ProbeParams &, int g) { return " +
              gchain([&](uint32_t g) { return u32s(f(P.grp[g])); }) + "; }\n";
     };
+    {
+        const char *ab = getenv("GACE_ABLATE");          // design experiments: ablations baked in
+        o += std::string("  __device__ static constexpr uint32_t dbg(const ProbeParams &) { return ") +
+             std::to_string(ab ? (uint32_t)strtoul(ab, nullptr, 0) : 0u) + "u; }\n";
+    }
     o += "  __device__ static constexpr bool sclamp(const ProbeParams &, int s) { return " +
          chain([&](int i) {
              const SlotParams &Q = P.slot[i];

@@ -191,6 +191,7 @@ struct RtShape {
     __device__ static constexpr bool gdirect(int) { return false; }
     // plan layout (read from the parameters; JitShape bakes them in as immediates)
     __device__ static bool sclamp(const ProbeParams &P, int) { return P.clamp; }
+    __device__ static uint32_t dbg(const ProbeParams &P) { return P.dbg; }
     __device__ static int64_t base(const ProbeParams &P, int s) { return P.slot[s].base; }
     __device__ static int64_t clo(const ProbeParams &P, int s) { return P.slot[s].clamp_lo; }
     __device__ static int64_t chi(const ProbeParams &P, int s) { return P.slot[s].clamp_hi; }
@@ -344,7 +345,7 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
             uint32_t inc = 1u;
             if (Sh::packs(P, s))
                 inc = ((Sh::t1cutsh(P, s) ? __umulhi(x, Sh::t1cutmul(P, s)) : x) & (Sh::bmask(P, s) + 1u)) | 1u;
-            bs[k] = zz >= x ? lo * P.c1 + inc : lo;
+            bs[k] = lo + (zz >= x ? inc : 0u);
             any |= x;
         }
         if (any & sp) {                // >= 2 breakpoints in some cell
@@ -445,7 +446,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
                                             const KeyT<Sh> (&v)[4], const uint32_t (&bs)[4], const uint32_t (&ex)[4]) {
     constexpr bool same = NK == 1;
     uint32_t *sm = smem32();
-    const uint32_t dbg = P.dbg;
+    const uint32_t dbg = Sh::dbg(P);
     if (Sh::ownh(P, s) && !(dbg & 2)) {
         const uint32_t h = Sh::histb(P, s);
 #pragma unroll
@@ -499,15 +500,16 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
                 // exact test against the CTA's register first (all loads issued, then the
                 // compares): a frequent value whose rank is already in (a skewed column's
                 // head, e.g. fmix32(0) = 0 -> rank 21) never reaches the atomic
+                // rank > cur  <=>  w <= ~0 >> cur (cur <= 21; 31 marks "not a survivor": w >= 2^11)
                 uint32_t cur[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    cur[k] = w32[k] <= lim ? R[idx[k]] : 64u;
+                    cur[k] = w32[k] <= lim ? R[idx[k]] : 31u;
                     if (same) break;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    red_max_if(__clz(w32[k]) + 1 > cur[k], R + idx[k], __clz(w32[k]) + 1);
+                    red_max_if(w32[k] <= (0xFFFFFFFFu >> cur[k]), R + idx[k], __clz(w32[k]) + 1);
                     if (same) break;
                 }
             }
@@ -561,7 +563,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
                                           uint32_t keep, const uint32_t *wlim) {
     constexpr int NC = Sh::NC;
     uint32_t *sm = smem32();
-    const uint32_t dbg = P.dbg;
+    const uint32_t dbg = Sh::dbg(P);
     uint32_t bs[NC][4];
     // one column at a time (bucket, own histogram, HLL): only that column's keys and lookup
     // words are live next to the quad's bucket words
