@@ -247,6 +247,18 @@ __device__ __forceinline__ void load_unit(const ProbeParams &P, uint32_t u, Unit
     }
 }
 
+// Column s of unit u (U == 1 layout) into r.
+template <class Sh>
+__device__ __forceinline__ void load_col(const ProbeParams &P, int s, uint32_t u, int4 (&r)[Sh::I64 ? 2 : 1]) {
+    const char *base = static_cast<const char *>(P.slot[s].ptr);
+    if (Sh::is32(P, s)) {
+        r[0] = ld_stream(base + (uint64_t)u * 16);
+    } else {
+        r[0] = ld_stream(base + (uint64_t)u * 32);
+        r[Sh::I64 ? 1 : 0] = ld_stream(base + (uint64_t)u * 32 + 16);
+    }
+}
+
 template <class Sh>
 __device__ __forceinline__ void decode(const ProbeParams &P, int s, const int4 (&r)[Sh::I64 ? 2 : 1],
                                        KeyT<Sh> (&v)[4]) {
@@ -558,9 +570,13 @@ __device__ __forceinline__ void pair_work(const ProbeParams &P, uint32_t keep, c
 }
 
 // Everything one row quad contributes.  keep: one bit per row.
+// unext != kNoUnit: once column s is consumed, its registers are refilled with column s of
+// unit unext, so the next unit's keys are in flight during the rest of this one (no extra
+// registers: a software pipeline column by column).
+constexpr uint32_t kNoUnit = 0xFFFFFFFFu;
 template <class Sh>
-__device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
-                                          uint32_t keep, const uint32_t *wlim) {
+__device__ __forceinline__ void quad_work(const ProbeParams &P, int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
+                                          uint32_t keep, const uint32_t *wlim, uint32_t unext = kNoUnit) {
     constexpr int NC = Sh::NC;
     uint32_t *sm = smem32();
     const uint32_t dbg = Sh::dbg(P);
@@ -584,6 +600,7 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, const int4 (&r)[
             bucket_col<Sh, 4>(P, s, v, bs[s], ex);
             column_tail<Sh, 4>(P, s, keep, wlim, v, bs[s], ex);
         }
+        if (unext != kNoUnit) load_col<Sh>(P, s, unext, r[s]);
     }
     // pairs
     if (dbg & 4) return;
@@ -666,6 +683,53 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         ++it;
     };
     uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    // sample bits of a row quad (all four rows when the probe is not sampled)
+    auto quad_keep = [&](uint32_t uu) -> uint32_t {
+        if (!Sh::SAMPLE) return 0xFu;
+        const uint64_t g0 = P.row0 + (uint64_t)uu * 4;
+        uint32_t kk = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) kk |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
+        return kk;
+    };
+    if (U == 1 && NC <= 4) {
+        // column-streamed loop; a sampled probe loads only quads with a kept row (at rate
+        // 0.01 that is 4 % of the quads, so most key bytes are never read)
+        int4 r[NC][Sh::I64 ? 2 : 1];
+        uint32_t keep = u < nunits ? quad_keep(u) : 0u;
+        if (keep) {
+#pragma unroll
+            for (int s = 0; s < NC; ++s)
+                if (Sh::active(P, s)) load_col<Sh>(P, s, u, r[s]);
+        }
+        for (; u < nunits; u += stride) {
+            uint32_t un = u + stride < nunits ? u + stride : kNoUnit;
+            const uint32_t keep_n = un != kNoUnit ? quad_keep(un) : 0u;
+            if (!keep_n) un = kNoUnit;
+            if (it == next_refresh) {
+                next_refresh = it + min(it, 32u);
+                if (__activemask() == 0xFFFFFFFFu) {
+#pragma unroll
+                    for (int s = 0; s < NC; ++s)
+                        if (Sh::active(P, s) && Sh::hll(P, s)) {
+                            const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 31u);
+                            if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
+                        }
+                    __syncwarp();
+                }
+            }
+            ++it;
+            if (Sh::SAMPLE) kept += __popc(keep);
+            if (keep) {
+                quad_work<Sh>(P, r, keep, wlim, un);
+            } else if (un != kNoUnit) {        // nothing kept here: start the next unit's loads
+#pragma unroll
+                for (int s = 0; s < NC; ++s)
+                    if (Sh::active(P, s)) load_col<Sh>(P, s, un, r[s]);
+            }
+            keep = keep_n;
+        }
+    } else {
 #if GACE_PREFETCH
     Unit<Sh> X;
     if (u < nunits) load_unit<Sh>(P, u, X);
@@ -684,6 +748,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         body(X, u);
     }
 #endif
+    }
     if (!Sh::SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed
     // tail rows [nunits * 4U, nrows): one row per thread of the last CTA
     const uint64_t tail0 = nunits * 4 * U;
