@@ -495,11 +495,13 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 uint32_t h = static_cast<uint32_t>(v[k]);
-                h ^= __umulhi(h, 1u << 16);
+                // fmix32; one shift on the FMA pipe (high multiply), two on the ALU pipe, so
+                // the hash block does not pile onto one pipe (5 FMA + 5 ALU ops)
+                h ^= h >> 16;
                 h *= 0x85EBCA6BU;
                 h ^= __umulhi(h, 1u << 19);
                 h *= 0xC2B2AE35U;
-                h ^= __umulhi(h, 1u << 16);                          // = fmix32(x)
+                h ^= h >> 16;                                        // = fmix32(x)
                 w32[k] = h * P.c_hll + (1u << (kHllP - 1));          // never ~0 (low bits 0x800)
                 idx[k] = __umulhi(h, 1u << kHllP);                   // h >> (32 - p)
                 const bool kept_k = (same && k > 0) ? false : (same ? keep != 0 : ((keep >> k) & 1u));
