@@ -431,13 +431,13 @@ __device__ __forceinline__ void direct_pairs(const ProbeParams &P, uint32_t ma, 
 }
 
 // grid[bucket of a][sub-bucket of b] += 1 for each kept row (sub: packed or via the map)
-__device__ __forceinline__ void grid_add(uint32_t c4, uint32_t amask, uint32_t submul, uint32_t submask, uint32_t bmask,
+__device__ __forceinline__ void grid_add(uint32_t c4, uint32_t amask, uint32_t bsh, uint32_t submask, uint32_t bmask,
                                          uint32_t grid, uint32_t nbs, uint32_t map, bool packed,
                                          const uint32_t (&bsa)[4], const uint32_t (&bsb)[4], uint32_t keep) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if ((keep >> k) & 1u) {
-            const uint32_t sub = packed ? __umulhi(bsb[k], submul) & submask : *at(map + 4 * (bsb[k] & bmask));
+            const uint32_t sub = packed ? (bsb[k] >> bsh) & submask : *at(map + 4 * (bsb[k] & bmask));
             red_add1(((bsa[k] & amask) * nbs + sub) * c4 + grid);
         }
     }
@@ -503,7 +503,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
                 h *= 0xC2B2AE35U;
                 h ^= h >> 16;                                        // = fmix32(x)
                 w32[k] = h * P.c_hll + (1u << (kHllP - 1));          // never ~0 (low bits 0x800)
-                idx[k] = __umulhi(h, 1u << kHllP);                   // h >> (32 - p)
+                idx[k] = h >> (32 - kHllP);
                 const bool kept_k = (same && k > 0) ? false : (same ? keep != 0 : ((keep >> k) & 1u));
                 if (!kept_k) w32[k] = 0xFFFFFFFFu;
                 wmin = min(wmin, w32[k]);
@@ -550,7 +550,7 @@ __device__ __forceinline__ void pair_work(const ProbeParams &P, uint32_t keep, c
             const GroupParams &G = P.grp[g];
             const int a = Sh::ga(g), b = Sh::gb(g);
             if (Sh::ggrid(g))
-                grid_add(P.c4, Sh::bmask(P, a), Sh::submul(P, b), Sh::submask(P, b), Sh::bmask(P, b), Sh::ggridb(P, g),
+                grid_add(P.c4, Sh::bmask(P, a), Sh::sb(P, b), Sh::submask(P, b), Sh::bmask(P, b), Sh::ggridb(P, g),
                          Sh::gnbs(P, g), Sh::gmapb(P, g), Sh::gpacked(g), bs[a], bs[b], keep);
             if (Sh::gdirect(g)) direct_pairs(P, Sh::bmask(P, a), Sh::bmask(P, b), G, bs[a], bs[b], keep);
         }
@@ -564,7 +564,7 @@ __device__ __forceinline__ void pair_work(const ProbeParams &P, uint32_t keep, c
                 bb[k] = pick<NC>(bs, G.b, k);
             }
             if (G.has_grid)
-                grid_add(P.c4, P.slot[G.a].bmask, P.slot[G.b].sub_mul, P.slot[G.b].submask, P.slot[G.b].bmask,
+                grid_add(P.c4, P.slot[G.a].bmask, P.slot[G.b].sb, P.slot[G.b].submask, P.slot[G.b].bmask,
                          G.grid_addr, G.nbs, G.map_addr, G.packed, ba, bb, keep);
             if (G.dend > G.dbeg) direct_pairs(P, P.slot[G.a].bmask, P.slot[G.b].bmask, G, ba, bb, keep);
         }
