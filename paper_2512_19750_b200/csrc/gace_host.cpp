@@ -566,7 +566,14 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     // level-1 size target: 16 cells per breakpoint, 64..4096; coarsen the largest table while over budget
     std::vector<uint32_t> s1(pl.slots.size(), 0);
     auto span_of = [](const SlotPlan &S) -> uint64_t {
-        return S.clamp ? (uint64_t)S.clamp_hi - (uint64_t)S.clamp_lo : (uint64_t)S.dh - (uint64_t)S.dl;
+        return S.clamp ? (uint64_t)S.clamp_hi - (uint64_t)S.clamp_lo : (uint64_t)S.dh - (uint64_t)S.base;
+    };
+    // FMT1T on a non-negative (or all-negative) int32 domain: cells aligned to multiples of
+    // 2^s1 of the key itself, so the kernel indexes with key >> s1 and folds the base into
+    // the address immediate (one op per key less)
+    auto t1_rebase = [](SlotPlan &S, uint32_t sh) {
+        if (S.fmt != FMT1T || S.clamp || S.dtype != GACE_I32 || !(S.dl >= 0 || S.dh < 0)) return;
+        S.base = (int64_t)((uint64_t)S.dl & ~((1ull << sh) - 1));
     };
     auto to_search = [](SlotPlan &S) {
         S.mode = MODE_SEARCH;
@@ -603,6 +610,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         } else if (use_t1 && t1s <= t1_max_s1(S, nsub_of(S))) {
             S.fmt = FMT1T;
             s1[i] = t1s;
+            t1_rebase(S, t1s);
         } else {
             S.fmt = narrow ? FMT16 : FMT32;
             const uint64_t cap = S.fmt == FMT16 ? 16384 : 8192;
@@ -612,7 +620,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             while (sh < 31 && (span >> sh) + 1 > target) ++sh;
             s1[i] = sh;
         }
-        if (!build_lut(S, span, s1[i]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
+        if (!build_lut(S, span_of(S), s1[i]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
     for (int iter = 0; iter < 256; ++iter) {
         size_t tot = 0;
@@ -636,7 +644,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             to_search(S);
             continue;
         }
-        if (!build_lut(S, span_of(S), ++s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
+        ++s1[worst];
+        if (S.fmt == FMT1T) t1_rebase(S, s1[worst]);
+        else if (!S.clamp && S.mode == MODE_LUT) S.base = S.dl;          // left FMT1T: plain domain cover
+        if (!build_lut(S, span_of(S), s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
 
     // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] | hll
@@ -1115,6 +1126,20 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
              return std::string(c ? "1" : "0");
          }, nc) + "; }\n";
     slot_i64("base", [](const SlotParams &Q) { return Q.base; });
+    // folded addressing (int32, no clamp): FMTEX always; FMT1T when its cells are aligned keys
+    auto foldable = [](const SlotParams &Q) {
+        if (Q.dtype != 0 || Q.mode != MODE_LUT || Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX) return false;
+        if (Q.fmt == FMTEX) return true;
+        return Q.fmt == FMT1T && Q.s1 >= 1 && ((uint64_t)Q.base & ((1ull << Q.s1) - 1)) == 0 && Q.base >= 0;
+    };
+    o += "  __device__ static constexpr bool fold(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(foldable(P.slot[i]) ? "1" : "0"); }, nc) + "; }\n";
+    slot_u32("foldb", [&](const SlotParams &Q) {
+        return foldable(Q) ? 4 * Q.lut_w - 4 * (uint32_t)((uint64_t)Q.base >> Q.s1) : 0u;
+    });
+    slot_u32("foldz", [&](const SlotParams &Q) {
+        return foldable(Q) && Q.fmt == FMT1T ? Q.t1_ones - (uint32_t)Q.base * Q.t1_mul : 0u;
+    });
     slot_i64("clo", [](const SlotParams &Q) { return Q.clamp_lo; });
     slot_i64("chi", [](const SlotParams &Q) { return Q.clamp_hi; });
     slot_u32("s1", [](const SlotParams &Q) { return Q.s1; });

@@ -210,6 +210,9 @@ struct RtShape {
     __device__ static uint32_t submask(const ProbeParams &P, int s) { return P.slot[s].submask; }
     __device__ static uint32_t submul(const ProbeParams &P, int s) { return P.slot[s].sub_mul; }
     __device__ static uint32_t cellmul(const ProbeParams &P, int s) { return P.slot[s].cell_mul; }
+    __device__ static constexpr bool fold(const ProbeParams &, int) { return false; }
+    __device__ static constexpr uint32_t foldb(const ProbeParams &, int) { return 0u; }
+    __device__ static constexpr uint32_t foldz(const ProbeParams &, int) { return 0u; }
     __device__ static uint32_t mapb(const ProbeParams &P, int s) {      // packed group's map, or kNone
         return P.slot[s].prim_b >= 0 ? P.grp[P.slot[s].prim_b].map_addr : kNone;
     }
@@ -336,6 +339,12 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
         u[k] = 0u;
         e[k] = 0u;
         if (k >= nk || !lut) continue;
+        if (Sh::fold(P, s)) {          // base folded into the immediates: index with the key itself
+            const uint32_t x = static_cast<uint32_t>(v[k]);
+            const uint32_t cell = f == FMTEX ? x : __umulhi(x, Sh::cellmul(P, s));
+            e[k] = lds_u32(cell * P.c4 + Sh::foldb(P, s));
+            continue;
+        }
         u[k] = offset_of<Sh>(P, s, v[k]);
         if (f == FMT16) {
             const uint32_t cell = u[k] >> Sh::s1(P, s);
@@ -352,7 +361,8 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
         for (int k = 0; k < 4; ++k) {
             if (k >= nk) continue;
             const uint32_t x = e[k];
-            const uint32_t zz = u[k] * P.slot[s].t1_mul + Sh::t1ones(P, s);
+            const uint32_t zz = Sh::fold(P, s) ? static_cast<uint32_t>(v[k]) * P.slot[s].t1_mul + Sh::foldz(P, s)
+                                               : u[k] * P.slot[s].t1_mul + Sh::t1ones(P, s);
             const uint32_t lo = x & Sh::t1dmask(P, s);
             uint32_t inc = 1u;
             if (Sh::packs(P, s))
@@ -364,6 +374,7 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (k >= nk || !(e[k] & sp)) continue;
+                if (Sh::fold(P, s)) u[k] = offset_of<Sh>(P, s, v[k]);
                 const uint4 r = g_smem[e[k] & Sh::t1dmask(P, s)];
                 if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
                     const uint32_t c1 = u[k] > r.y, c2 = u[k] > r.z, c3 = u[k] > r.w;
