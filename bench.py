@@ -274,9 +274,13 @@ def main():
         "latency_ms": {"p50": nearest_rank(lat, 0.5), "p99": nearest_rank(lat, 0.99), "kind": "wall, per gace_probe"},
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "probe_kernel",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "gace_jit_probe (plan-specialised probe kernel)",
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_scanned},
+                     "algorithmic_bytes_per_launch": bytes_scanned,
+                     "note": "HBM roofline of the north-star target; the measured limiter is instruction "
+                             "issue / shared-memory pipe (profiles/r01_ncu_C5.md), a read-only scan of the "
+                             "same columns runs at ~8 TB/s"},
         "gpu_launches": launches,
         "clocks": clk,
     }
