@@ -240,6 +240,10 @@ struct SlotPlan {
     // layout
     uint32_t lut_idx = 0, l2_idx = 0, lst_idx = 0, hist_w = kNone, hll_idx = kNone, bps_off = 0;
     uint32_t pre = 0, pre_stride = 1;  // finalize: bucket-count prefix of this column
+    // HLL by presence bitmap (gace_plan.h SlotParams::bm_addr)
+    bool bm = false;
+    int64_t bm_base = 0;
+    uint32_t bm_words = 0, bm_w = kNone, bm_goff = 0, hll_out = 0;
 };
 
 uint32_t ceil_log2(uint64_t x) {
@@ -379,6 +383,7 @@ struct Plan {
     std::vector<uint8_t> image;        // shared-memory image (tables + maps)
     uint32_t acc_idx = 0, acc_words = 0, hll_off = 0, hll_bytes = 0, smem_bytes = 0;
     uint32_t pre_words = 0;
+    uint32_t bm_gwords = 0;            // merged presence bitmaps (u32 words in g_bm)
     std::vector<DirectPair> direct;
     std::vector<FinJob> jobs;
     std::vector<FinPred> fpreds;
@@ -396,9 +401,9 @@ void dump_plan(const Plan &pl) {
         size_t special = 0;
         for (uint32_t c : S.l1) special += (c & (S.fmt == FMT1T ? t1_special(S.s1) : kSpecial)) ? 1 : 0;
         fprintf(stderr, "slot %zu col %d dt %d mode %d fmt %d s1 %u sb %u nb %u cells %zu special %zu (%.2f%%) l2 %zu lst %zu "
-                "hll %d hist_grp %d prim_b %d span %llu\n", i, S.col, S.dtype, (int)S.mode, (int)S.fmt, S.s1, S.sb, S.nb,
+                "hll %d%s hist_grp %d prim_b %d span %llu\n", i, S.col, S.dtype, (int)S.mode, (int)S.fmt, S.s1, S.sb, S.nb,
                 S.l1.size(), special, S.l1.empty() ? 0.0 : 100.0 * special / S.l1.size(), S.l2.size(), S.lst.size(),
-                (int)S.has_hll, S.hist_grp, S.prim_b, (unsigned long long)((uint64_t)S.dh - (uint64_t)S.dl));
+                (int)S.has_hll, S.bm ? " (bitmap)" : "", S.hist_grp, S.prim_b, (unsigned long long)((uint64_t)S.dh - (uint64_t)S.dl));
     }
     for (size_t g = 0; g < pl.groups.size(); ++g) {
         const Group &G = pl.groups[g];
@@ -650,7 +655,34 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (!build_lut(S, span_of(S), s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
 
-    // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] | hll
+    // ---- HLL mode per column: a presence bitmap (one bit per value of a small int32 domain;
+    // the finalize hashes each present value once) instead of hashing every key, when it
+    // fits where the u32 registers were budgeted (exact: registers depend only on the set
+    // of distinct kept values).  Exact-cell columns keep their per-cell (index, rank).
+    {
+        size_t used = fixed;
+        for (auto &S : pl.slots)
+            if (S.mode == MODE_LUT) used += lut_bytes(S);
+        for (auto &S : pl.slots) {
+            if (!S.has_hll || S.dtype != GACE_I32 || t->host || getenv("GACE_NO_BITMAP")) continue;
+            if (S.mode == MODE_LUT && S.fmt == FMTEX) continue;
+            const int64_t base = (int64_t)((uint64_t)S.dl & ~31ull);
+            const uint64_t words = (((uint64_t)S.dh - (uint64_t)base) >> 5) + 1;
+            if (words > 32768) continue;                        // <= 128 KB
+            // zeroing and merging the bitmap costs ~words per CTA: worth it when every CTA
+            // scans many rows per bitmap word (C4: 200M rows, 2K words; not C1's 1M rows)
+            if (t->nrows < 32ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
+            const size_t bytes = 4 * words;
+            if (bytes > 4ull * kHllM && used + bytes - 4ull * kHllM > kSmemBudget) continue;
+            used = used + bytes - 4ull * kHllM;
+            S.bm = true;
+            S.bm_base = base;
+            S.bm_words = (uint32_t)words;
+        }
+    }
+
+    // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] |
+    //      presence bitmaps | hll registers
     uint32_t w = 0;    // u32 cursor
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
@@ -685,15 +717,27 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     w += (uint32_t)ndirect;
     w = (w + 3) & ~3u;
     pl.acc_words = w - pl.acc_idx;
+    uint32_t gbm = 0;
+    for (auto &S : pl.slots) {
+        if (!S.bm) continue;
+        S.bm_w = w;
+        w += S.bm_words;
+        S.bm_goff = gbm;
+        gbm += (S.bm_words + 3) & ~3u;
+    }
+    pl.bm_gwords = gbm;
+    w = (w + 3) & ~3u;
     pl.hll_off = w * 4;
-    uint32_t nh = 0;
+    uint32_t nh = 0, nreg = 0;
     for (auto &S : pl.slots) {
         if (!S.has_hll) continue;
-        S.hll_idx = w + nh * kHllM;
-        ++nh;
+        S.hll_out = nh++;
+        if (S.bm) continue;
+        S.hll_idx = w + nreg * kHllM;
+        ++nreg;
     }
     pl.hll_bytes = nh * kHllM;
-    pl.smem_bytes = (uint32_t)align16(pl.hll_off + 4 * pl.hll_bytes);
+    pl.smem_bytes = (uint32_t)align16(pl.hll_off + 4ull * nreg * kHllM);
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
 
@@ -843,6 +887,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.mode = S.has_preds ? S.mode : (uint8_t)MODE_NOPRED;
         Q.has_hll = S.has_hll ? 1 : 0;
         Q.hll_idx = S.hll_idx;
+        Q.bm_addr = S.bm ? 4 * S.bm_w : kNone;
+        Q.bm_words = S.bm_words;
+        Q.bm_goff = S.bm_goff;
+        Q.bm_base = S.bm_base;
+        Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
         Q.prim_b = (int8_t)S.prim_b;
         Q.base = S.base;
@@ -1146,6 +1195,11 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
     slot_u32("lutb", [](const SlotParams &Q) { return 4 * Q.lut_w; });
     slot_u32("histb", [](const SlotParams &Q) { return Q.hist_addr; });
     slot_u32("hllw", [](const SlotParams &Q) { return Q.hll_idx; });
+    o += "  __device__ static constexpr bool hllbm(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].bm_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
+    slot_u32("bmaddr", [](const SlotParams &Q) { return Q.bm_addr; });
+    slot_u32("bmbase", [](const SlotParams &Q) { return (uint32_t)Q.bm_base; });
+    slot_u32("hllout", [](const SlotParams &Q) { return Q.hll_out; });
     slot_u32("sb", [](const SlotParams &Q) { return (uint32_t)Q.sb; });
     slot_u32("bmask", [](const SlotParams &Q) { return Q.bmask; });
     slot_u32("t1mul", [](const SlotParams &Q) { return Q.t1_mul; });
@@ -1284,7 +1338,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
 
     const int grid = t->sms;
-    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 16;   // + merged HLL bound registers
+    // + merged HLL bound registers + merged presence bitmaps
+    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 16;
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
@@ -1306,6 +1361,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
     P.g_acc = t->d_acc.as<unsigned long long>();
     P.g_hll_glob = t->d_acc.as<uint32_t>(8ull * pl.acc_words);
+    P.g_bm = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes);
     P.g_hll_part = t->d_part.as<uint8_t>();
     P.g_nsamp = t->d_nsamp.as<unsigned long long>();
     P.thr = threshold_of(sample_rate);
@@ -1415,8 +1471,19 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.npairs = npairs;
     F.out = t->d_out.as<unsigned long long>();
     F.out_regs = t->d_out.as<uint8_t>(align16(8 * out_words));
+    F.g_bm = P.g_bm;
+    F.nbm = 0;
+    for (auto &S : pl.slots) {
+        if (!S.bm) continue;
+        FinParams::BmJob &J = F.bm[F.nbm++];
+        J.goff = S.bm_goff;
+        J.words = S.bm_words;
+        J.out = S.hll_out;
+        J.is64 = 0;
+        J.base = S.bm_base;
+    }
     CUDA_TRY(launch_finalize(F, s));
-    g_launches += (F.njobs + F.hll_blocks ? 2 : 1);
+    g_launches += (F.njobs + F.hll_blocks ? 2 : 1) + (F.nbm ? 1 : 0);
     CUDA_TRY(cudaEventRecord(t->ev[3], s));
 
     if (t->has_dist && t->dist.nranks > 1) {

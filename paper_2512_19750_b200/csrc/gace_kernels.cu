@@ -107,6 +107,34 @@ __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
     }
 }
 
+// HLL registers of a presence-bitmap column (one block each): every present value hashed
+// once, p = 12 registers in shared memory, then its block of the output registers.  Same
+// hash and index/rank convention as the probe (fmix32 for int32 keys, DESIGN.md §2 step 6).
+__global__ void __launch_bounds__(1024) fin_bitmap_hll(const FinParams F) {
+    __shared__ uint32_t R[kHllM];
+    const FinParams::BmJob J = F.bm[blockIdx.x];
+    for (uint32_t i = threadIdx.x; i < kHllM; i += blockDim.x) R[i] = 0;
+    __syncthreads();
+    const uint32_t *bm = F.g_bm + J.goff;
+    for (uint32_t i = threadIdx.x; i < J.words; i += blockDim.x) {
+        uint32_t w = bm[i];
+        while (w) {
+            const uint32_t b = __ffs(w) - 1;
+            w &= w - 1;
+            uint32_t h = static_cast<uint32_t>(J.base + 32ll * i + b);
+            h ^= h >> 16;
+            h *= 0x85EBCA6BU;
+            h ^= h >> 13;
+            h *= 0xC2B2AE35U;
+            h ^= h >> 16;
+            atomicMax(R + (h >> (32 - kHllP)), __clz((h << kHllP) | (1u << (kHllP - 1))) + 1);
+        }
+    }
+    __syncthreads();
+    uint8_t *out = F.out_regs + (size_t)J.out * kHllM;
+    for (uint32_t i = threadIdx.x; i < kHllM; i += blockDim.x) out[i] = (uint8_t)R[i];
+}
+
 // count of buckets [lo, hi] from a bucket-count prefix P(b) = pre[b * stride]
 __device__ __forceinline__ unsigned long long iv(const unsigned long long *pre, uint32_t stride, uint32_t lo,
                                                  uint32_t hi) {
@@ -242,6 +270,11 @@ cudaError_t launch_finalize(const FinParams &F, cudaStream_t s) {
     const uint32_t blocks = F.njobs + F.hll_blocks;
     if (blocks) {
         fin_prefix<<<blocks, 1024, 0, s>>>(F);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (F.nbm) {                         // after fin_prefix wrote the register blocks
+        fin_bitmap_hll<<<F.nbm, 1024, 0, s>>>(F);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

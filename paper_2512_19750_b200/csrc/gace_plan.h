@@ -193,6 +193,15 @@ struct SlotParams {
     uint32_t t1_sp;         // special flag
     uint32_t t1_cutsh;      // cut flag >> t1_cutsh lands on bit sb
     uint32_t t1_cutmul;     // 2^(32 - t1_cutsh), or 0 when t1_cutsh = 0
+    // HLL by presence bitmap (small int32 domains): registers depend only on the set of
+    // distinct kept values, so the scan records the set (one bit per value) and the
+    // finalize hashes each present value once.  bm_addr = byte address of the CTA's bitmap
+    // (kNone: u32 registers at hll_idx instead), bit i <-> value bm_base + i.
+    uint32_t bm_addr;
+    uint32_t bm_words;
+    uint32_t bm_goff;       // word offset of this column's merged bitmap in g_bm
+    uint32_t hll_out;       // output register block (ascending HLL column order)
+    int64_t bm_base;        // multiple of 32
 };
 
 struct GroupParams {
@@ -230,6 +239,7 @@ struct ProbeParams {
     unsigned long long *g_acc;             // u64[acc_words], summed over CTAs (and launches)
     uint8_t *g_hll_part;                   // [CTA][hll_bytes] per-CTA register partials
     unsigned long long *g_nsamp;
+    uint32_t *g_bm;                        // merged presence bitmaps (OR over CTAs; zeroed per probe)
     uint32_t *g_hll_glob;                  // u32[hll_bytes]: registers merged across CTAs while the
                                            // scan runs (max; zeroed per probe) -> HLL skip bound
     uint64_t nrows;                        // rows in this launch
@@ -291,6 +301,13 @@ struct FinParams {
     uint32_t npairs;
     unsigned long long *out;    // [1 + npreds + npairs]: n_sampled, counts, joints
     uint8_t *out_regs;          // [hll_bytes]
+    // presence-bitmap HLL columns: registers from the merged bitmap (fin_bitmap_hll)
+    uint32_t nbm;
+    const uint32_t *g_bm;
+    struct BmJob {
+        uint32_t goff, words, out, is64;
+        int64_t base;
+    } bm[kMaxSlots];
 };
 
 }  // namespace gace

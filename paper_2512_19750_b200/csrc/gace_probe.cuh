@@ -199,6 +199,10 @@ struct RtShape {
     __device__ static uint32_t lutb(const ProbeParams &P, int s) { return 4 * P.slot[s].lut_w; }
     __device__ static uint32_t histb(const ProbeParams &P, int s) { return P.slot[s].hist_addr; }
     __device__ static uint32_t hllw(const ProbeParams &P, int s) { return P.slot[s].hll_idx; }
+    __device__ static bool hllbm(const ProbeParams &P, int s) { return P.slot[s].bm_addr != kNone; }
+    __device__ static uint32_t bmaddr(const ProbeParams &P, int s) { return P.slot[s].bm_addr; }
+    __device__ static uint32_t bmbase(const ProbeParams &P, int s) { return (uint32_t)P.slot[s].bm_base; }
+    __device__ static uint32_t hllout(const ProbeParams &P, int s) { return P.slot[s].hll_out; }
     __device__ static uint32_t sb(const ProbeParams &P, int s) { return P.slot[s].sb; }
     __device__ static uint32_t bmask(const ProbeParams &P, int s) { return P.slot[s].bmask; }
     __device__ static uint32_t t1mul(const ProbeParams &P, int s) { return P.slot[s].t1_mul; }
@@ -479,7 +483,26 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
     // which the rest of the loop leaves idle); survivors do a predicated ATOMS.MAX.
-    if (Sh::hll(P, s) && !(dbg & 8)) {
+    if (Sh::hll(P, s) && Sh::hllbm(P, s) && !(dbg & 8)) {
+        // presence bitmap: set the bit of each kept value (test first: after the first rows
+        // nearly every value is present, so the quad costs four loads and no atomics)
+        uint32_t wa[4], bit[4], need = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t u = static_cast<uint32_t>(v[k]) - Sh::bmbase(P, s);
+            wa[k] = (u >> 5) * P.c4 + Sh::bmaddr(P, s);
+            bit[k] = 1u << (u & 31u);
+            const bool kept_k = same ? keep != 0 : ((keep >> k) & 1u);
+            if (kept_k && !(lds_u32(wa[k]) & bit[k])) need |= 1u << k;
+            if (same) break;
+        }
+        if (need) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((need >> k) & 1u)
+                    asm volatile("red.shared.or.b32 [%0], %1;" :: "r"(sbase() + wa[k]), "r"(bit[k]) : "memory");
+        }
+    } else if (Sh::hll(P, s) && !(dbg & 8)) {
         uint32_t *R = sm + Sh::hllw(P, s);
         if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
             // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
@@ -667,8 +690,8 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
-                    if (Sh::active(P, s) && Sh::hll(P, s)) {
-                        const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 31u);
+                    if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s)) {
+                        const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
                         if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
                     }
                 __syncwarp();
@@ -724,8 +747,8 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                     for (int s = 0; s < NC; ++s)
-                        if (Sh::active(P, s) && Sh::hll(P, s)) {
-                            const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + (Sh::hllw(P, s) - P.hll_off / 4), s), 31u);
+                        if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s)) {
+                            const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
                             if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
                         }
                     __syncwarp();
@@ -773,14 +796,35 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         const uint32_t x = sm[P.acc_idx + i];
         if (x) atomicAdd(P.g_acc + i, (unsigned long long)x);
     }
-    if (P.hll_bytes) {   // u32 registers -> packed u8 partial of this CTA
-        const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(g_smem) + P.hll_off);
-        uint32_t *dst = reinterpret_cast<uint32_t *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes);
-        for (uint32_t i = threadIdx.x; i < P.hll_bytes / 4; i += blockDim.x) {
+#pragma unroll 1
+    for (int s = 0; s < NC; ++s) {
+        if (!Sh::active(P, s) || !Sh::hll(P, s)) continue;
+        if (Sh::hllbm(P, s)) {           // presence bitmap -> OR into the merged bitmap
+            const uint32_t *src = smem32() + Sh::bmaddr(P, s) / 4;
+            uint32_t *dst = P.g_bm + P.slot[s].bm_goff;
+            for (uint32_t i = threadIdx.x; i < P.slot[s].bm_words; i += blockDim.x)
+                if (src[i]) atomicOr(dst + i, src[i]);
+            continue;
+        }
+        // u32 registers -> packed u8 partial of this CTA (its output block; a bitmap
+        // column's block stays zero and is filled by fin_bitmap_hll)
+        const uint4 *src = reinterpret_cast<const uint4 *>(smem32() + Sh::hllw(P, s));
+        uint32_t *dst = reinterpret_cast<uint32_t *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes +
+                                                     (size_t)Sh::hllout(P, s) * kHllM);
+        for (uint32_t i = threadIdx.x; i < kHllM / 4; i += blockDim.x) {
             const uint4 q = src[i];
             uint32_t x = q.x | (q.y << 8) | (q.z << 16) | (q.w << 24);
             if (P.part_merge) x = __vmaxu4(x, dst[i]);   // later launch of a chunked probe
             dst[i] = x;
+        }
+    }
+    if (P.hll_bytes && !P.part_merge) {  // bitmap columns' blocks of the partial: zeros
+#pragma unroll 1
+        for (int s = 0; s < NC; ++s) {
+            if (!Sh::active(P, s) || !Sh::hll(P, s) || !Sh::hllbm(P, s)) continue;
+            uint32_t *dst = reinterpret_cast<uint32_t *>(P.g_hll_part + (size_t)blockIdx.x * P.hll_bytes +
+                                                         (size_t)Sh::hllout(P, s) * kHllM);
+            for (uint32_t i = threadIdx.x; i < kHllM / 4; i += blockDim.x) dst[i] = 0u;
         }
     }
     kept = __reduce_add_sync(0xFFFFFFFFu, kept);

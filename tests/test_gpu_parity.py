@@ -402,3 +402,16 @@ def test_full_size_shard_invariance(G):
             np.testing.assert_array_equal(whole.counts + comp.counts, np.full(len(P), whole.n_sampled, np.uint64))
     finally:
         t.detach()
+
+
+@pytest.mark.parametrize("name,nrows,rate", [("C4", 100_003, 1.0), ("C4", 80_001, 0.3), ("C1", 100_003, 1.0),
+                                             ("C1", 50_001, 0.37), ("C3", 200_002, 1.0)])
+def test_presence_bitmap_hll(G, oracle, monkeypatch, name, nrows, rate):
+    """HLL by presence bitmap (small int32 domains; the finalize hashes each present value)
+    forced at sizes where the planner would not pick it, generic and specialised kernels."""
+    monkeypatch.setenv("GACE_FORCE_BITMAP", "1")
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    for jit in ("0", "1"):
+        monkeypatch.setenv("GACE_JIT", jit)
+        _check(G, oracle, cols, w.preds, w.pairs, rate, 29, w.hll_cols)
