@@ -212,3 +212,70 @@ int oracle_sample_mask(uint64_t nrows, uint64_t row_offset, double rate, uint64_
         if (oracle_keep(rate, seed, row_offset + r)) bits[r / 64] |= 1ULL << (r % 64);
     return 0;
 }
+
+/*
+ * Candidate-set conjunction counts (§IV-H "Experiment D: Replacing Dynamic
+ * Sampling (Key-Only + Bitmask)", lines 250-270: M candidate predicate sets of K
+ * predicates each; SPEC.md evaluate_bitmasks: "per-set count = popcount of AND-ed
+ * bitmaps").  Over rows [0, nrows) of a shard whose first row has global id row_offset:
+ *   set_counts[m] = sum_r keep(r) * prod_{p in members(m)} pred_p(row r)
+ * members(m) = set_members[set_offsets[m] .. set_offsets[m+1]); an empty set counts every
+ * kept row.  Each member predicate is evaluated by its operator as written, per row and per
+ * set (no sharing, no bucketing).  Returns 0, or -1 on an invalid argument.
+ */
+int oracle_probe_sets(const void *const *cols, const int *dtypes, uint32_t ncols,
+                      uint64_t nrows, uint64_t row_offset,
+                      const or_pred *preds, uint32_t npreds,
+                      const uint32_t *set_offsets, const uint32_t *set_members, uint32_t nsets,
+                      double rate, uint64_t seed, int nthreads,
+                      uint64_t *n_sampled, uint64_t *set_counts) {
+    if (!(rate >= 0.0 && rate <= 1.0)) return -1;
+    if (ncols > 64) return -1;
+    for (uint32_t p = 0; p < npreds; p++)
+        if (preds[p].col >= ncols || preds[p].op > OR_BETWEEN) return -1;
+    if (nsets && set_offsets[0] != 0) return -1;
+    for (uint32_t m = 0; m < nsets; m++) {
+        if (set_offsets[m + 1] < set_offsets[m]) return -1;
+        for (uint32_t k = set_offsets[m]; k < set_offsets[m + 1]; k++)
+            if (set_members[k] >= npreds) return -1;
+    }
+    memset(set_counts, 0, sizeof(uint64_t) * nsets);
+    uint64_t total = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#else
+    nthreads = 1;
+#endif
+    int err = 0;
+#pragma omp parallel num_threads(nthreads) reduction(+ : total)
+    {
+        uint64_t *my = calloc(nsets ? nsets : 1, sizeof(uint64_t));
+        if (!my) {
+#pragma omp atomic write
+            err = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t rr = 0; rr < (int64_t)nrows; rr++) {
+                uint64_t r = (uint64_t)rr;
+                if (!oracle_keep(rate, seed, row_offset + r)) continue;
+                total += 1;
+                for (uint32_t m = 0; m < nsets; m++) {
+                    int all = 1;
+                    for (uint32_t k = set_offsets[m]; k < set_offsets[m + 1] && all; k++) {
+                        const or_pred *p = &preds[set_members[k]];
+                        all = oracle_pred(p, col_value(cols[p->col], dtypes[p->col], r));
+                    }
+                    my[m] += (uint64_t)all;
+                }
+            }
+#pragma omp critical
+            {
+                for (uint32_t m = 0; m < nsets; m++) set_counts[m] += my[m];
+            }
+        }
+        free(my);
+    }
+    if (err) return -1;
+    *n_sampled = total;
+    return 0;
+}

@@ -12,6 +12,9 @@ Three independent pieces, each following the paper's definitions
 * ``brute_probe`` -- the same definition as pure-Python loops over Python
   ints, for tiny tables.  It is written separately from the C scan so the two
   pin each other (tests/test_oracle_bruteforce.py).
+* ``probe_sets`` / ``brute_probe_sets`` -- candidate-set conjunction counts
+  (§IV-H Exp. D, lines 250-270), C scan and
+  pure-Python loops, pinned by tests/test_oracle_sets.py.
 * ``derive`` / ``ndv_est`` / ``gate`` -- the host-side double arithmetic:
   S_probe = count / n (reading L13), PCS = P(A,B) / (P(A) P(B)) in the literal
   Eq. 3 order (L14), HLL raw + linear-counting estimate (L5), drift D (Eq. 1)
@@ -87,6 +90,13 @@ def lib():
             ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32,
             ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
             ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_probe_sets.restype = ctypes.c_int
+        L.oracle_probe_sets.argtypes = [
+            ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int), ctypes.c_uint32,
+            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+            ctypes.c_double, ctypes.c_uint64, ctypes.c_int,
+            ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p]
         L.oracle_sample_mask.restype = ctypes.c_int
         L.oracle_sample_mask.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
                                          ctypes.c_uint64, ctypes.c_void_p]
@@ -155,6 +165,43 @@ def probe(columns: Sequence[np.ndarray], preds, pairs=None, rate: float = 1.0, s
     if rc != 0:
         raise OracleError("oracle_probe rejected its arguments")
     return int(n.value), counts[:len(P)], joints[:len(Q)], regs[:nh]
+
+
+def sets_csr(sets) -> tuple[np.ndarray, np.ndarray]:
+    """A list of member-index lists -> (offsets u32[M+1], members u32[...])."""
+    offs = [0]
+    mem: list[int] = []
+    for s in sets:
+        mem.extend(int(i) for i in s)
+        offs.append(len(mem))
+    return np.asarray(offs, dtype=np.uint32), np.asarray(mem, dtype=np.uint32)
+
+
+def probe_sets(columns: Sequence[np.ndarray], preds, sets, rate: float = 1.0, seed: int = 0,
+               row_offset: int = 0, nthreads: int = 0):
+    """C oracle of the candidate-set conjunction counts (§IV-H Exp. D, lines
+    250-270): set_counts[m] = #{kept r : every member predicate of set m holds on row r}.
+
+    ``sets``: list of member-index lists.  Returns (n_sampled, set_counts u64[M])."""
+    cols = [np.ascontiguousarray(c) for c in columns]
+    nrows = len(cols[0])
+    dtypes = [I32 if c.dtype == np.int32 else I64 for c in cols]
+    for c in cols:
+        if c.dtype not in (np.int32, np.int64) or len(c) != nrows:
+            raise OracleError("columns must be int32 / int64 of equal length")
+    P = _as_preds(preds)
+    offs, mem = sets_csr(sets)
+    out = np.zeros(max(len(sets), 1), dtype=np.uint64)
+    ptrs = (ctypes.c_void_p * len(cols))(*[c.ctypes.data for c in cols])
+    dt = (ctypes.c_int * len(cols))(*dtypes)
+    n = ctypes.c_uint64(0)
+    rc = lib().oracle_probe_sets(ptrs, dt, len(cols), nrows, row_offset,
+                                 P.ctypes.data if len(P) else None, len(P),
+                                 offs.ctypes.data, mem.ctypes.data if len(mem) else None, len(sets),
+                                 float(rate), seed & M64, nthreads, ctypes.byref(n), out.ctypes.data)
+    if rc != 0:
+        raise OracleError("oracle_probe_sets rejected its arguments")
+    return int(n.value), out[:len(sets)]
 
 
 def sample_mask(nrows: int, rate: float, seed: int, row_offset: int = 0) -> np.ndarray:
@@ -264,6 +311,25 @@ def brute_probe(columns: Sequence[Sequence[int]], dtypes: Sequence[int], preds, 
             idx, rank = py_hll_i32(x, hll_p) if dtypes[c] == I32 else py_hll_i64(x, hll_p)
             regs[k][idx] = max(regs[k][idx], rank)
     return n, counts, joints, regs
+
+
+def brute_probe_sets(columns: Sequence[Sequence[int]], preds, sets, rate: float = 1.0, seed: int = 0,
+                     row_offset: int = 0):
+    """Pure-Python conjunction counts (tiny tables only): written apart from the C scan so
+    the two pin each other."""
+    nrows = len(columns[0]) if columns else 0
+    P = [(int(p["col"]), int(p["op"]), int(p["flags"]), int(p["a"]), int(p["b"])) for p in preds] \
+        if isinstance(preds, np.ndarray) else list(preds)
+    n = 0
+    out = [0] * len(sets)
+    for r in range(nrows):
+        if not py_keep(rate, seed, row_offset + r):
+            continue
+        n += 1
+        for m, members in enumerate(sets):
+            out[m] += int(all(py_pred(P[i][1], P[i][2], P[i][3], P[i][4], int(columns[P[i][0]][r]))
+                              for i in members))
+    return n, out
 
 
 # ----------------------------------------------------------------------------- derive and gate
