@@ -54,6 +54,14 @@ def peaks():
 
 
 def describe(w) -> dict:
+    if w.sets:
+        ks = sorted(set(len(x) for x in w.sets))
+        return {"workload": f"{w.name}: {w.nrows:,} rows x {len(w.probed_cols)} key columns "
+                            f"({'/'.join(w.columns[c].dtype for c in w.probed_cols)}), {len(w.sets)} candidate sets "
+                            f"x K={'/'.join(map(str, ks))} predicates from a pool of {len(w.preds)} "
+                            f"(conjunction counts, PAPER.md Exp. D), sample rate {w.rate}",
+                "rows": w.nrows, "predicates": int(len(w.preds)), "sets": len(w.sets), "k": ks,
+                "sample_rate": w.rate, "bytes_per_row": w.bytes_per_row}
     return {"workload": f"{w.name}: {w.nrows:,} rows x {len(w.probed_cols)} key columns "
                         f"({'/'.join(w.columns[c].dtype for c in w.probed_cols)}), {len(w.preds)} predicates, "
                         f"{len(w.pairs)} pairs, HLL p=12 on {len(w.hll_cols)} columns, sample rate {w.rate}",
@@ -120,7 +128,10 @@ def oracle_rate(w, rows: int, threads: int = 0):
     from oracle import reference as R
     cols = [w.column(c, 0, rows).numpy() for c in range(len(w.columns))]
     t0 = time.perf_counter()
-    R.probe(cols, w.preds, w.pairs, rate=w.rate, seed=w.sample_seed, hll_cols=w.hll_cols, nthreads=threads)
+    if w.sets:
+        R.probe_sets(cols, w.preds, w.sets, rate=w.rate, seed=w.sample_seed, nthreads=threads)
+    else:
+        R.probe(cols, w.preds, w.pairs, rate=w.rate, seed=w.sample_seed, hll_cols=w.hll_cols, nthreads=threads)
     dt = time.perf_counter() - t0
     return rows / dt, dt, (threads or os.cpu_count())
 
@@ -207,6 +218,8 @@ def main():
         flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
 
     def step():
+        if w.sets:
+            return table.probe_sets(w.preds, w.sets, w.rate, w.sample_seed)
         return table.probe(w.preds, w.pairs, w.rate, w.sample_seed, w.hll_cols)
 
     for _ in range(args.warmup):
@@ -275,7 +288,8 @@ def main():
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "gace_jit_probe (plan-specialised probe kernel)",
+                     "kernel": ("sets_kernel (candidate-set conjunction kernel)" if w.sets
+                                else "gace_jit_probe (plan-specialised probe kernel)"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_scanned,
                      "note": "HBM roofline of the north-star target; the measured limiter is instruction "
@@ -286,7 +300,9 @@ def main():
     }
 
     # e2e: host-resident keys, H2D inside every step (pinned host memory)
-    if not args.no_e2e:
+    if w.sets:
+        out["e2e"] = None     # gace_probe_sets takes device tables only (include/gace.h)
+    elif not args.no_e2e:
         hcols = [c.cpu().pin_memory() if len(c) == nloc else c.cpu() for c in cols]
         htable = gace.Table(hcols, host=True, dist=dinfo, device=local, stream=stream)
         hstep = lambda: htable.probe(w.preds, w.pairs, w.rate, w.sample_seed, w.hll_cols)  # noqa: E731
@@ -318,7 +334,8 @@ def main():
         rows = calibrate_oracle_rows(w, budget_s=15.0)
         r, dt, cores = oracle_rate(w, rows)
         out["cpu_baseline"] = {"value": r, "unit": "rows/s", "cores": cores, "kind": "oracle",
-                               "sample": f"rows [0, {rows:,}) of {w.name} ({dt:.1f} s, all predicates/pairs/HLL)"}
+                               "sample": f"rows [0, {rows:,}) of {w.name} ({dt:.1f} s, "
+                                         f"{'all sets' if w.sets else 'all predicates/pairs/HLL'})"}
     table.detach()
     if rank == 0:
         print(json.dumps(out), flush=True)

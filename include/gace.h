@@ -151,6 +151,32 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds,
                        uint64_t *n_sampled, uint64_t *counts, uint64_t *joint_counts,
                        uint8_t *hll_regs);
 
+/*
+ * Candidate-set conjunction counts (§IV-H "Experiment D: Replacing Dynamic
+ * Sampling (Key-Only + Bitmask)", lines 250-270: M candidate sets of K predicates; SPEC.md
+ * evaluate_bitmasks: "per-set count = popcount of AND-ed bitmaps").
+ *   preds[npreds]                  host array, validated as for gace_probe
+ *   set_offsets[nsets + 1]         CSR offsets into set_members (set_offsets[0] == 0,
+ *                                  non-decreasing); set m = set_members[off[m] .. off[m+1])
+ *   set_members[set_offsets[nsets]] predicate indices (< npreds); duplicates allowed;
+ *                                  an empty set holds on every row
+ *   sample_rate, seed              the sample of gace_probe (same rows for the same rate/seed)
+ * Outputs (host, caller-allocated; merged over ranks when attached with dist):
+ *   *n_sampled                     number of kept rows
+ *   set_counts[nsets]              #{kept r : every member predicate of set m holds on row r}
+ * Limits: nsets <= GACE_MAX_SETS, members <= GACE_MAX_SET_MEMBERS (GACE_EUNSUPPORTED
+ * beyond); members on at most 8 distinct columns; device tables only (GACE_EUNSUPPORTED
+ * for host tables); the plan must fit one CTA's shared memory (GACE_EUNSUPPORTED).
+ * Synchronous; one call in flight per handle; collective over ranks with dist.
+ * gace_last_timing reports it like a probe (scan_ms = the set kernel).
+ */
+#define GACE_MAX_SETS 256
+#define GACE_MAX_SET_MEMBERS 65536
+gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npreds,
+                            const uint32_t *set_offsets, const uint32_t *set_members, uint32_t nsets,
+                            double sample_rate, uint64_t seed, uint64_t *n_sampled,
+                            uint64_t *set_counts);
+
 /* Test hook: the deterministic sample mask of this shard's rows, bit-packed:
  * bit (r % 64) of bits[r / 64] = keep(row_offset + r); bits has ceil(nrows_local/64)
  * words (host).  Device tables only.                                               */

@@ -18,8 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["gace_kernels.cu", "gace_host.cpp", "gace_jit.cpp"]
-HEADERS = ["gace_plan.h", "gace_kernels.h", "gace_probe.cuh", "gace_jit.h"]
+SOURCES = ["gace_kernels.cu", "gace_sets.cu", "gace_host.cpp", "gace_jit.cpp"]
+HEADERS = ["gace_plan.h", "gace_kernels.h", "gace_probe.cuh", "gace_jit.h", "gace_sets.h"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

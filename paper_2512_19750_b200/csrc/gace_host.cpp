@@ -31,6 +31,7 @@
 #include "gace_jit.h"
 #include "gace_kernels.h"
 #include "gace_plan.h"
+#include "gace_sets.h"
 
 using namespace gace;
 
@@ -166,6 +167,11 @@ struct gace_table {
     std::string plan_key;
     std::shared_ptr<void> plan;
     size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0;
+    // candidate-set probe (gace_probe_sets): plan cache and buffers
+    std::string sets_key;
+    std::shared_ptr<void> sets_plan;
+    DevBuf d_sets_img, d_sets_out;
+    HostBuf h_sets_img, h_sets_out;
 };
 
 namespace {
@@ -1230,6 +1236,149 @@ int jit_mode() {
 
 // ====================================================================== C-ABI
 
+// ------------------------------------------------------------------ candidate sets
+
+namespace {
+
+// Operator as written (DESIGN.md §2 step 4), used to evaluate each member predicate on a
+// bucket's representative value: independent of the interval normalisation that places
+// the breakpoints, so a breakpoint slip shows up as a parity failure, not as agreement.
+bool eval_pred(const gace_pred &p, int64_t v) {
+    bool r;
+    switch (p.op) {
+        case GACE_EQ: r = v == p.a; break;
+        case GACE_LT: r = v < p.a; break;
+        case GACE_LE: r = v <= p.a; break;
+        case GACE_GT: r = v > p.a; break;
+        case GACE_GE: r = v >= p.a; break;
+        default: r = p.a <= v && v <= p.b;
+    }
+    return (p.flags & GACE_PRED_NEGATE) ? !r : r;
+}
+
+struct SetsPlan {
+    SetsParams P{};
+    std::vector<uint32_t> cols;        // table column of each slot
+    std::vector<uint8_t> image;        // cells | breakpoints | sat masks
+    bool i64 = false;
+    uint64_t bytes_per_row = 0;
+};
+
+constexpr size_t kSetsSmemSoft = 100 * 1024;   // two CTAs per SM when the plan fits
+constexpr size_t kSetsSmemHard = 200 * 1024;
+
+// Planner of gace_probe_sets (DESIGN.md §6 "Candidate sets").  For each probed column:
+// sorted breakpoints of its member predicates' intervals clipped to the column domain
+// (every predicate is constant on each bucket), sat[b] = bitmask of the sets all of whose
+// members on this column hold on bucket b, and a cell table over the domain (cell word =
+// first bucket of the cell | breakpoints inside << 20) sized to the shared-memory budget.
+gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const uint32_t *offs,
+                           const uint32_t *mem, uint32_t nsets, SetsPlan &out) {
+    const uint32_t W = nsets <= 32 ? 1 : nsets <= 64 ? 2 : nsets <= 128 ? 4 : 8;
+    std::map<uint32_t, uint32_t> slot_of;      // table column -> slot
+    for (uint32_t m = 0; m < nsets; ++m)
+        for (uint32_t k = offs[m]; k < offs[m + 1]; ++k) {
+            const uint32_t c = preds[mem[k]].col;
+            if (!slot_of.count(c)) {
+                if (slot_of.size() == (size_t)kSetsMaxCols)
+                    return fail(GACE_EUNSUPPORTED, "candidate sets reference more than 8 columns");
+                const uint32_t sl = (uint32_t)slot_of.size();
+                slot_of[c] = sl;
+            }
+        }
+    const uint32_t ns = (uint32_t)slot_of.size();
+    out.cols.assign(ns, 0);
+    for (auto &kv : slot_of) out.cols[kv.second] = kv.first;
+    std::vector<std::vector<uint64_t>> bps(ns);        // offsets t - dlo, sorted, unique
+    std::vector<std::vector<uint32_t>> sat(ns);
+    size_t fixed = 0;
+    for (uint32_t sl = 0; sl < ns; ++sl) {
+        const uint32_t c = out.cols[sl];
+        const int64_t dl = t->dlo[c], dh = t->dhi[c];
+        std::vector<int64_t> T;
+        for (uint32_t m = 0; m < nsets; ++m)
+            for (uint32_t k = offs[m]; k < offs[m + 1]; ++k)
+                if (preds[mem[k]].col == c) add_breakpoints(clip(op_interval(preds[mem[k]]), dl, dh), dl, dh, T);
+        std::sort(T.begin(), T.end());
+        T.erase(std::unique(T.begin(), T.end()), T.end());
+        const uint32_t nb = (uint32_t)T.size() + 1;
+        if (nb >= (1u << kSetsCellB0Bits)) return fail(GACE_EUNSUPPORTED, "too many breakpoints on one column");
+        for (int64_t x : T) bps[sl].push_back((uint64_t)x - (uint64_t)dl);
+        sat[sl].assign((size_t)nb * W, 0xFFFFFFFFu);
+        for (uint32_t b = 0; b < nb; ++b) {
+            const int64_t rep = b == 0 ? dl : T[b - 1];       // every value of bucket b behaves alike
+            for (uint32_t m = 0; m < nsets; ++m)
+                for (uint32_t k = offs[m]; k < offs[m + 1]; ++k) {
+                    const gace_pred &p = preds[mem[k]];
+                    if (p.col == c && !eval_pred(p, rep)) {
+                        sat[sl][(size_t)b * W + m / 32] &= ~(1u << (m % 32));
+                        break;
+                    }
+                }
+        }
+        fixed += 8 * bps[sl].size() + 4 * sat[sl].size() + 16;
+    }
+    if (fixed > kSetsSmemHard) return fail(GACE_EUNSUPPORTED, "candidate-set plan exceeds shared memory");
+    const size_t budget = fixed + 4096 * (size_t)ns <= kSetsSmemSoft ? kSetsSmemSoft : kSetsSmemHard;
+    const size_t cell_words = ns ? (budget - fixed) / 4 / ns : 0;     // per slot
+    std::vector<std::vector<uint32_t>> cells(ns);
+    for (uint32_t sl = 0; sl < ns; ++sl) {
+        const uint32_t c = out.cols[sl];
+        const uint64_t span = (uint64_t)t->dhi[c] - (uint64_t)t->dlo[c];
+        const std::vector<uint64_t> &B = bps[sl];
+        const uint64_t want = std::min<uint64_t>(cell_words, std::max<uint64_t>(64ull * (B.size() + 1), 1024));
+        uint32_t sh = 0;
+        while (sh < 63 && (span >> sh) >= want) ++sh;
+        for (;; --sh) {                       // finer cells while a cell holds too many breakpoints
+            const uint64_t nc = (span >> sh) + 1;
+            if (nc > cell_words) return fail(GACE_EUNSUPPORTED, "candidate-set cells exceed shared memory");
+            std::vector<uint32_t> cw(nc);
+            size_t i = 0;
+            bool ok = true;
+            for (uint64_t cell = 0; cell < nc; ++cell) {
+                const uint64_t cs = cell << sh;
+                while (i < B.size() && B[i] < cs) ++i;
+                size_t e = i;
+                const uint64_t ce_minus1 = cs + ((sh >= 64) ? ~0ull : ((1ull << sh) - 1));   // inclusive end
+                while (e < B.size() && B[e] <= ce_minus1) ++e;
+                if (e - i > kSetsCellNMax) { ok = false; break; }
+                cw[cell] = (uint32_t)i | ((uint32_t)(e - i) << kSetsCellB0Bits);
+            }
+            if (ok) { cells[sl].swap(cw); out.P.col[sl].shift = sh; break; }
+            if (sh == 0) return fail(GACE_EUNSUPPORTED, "candidate-set cell overflow");
+        }
+    }
+    // image: cells (u32) | breakpoints (u64, 8-aligned) | sat (u32)
+    size_t w32 = 0;
+    for (uint32_t sl = 0; sl < ns; ++sl) { out.P.col[sl].cell_off = (uint32_t)w32; w32 += cells[sl].size(); }
+    w32 = (w32 + 1) & ~size_t(1);
+    size_t w64 = w32 / 2;
+    for (uint32_t sl = 0; sl < ns; ++sl) { out.P.col[sl].bps_off = (uint32_t)w64; w64 += bps[sl].size(); }
+    w32 = 2 * w64;
+    for (uint32_t sl = 0; sl < ns; ++sl) { out.P.col[sl].sat_off = (uint32_t)w32; w32 += sat[sl].size(); }
+    const size_t bytes = std::max<size_t>(align16(4 * w32), 16);
+    if (bytes > kSetsSmemHard) return fail(GACE_EUNSUPPORTED, "candidate-set plan exceeds shared memory");
+    out.image.assign(bytes, 0);
+    uint32_t *i32 = reinterpret_cast<uint32_t *>(out.image.data());
+    uint64_t *i64p = reinterpret_cast<uint64_t *>(out.image.data());
+    for (uint32_t sl = 0; sl < ns; ++sl) {
+        std::copy(cells[sl].begin(), cells[sl].end(), i32 + out.P.col[sl].cell_off);
+        std::copy(bps[sl].begin(), bps[sl].end(), i64p + out.P.col[sl].bps_off);
+        std::copy(sat[sl].begin(), sat[sl].end(), i32 + out.P.col[sl].sat_off);
+        const uint32_t c = out.cols[sl];
+        out.P.col[sl].dlo = t->dlo[c];
+        out.P.col[sl].is64 = t->dtypes[c] == GACE_I64 ? 1u : 0u;
+        out.i64 |= t->dtypes[c] == GACE_I64;
+        out.bytes_per_row += t->dtypes[c] == GACE_I64 ? 8 : 4;
+    }
+    out.P.ncols = ns;
+    out.P.W = W;
+    out.P.image_u4 = (uint32_t)(bytes / 16);
+    return GACE_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char *gace_last_error(void) { return g_err.c_str(); }
@@ -1279,6 +1428,7 @@ gace_status gace_table_detach(gace_table *t) {
     t->d_plan.release(); t->d_acc.release(); t->d_pre.release(); t->d_part.release();
     t->d_out.release(); t->d_nsamp.release(); t->d_mask.release();
     t->h_plan.release(); t->h_out.release();
+    t->d_sets_img.release(); t->d_sets_out.release(); t->h_sets_img.release(); t->h_sets_out.release();
     if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
     if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
     t->magic = 0;
@@ -1523,6 +1673,108 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     T.jit = jit_used;
     T.jit_compile_ms = jit_ms;
     T.bytes_scanned = t->nrows * bytes_per_row;
+    return GACE_OK;
+}
+
+gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npreds, const uint32_t *set_offsets,
+                            const uint32_t *set_members, uint32_t nsets, double sample_rate, uint64_t seed,
+                            uint64_t *n_sampled, uint64_t *set_counts) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(t->mu);
+    st = validate_batch(t, preds, npreds, nullptr, 0, sample_rate, 0, GACE_HLL_P);
+    if (st) return st;
+    if (!n_sampled) return fail(GACE_EINVAL, "n_sampled is NULL");
+    if (nsets > GACE_MAX_SETS) return fail(GACE_EUNSUPPORTED, "nsets > 256");
+    if (nsets && (!set_offsets || !set_counts)) return fail(GACE_EINVAL, "set_offsets / set_counts is NULL");
+    if (nsets && set_offsets[0] != 0) return fail(GACE_EINVAL, "set_offsets[0] must be 0");
+    for (uint32_t m = 0; m < nsets; ++m)
+        if (set_offsets[m + 1] < set_offsets[m]) return fail(GACE_EINVAL, "set_offsets must be non-decreasing");
+    const uint32_t nmem = nsets ? set_offsets[nsets] : 0;
+    if (nmem > GACE_MAX_SET_MEMBERS) return fail(GACE_EUNSUPPORTED, "more than 65536 set members");
+    if (nmem && !set_members) return fail(GACE_EINVAL, "set_members is NULL");
+    for (uint32_t k = 0; k < nmem; ++k)
+        if (set_members[k] >= npreds) return fail(GACE_EINVAL, "set member index out of range");
+    if (t->host) return fail(GACE_EUNSUPPORTED, "gace_probe_sets needs a device table");
+
+    CUDA_TRY(cudaSetDevice(t->device));
+    CUDA_TRY(cudaStreamSynchronize(t->stream));
+    std::string key;
+    key.append(reinterpret_cast<const char *>(&nsets), 4);
+    if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
+    if (nsets) key.append(reinterpret_cast<const char *>(set_offsets), 4ull * (nsets + 1));
+    if (nmem) key.append(reinterpret_cast<const char *>(set_members), 4ull * nmem);
+    cudaStream_t s = t->stream;
+    CUDA_TRY(cudaEventRecord(t->ev[0], s));
+    if (!t->sets_plan || key != t->sets_key) {
+        auto fresh = std::make_shared<SetsPlan>();
+        st = make_sets_plan(t, preds, set_offsets, set_members, nsets, *fresh);
+        if (st) return st;
+        const size_t n = fresh->image.size();
+        if (t->h_sets_img.ensure(n) != cudaSuccess || t->d_sets_img.ensure(n) != cudaSuccess)
+            return fail(GACE_ENOMEM, "candidate-set plan buffers");
+        memcpy(t->h_sets_img.p, fresh->image.data(), n);
+        CUDA_TRY(cudaMemcpyAsync(t->d_sets_img.p, t->h_sets_img.p, n, cudaMemcpyHostToDevice, s));
+        t->sets_plan = fresh;
+        t->sets_key.swap(key);
+    }
+    const SetsPlan &pl = *static_cast<const SetsPlan *>(t->sets_plan.get());
+    const size_t out_words = 1 + 32ull * pl.P.W;          // [n_sampled, counts of W*32 sets]
+    if (t->d_sets_out.ensure(8 * out_words) != cudaSuccess || t->h_sets_out.ensure(8 * out_words) != cudaSuccess)
+        return fail(GACE_ENOMEM, "candidate-set scratch");
+    CUDA_TRY(cudaMemsetAsync(t->d_sets_out.p, 0, 8 * out_words, s));
+    CUDA_TRY(cudaEventRecord(t->ev[1], s));
+    SetsParams P = pl.P;
+    P.image = t->d_sets_img.as<const uint4>();
+    P.g_nsamp = t->d_sets_out.as<unsigned long long>();
+    P.g_counts = t->d_sets_out.as<unsigned long long>(8);
+    P.seed = seed;
+    P.thr = threshold_of(sample_rate);
+    const bool sample = sample_rate < 1.0;
+    const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
+    const int grid = t->sms * (pl.image.size() <= kSetsSmemSoft ? 2 : 1);
+    // rows per launch: per-warp u32 counters and per-CTA u32 sums stay below 2^32
+    const uint64_t max_rows = 1ull << 33;
+    uint64_t launches = 0;
+    for (uint64_t r0 = 0; r0 < t->nrows; r0 += max_rows) {
+        const uint64_t n = std::min(max_rows, t->nrows - r0);
+        for (uint32_t sl = 0; sl < P.ncols; ++sl) {
+            const size_t w = pl.P.col[sl].is64 ? 8 : 4;
+            P.col[sl].ptr = static_cast<const char *>(t->cols[pl.cols[sl]]) + r0 * w;
+        }
+        P.nrows = n;
+        P.row0 = row_offset + r0;
+        CUDA_TRY(launch_sets(P, sample, pl.i64, grid, s));
+        ++launches;
+    }
+    g_launches += launches;
+    CUDA_TRY(cudaEventRecord(t->ev[2], s));
+    CUDA_TRY(cudaEventRecord(t->ev[3], s));
+    if (t->has_dist && t->dist.nranks > 1) {
+        Nccl *nc = nccl();
+        if (!nc) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
+        void *buf = t->d_sets_out.p;
+        if (nc->AllReduce(buf, buf, out_words, kNcclUint64, kNcclSum, t->comm, s))
+            return fail(GACE_ENCCL, "ncclAllReduce failed");
+    }
+    CUDA_TRY(cudaEventRecord(t->ev[4], s));
+    CUDA_TRY(cudaMemcpyAsync(t->h_sets_out.p, t->d_sets_out.p, 8 * out_words, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(t->ev[5], s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const uint64_t *ho = t->h_sets_out.as<uint64_t>();
+    *n_sampled = ho[0];
+    if (nsets) memcpy(set_counts, ho + 1, 8ull * nsets);
+
+    gace_timing &T = t->last;
+    T = gace_timing{};
+    float ms;
+    cudaEventElapsedTime(&ms, t->ev[0], t->ev[1]); T.plan_upload_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[1], t->ev[2]); T.scan_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[3], t->ev[4]); T.merge_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[4], t->ev[5]); T.d2h_ms = ms;
+    cudaEventElapsedTime(&ms, t->ev[0], t->ev[5]); T.total_ms = ms;
+    T.scan_launches = launches;
+    T.bytes_scanned = t->nrows * pl.bytes_per_row;
     return GACE_OK;
 }
 

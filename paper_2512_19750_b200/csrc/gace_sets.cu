@@ -1,0 +1,248 @@
+// gace_sets.cu -- sm_100a kernel of the candidate-set probe (gace_probe_sets).
+//
+// PAPER.md §IV-H Exp. D (lines 250-270): per candidate set m, the number of sampled rows on
+// which every member predicate holds.  One pass over the probed key columns (128-bit
+// non-allocating loads, each key read once); per row and column one cell lookup (+ a short
+// in-cell binary search on cells holding breakpoints) gives the bucket, and one shared-memory
+// load gives that bucket's set-satisfaction mask (gace_sets.h); the AND over the columns is
+// the row's set mask.  Counting: 5 bit-sliced planes per lane (a carry-save add per row),
+// flushed every 28 rows by a 32x32 warp bit-matrix transpose (5 shuffles) + popcount, so the
+// cost per row is independent of K and of M within a 32-set word, and there are no per-row
+// atomics.  No tensor cores: an integer scan, not a contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gace_sets.h"
+
+namespace gace {
+namespace {
+
+__device__ __forceinline__ uint64_t sets_mix64(uint64_t z) {   // SplitMix64 finaliser (DESIGN.md §2 step 1)
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ bool sets_keep(uint64_t seed, uint64_t thr, uint64_t g) {
+    return sets_mix64(seed + (g + 1) * 0x9E3779B97F4A7C15ULL) < thr;
+}
+
+__device__ __forceinline__ int4 ld_nc128(const void *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// #{i < n : bps[i] <= u} over sorted bps (branch-free binary search)
+__device__ __forceinline__ uint32_t count_le(const uint64_t *bps, uint32_t n, uint64_t u) {
+    uint32_t lo = 0;
+    while (n > 0) {
+        const uint32_t half = n >> 1;
+        const bool right = bps[lo + half] <= u;
+        lo = right ? lo + half + 1 : lo;
+        n = right ? n - half - 1 : half;
+    }
+    return lo;
+}
+
+// 32x32 bit-matrix transpose across the warp (recursive off-diagonal block swap):
+// on return, bit l of lane m's word = bit m of lane l's input word.
+__device__ __forceinline__ uint32_t warp_transpose(uint32_t x, uint32_t lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                           : s == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+    }
+    return x;
+}
+
+template <int W>
+__device__ __forceinline__ void flush(uint32_t (&pl)[W][5], uint32_t (&cnt)[W], uint32_t lane) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+            acc += static_cast<uint32_t>(__popc(warp_transpose(pl[j][p], lane))) << p;
+            pl[j][p] = 0u;
+        }
+        cnt[j] += acc;
+    }
+}
+
+}  // namespace
+
+template <int W, int NCM, bool I64, bool SAMPLE>
+__global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constant__ SetsParams P) {
+    extern __shared__ uint4 s_img[];
+    __shared__ uint32_t s_cnt[kSetsMaxWords * 32];
+    for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) s_img[i] = __ldg(P.image + i);
+    for (uint32_t i = threadIdx.x; i < W * 32; i += blockDim.x) s_cnt[i] = 0u;
+    __syncthreads();
+    const uint32_t *sm32 = reinterpret_cast<const uint32_t *>(s_img);
+    const uint64_t *sm64 = reinterpret_cast<const uint64_t *>(s_img);
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nfull = P.nrows / 4, nunits = (P.nrows + 3) / 4;   // unit nfull may be partial
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t pl[W][5], cnt[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        cnt[j] = 0u;
+#pragma unroll
+        for (int p = 0; p < 5; ++p) pl[j][p] = 0u;
+    }
+    uint32_t kept = 0;
+    int pend = 0;
+    // warp-uniform trip count (the flush is warp-collective)
+    for (uint64_t base = gw * 32; base < nunits; base += stride) {
+        const uint64_t u = base + lane;
+        uint32_t keep = 0;
+        if (u < nunits) {
+            keep = u < nfull ? 0xFu : (1u << (uint32_t)(P.nrows - 4 * nfull)) - 1u;
+            if (SAMPLE) {
+                const uint64_t g0 = P.row0 + 4 * u;
+                uint32_t kk = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) kk |= (sets_keep(P.seed, P.thr, g0 + k) ? 1u : 0u) << k;
+                keep &= kk;
+            }
+        }
+        kept += __popc(keep);
+        uint32_t x[4][W];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < W; ++j) x[k][j] = ((keep >> k) & 1u) ? 0xFFFFFFFFu : 0u;
+        if (keep) {
+            // every probed column's keys of the unit in flight before any is used
+            int4 r[NCM][I64 ? 2 : 1];
+#pragma unroll
+            for (int c = 0; c < NCM; ++c) {
+                if (c >= (int)P.ncols) break;
+                const char *p = static_cast<const char *>(P.col[c].ptr);
+                const bool w64 = I64 && P.col[c].is64;
+                if (u < nfull) {
+                    if (!w64) {
+                        r[c][0] = ld_nc128(p + u * 16);
+                    } else {
+                        r[c][0] = ld_nc128(p + u * 32);
+                        r[c][I64 ? 1 : 0] = ld_nc128(p + u * 32 + 16);
+                    }
+                } else {   // partial last unit: missing rows repeat row 0 (a valid key; keep bit 0)
+                    const uint32_t nk = (uint32_t)(P.nrows - 4 * nfull);
+                    if (!w64) {
+                        const int32_t *q = reinterpret_cast<const int32_t *>(p) + 4 * u;
+                        const int32_t a = q[0], b = nk > 1 ? q[1] : a, d = nk > 2 ? q[2] : a;
+                        r[c][0] = make_int4(a, b, d, a);
+                    } else {
+                        const long long *q = reinterpret_cast<const long long *>(p) + 4 * u;
+                        const long long a = q[0], b = nk > 1 ? q[1] : a, d = nk > 2 ? q[2] : a;
+                        r[c][0] = make_int4((int)a, (int)(a >> 32), (int)b, (int)(b >> 32));
+                        r[c][I64 ? 1 : 0] = make_int4((int)d, (int)(d >> 32), (int)a, (int)(a >> 32));
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NCM; ++c) {
+                if (c >= (int)P.ncols) break;
+                const SetsCol &C = P.col[c];
+                const bool w64 = I64 && C.is64;
+                uint64_t uo[4];
+                if (!w64) {
+                    const int4 q = r[c][0];
+                    const uint32_t d = static_cast<uint32_t>(C.dlo);
+                    uo[0] = static_cast<uint32_t>(q.x) - d;
+                    uo[1] = static_cast<uint32_t>(q.y) - d;
+                    uo[2] = static_cast<uint32_t>(q.z) - d;
+                    uo[3] = static_cast<uint32_t>(q.w) - d;
+                } else {
+                    const int4 a = r[c][0], b = r[c][I64 ? 1 : 0];
+                    const uint64_t d = static_cast<uint64_t>(C.dlo);
+                    uo[0] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.y)) << 32) | static_cast<uint32_t>(a.x)) - d;
+                    uo[1] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.w)) << 32) | static_cast<uint32_t>(a.z)) - d;
+                    uo[2] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.y)) << 32) | static_cast<uint32_t>(b.x)) - d;
+                    uo[3] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.w)) << 32) | static_cast<uint32_t>(b.z)) - d;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t cell = w64 ? static_cast<uint32_t>(uo[k] >> C.shift)
+                                              : static_cast<uint32_t>(uo[k]) >> C.shift;
+                    const uint32_t cw = sm32[C.cell_off + cell];
+                    uint32_t b = cw & ((1u << kSetsCellB0Bits) - 1u);
+                    const uint32_t n = cw >> kSetsCellB0Bits;
+                    if (n) b += count_le(sm64 + C.bps_off + b, n, uo[k]);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) x[k][j] &= sm32[C.sat_off + b * W + j];
+                }
+            }
+        }
+        // carry-save add of the four row masks into the 5 bit planes (counts <= 28 < 32)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                uint32_t cy = x[k][j];
+#pragma unroll
+                for (int p = 0; p < 5; ++p) {
+                    const uint32_t t = pl[j][p] & cy;
+                    pl[j][p] ^= cy;
+                    cy = t;
+                }
+            }
+        pend += 4;
+        if (pend >= 28) {
+            flush<W>(pl, cnt, lane);
+            pend = 0;
+        }
+    }
+    if (pend) flush<W>(pl, cnt, lane);
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+        if (cnt[j]) atomicAdd(&s_cnt[j * 32 + lane], cnt[j]);
+    kept = __reduce_add_sync(0xFFFFFFFFu, kept);
+    if (lane == 0 && kept) atomicAdd(P.g_nsamp, (unsigned long long)kept);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < W * 32; i += blockDim.x)
+        if (s_cnt[i]) atomicAdd(P.g_counts + i, (unsigned long long)s_cnt[i]);
+}
+
+namespace {
+template <int W, int NCM, bool I64, bool SAMPLE>
+cudaError_t launch_t(const SetsParams &P, int grid, size_t smem, cudaStream_t s) {
+    auto k = sets_kernel<W, NCM, I64, SAMPLE>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kSetsThreads, smem, s>>>(P);
+    return cudaGetLastError();
+}
+
+template <int W, int NCM>
+cudaError_t launch_w(const SetsParams &P, bool sample, bool i64, int grid, size_t smem, cudaStream_t s) {
+    if (i64) return sample ? launch_t<W, NCM, true, true>(P, grid, smem, s) : launch_t<W, NCM, true, false>(P, grid, smem, s);
+    return sample ? launch_t<W, NCM, false, true>(P, grid, smem, s) : launch_t<W, NCM, false, false>(P, grid, smem, s);
+}
+
+template <int W>
+cudaError_t launch_nc(const SetsParams &P, bool sample, bool i64, int grid, size_t smem, cudaStream_t s) {
+    return P.ncols <= 4 ? launch_w<W, 4>(P, sample, i64, grid, smem, s) : launch_w<W, 8>(P, sample, i64, grid, smem, s);
+}
+}  // namespace
+
+cudaError_t launch_sets(const SetsParams &P, bool sample, bool i64, int grid, cudaStream_t s) {
+    const size_t smem = 16ull * P.image_u4;
+    switch (P.W) {
+        case 1: return launch_nc<1>(P, sample, i64, grid, smem, s);
+        case 2: return launch_nc<2>(P, sample, i64, grid, smem, s);
+        case 4: return launch_nc<4>(P, sample, i64, grid, smem, s);
+        case 8: return launch_nc<8>(P, sample, i64, grid, smem, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace gace

@@ -32,7 +32,7 @@ HLL_M = 1 << HLL_P
 PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
 PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
-EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe",
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
            "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
     L.gace_table_detach.argtypes = [vp]
     L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
     L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
+    L.gace_probe_sets.argtypes = [vp, vp, u32, vp, vp, u32, dbl, u64, ctypes.POINTER(u64), vp]
     L.gace_derive.argtypes = [u64, vp, u32, vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp]
     L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
     L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
@@ -273,6 +274,24 @@ class Table:
                                 int(seed) & ((1 << 64) - 1), mask, hll_p, ctypes.byref(n),
                                 counts.ctypes.data, joints.ctypes.data, regs.ctypes.data))
         return ProbeResult(int(n.value), counts[:len(P)], joints[:len(Q)], regs[:nh])
+
+    def probe_sets(self, preds, sets, sample_rate: float = 1.0, seed: int = 0):
+        """Candidate-set conjunction counts (gace_probe_sets; §IV-H Exp. D).
+        ``sets``: list of member-index lists.  Returns (n_sampled, u64[len(sets)])."""
+        P = as_preds(preds)
+        offs = [0]
+        mem: list[int] = []
+        for st in sets:
+            mem.extend(int(i) for i in st)
+            offs.append(len(mem))
+        O = np.asarray(offs, dtype=np.uint32)
+        M = np.asarray(mem if mem else [0], dtype=np.uint32)
+        out = np.zeros(max(len(sets), 1), dtype=np.uint64)
+        n = ctypes.c_uint64()
+        _check(lib().gace_probe_sets(self._h, _ptr(P), len(P), O.ctypes.data, M.ctypes.data, len(sets),
+                                     float(sample_rate), int(seed) & ((1 << 64) - 1), ctypes.byref(n),
+                                     out.ctypes.data))
+        return int(n.value), out[:len(sets)]
 
     def sample_mask(self, sample_rate: float, seed: int) -> np.ndarray:
         bits = np.zeros(max(1, (self.nrows + 63) // 64), dtype=np.uint64)

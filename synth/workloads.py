@@ -21,6 +21,8 @@ Shapes (DESIGN.md "Input recipe"):
   C5  TPC-H SF100 lineitem-shaped keys (600,037,902 rows), 256 BETWEEN
       predicates, 64 pairs over 4 column pairs, HLL on all 4, rate 1.
       ("C5_i64": orderkey and partkey stored as int64.)
+  D   Exp. D (§IV-H): C5's table, a 64-predicate pool, M=16 candidate
+      sets of K=16 members (conjunction counts; "D_m1_k16": M=1).
 """
 from __future__ import annotations
 
@@ -75,6 +77,7 @@ class Workload:
     sample_seed: int = 0
     ndv_hist: list[float] = field(default_factory=list)   # one per hll column
     s_est: list[float] = field(default_factory=list)      # optimizer S_est per predicate
+    sets: list[list[int]] = field(default_factory=list)   # candidate sets (member predicate indices)
 
     @property
     def hll_mask(self) -> int:
@@ -329,14 +332,48 @@ def make_c5(nrows: int = SF100_ROWS, data_seed: int = 5, pred_seed: int = 505,
     return w
 
 
+def make_d(nrows: int = SF100_ROWS, data_seed: int = 5, pred_seed: int = 606, m: int = 16,
+           k: int = 16) -> Workload:
+    """Exp. D shape (§IV-H: M candidate sets of K predicates; the
+    paper's largest point M=16, K=16) on the C5 lineitem table: a pool of 64 predicates (16
+    per column: GE at a low / LT at a high quantile, a wide BETWEEN, 13 NOT-BETWEEN narrow windows
+    at values drawn from the data, so a conjunction of 16 keeps a fair share of the rows) and
+    M sets of K members drawn from the pool, so sets share predicates."""
+    cols = lineitem_cols(data_seed, 100, nrows)
+    w = Workload("D" if (m, k) == (16, 16) else f"D_m{m}_k{k}", nrows, cols, _preds([]), _pairs([]), [])
+    g = np.random.default_rng(pred_seed)
+    rows = []
+    for c in range(4):
+        col = cols[c]
+        v = w.values_at(c, g.integers(0, nrows, size=16))
+        dom = col.hi - col.lo + 1
+        for j in range(16):
+            x = int(v[j])
+            if j == 0:
+                rows.append((c, GE, 0, col.lo + int(g.uniform(0.0, 0.15) * dom), 0))
+            elif j == 1:
+                rows.append((c, LT, 0, col.hi - int(g.uniform(0.0, 0.15) * dom), 0))
+            elif j == 2:
+                rows.append((c, BETWEEN, 0, col.lo + int(g.uniform(0.0, 0.1) * dom), col.hi - int(g.uniform(0.0, 0.1) * dom)))
+            else:
+                wd = _log_uniform_width(g, max(1, dom // 32))
+                rows.append((c, BETWEEN, NEGATE, x, x + wd - 1))
+    w.preds = _preds(rows)
+    w.sets = [sorted(int(i) for i in g.choice(len(rows), size=k, replace=False)) for _ in range(m)]
+    return w
+
+
 CONFIGS = {
     "C1": make_c1, "C2": make_c2, "C3": make_c3, "C4": make_c4, "C5": make_c5,
     "C3B": lambda nrows=100_000_000: make_c3(nrows, variant="B"),
     "C5_i64": lambda nrows=SF100_ROWS: make_c5(nrows, i64=True),
+    "D": make_d,
+    "D_m1_k16": lambda nrows=SF100_ROWS: make_d(nrows, m=1, k=16),
 }
 
 FULL_ROWS = {"C1": 1_000_000, "C2": SF10_ROWS, "C3": 100_000_000, "C3B": 100_000_000,
-             "C4": 200_000_000, "C5": SF100_ROWS, "C5_i64": SF100_ROWS}
+             "C4": 200_000_000, "C5": SF100_ROWS, "C5_i64": SF100_ROWS, "D": SF100_ROWS,
+             "D_m1_k16": SF100_ROWS}
 
 
 def get(name: str, nrows: int | None = None) -> Workload:
