@@ -1264,8 +1264,7 @@ struct SetsPlan {
     uint64_t bytes_per_row = 0;
 };
 
-constexpr size_t kSetsSmemSoft = 100 * 1024;   // two CTAs per SM when the plan fits
-constexpr size_t kSetsSmemHard = 200 * 1024;
+constexpr size_t kSetsSmemHard = 200 * 1024;   // one 1024-thread CTA per SM
 
 // Planner of gace_probe_sets (DESIGN.md §6 "Candidate sets").  For each probed column:
 // sorted breakpoints of its member predicates' intervals clipped to the column domain
@@ -1275,6 +1274,7 @@ constexpr size_t kSetsSmemHard = 200 * 1024;
 gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const uint32_t *offs,
                            const uint32_t *mem, uint32_t nsets, SetsPlan &out) {
     const uint32_t W = nsets <= 32 ? 1 : nsets <= 64 ? 2 : nsets <= 128 ? 4 : 8;
+    const bool fold = nsets <= 31;             // bit 31 of a cell word is free: masks in the cells
     std::map<uint32_t, uint32_t> slot_of;      // table column -> slot
     for (uint32_t m = 0; m < nsets; ++m)
         for (uint32_t k = offs[m]; k < offs[m + 1]; ++k) {
@@ -1319,14 +1319,14 @@ gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const ui
         fixed += 8 * bps[sl].size() + 4 * sat[sl].size() + 16;
     }
     if (fixed > kSetsSmemHard) return fail(GACE_EUNSUPPORTED, "candidate-set plan exceeds shared memory");
-    const size_t budget = fixed + 4096 * (size_t)ns <= kSetsSmemSoft ? kSetsSmemSoft : kSetsSmemHard;
-    const size_t cell_words = ns ? (budget - fixed) / 4 / ns : 0;     // per slot
+    const size_t cell_words = ns ? (kSetsSmemHard - fixed) / 4 / ns : 0;     // per slot
     std::vector<std::vector<uint32_t>> cells(ns);
     for (uint32_t sl = 0; sl < ns; ++sl) {
         const uint32_t c = out.cols[sl];
         const uint64_t span = (uint64_t)t->dhi[c] - (uint64_t)t->dlo[c];
         const std::vector<uint64_t> &B = bps[sl];
-        const uint64_t want = std::min<uint64_t>(cell_words, std::max<uint64_t>(64ull * (B.size() + 1), 1024));
+        // ~256 cells per bucket: few keys land in a cell holding a breakpoint
+        const uint64_t want = std::min<uint64_t>(cell_words, std::max<uint64_t>(256ull * (B.size() + 1), 1024));
         uint32_t sh = 0;
         while (sh < 63 && (span >> sh) >= want) ++sh;
         for (;; --sh) {                       // finer cells while a cell holds too many breakpoints
@@ -1343,6 +1343,7 @@ gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const ui
                 while (e < B.size() && B[e] <= ce_minus1) ++e;
                 if (e - i > kSetsCellNMax) { ok = false; break; }
                 cw[cell] = (uint32_t)i | ((uint32_t)(e - i) << kSetsCellB0Bits);
+                if (fold) cw[cell] = e == i ? sat[sl][i] & ~kSetsImpure : cw[cell] | kSetsImpure;
             }
             if (ok) { cells[sl].swap(cw); out.P.col[sl].shift = sh; break; }
             if (sh == 0) return fail(GACE_EUNSUPPORTED, "candidate-set cell overflow");
@@ -1373,6 +1374,7 @@ gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const ui
     }
     out.P.ncols = ns;
     out.P.W = W;
+    out.P.fold = fold ? 1u : 0u;
     out.P.image_u4 = (uint32_t)(bytes / 16);
     return GACE_OK;
 }
@@ -1732,7 +1734,7 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     P.thr = threshold_of(sample_rate);
     const bool sample = sample_rate < 1.0;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
-    const int grid = t->sms * (pl.image.size() <= kSetsSmemSoft ? 2 : 1);
+    const int grid = t->sms;
     // rows per launch: per-warp u32 counters and per-CTA u32 sums stay below 2^32
     const uint64_t max_rows = 1ull << 33;
     uint64_t launches = 0;

@@ -76,8 +76,95 @@ __device__ __forceinline__ void flush(uint32_t (&pl)[W][5], uint32_t (&cnt)[W], 
 
 }  // namespace
 
-template <int W, int NCM, bool I64, bool SAMPLE>
-__global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constant__ SetsParams P) {
+// Keys of unit u of column c (4 rows) into r (int64 columns: two 128-bit loads).
+template <bool I64>
+__device__ __forceinline__ void load_col(const SetsParams &P, int c, uint64_t u, int4 (&r)[I64 ? 2 : 1]) {
+    const char *p = static_cast<const char *>(P.col[c].ptr);
+    if (!(I64 && P.col[c].is64)) {
+        r[0] = ld_nc128(p + u * 16);
+    } else {
+        r[0] = ld_nc128(p + u * 32);
+        r[I64 ? 1 : 0] = ld_nc128(p + u * 32 + 16);
+    }
+}
+
+// Offsets u = v - dlo of the four keys in r.
+template <bool I64>
+__device__ __forceinline__ void offsets(const SetsCol &C, const int4 (&r)[I64 ? 2 : 1], uint64_t (&uo)[4]) {
+    if (!(I64 && C.is64)) {
+        const uint32_t d = static_cast<uint32_t>(C.dlo);
+        uo[0] = static_cast<uint32_t>(r[0].x) - d;
+        uo[1] = static_cast<uint32_t>(r[0].y) - d;
+        uo[2] = static_cast<uint32_t>(r[0].z) - d;
+        uo[3] = static_cast<uint32_t>(r[0].w) - d;
+    } else {
+        const int4 a = r[0], b = r[I64 ? 1 : 0];
+        const uint64_t d = static_cast<uint64_t>(C.dlo);
+        uo[0] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.y)) << 32) | static_cast<uint32_t>(a.x)) - d;
+        uo[1] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.w)) << 32) | static_cast<uint32_t>(a.z)) - d;
+        uo[2] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.y)) << 32) | static_cast<uint32_t>(b.x)) - d;
+        uo[3] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.w)) << 32) | static_cast<uint32_t>(b.z)) - d;
+    }
+}
+
+// AND the set-satisfaction masks of column c's four keys (offsets uo) into x[k].  FOLD (one 32-set word): a cell with no breakpoint inside holds its sat
+// mask itself (bit 31 clear); other cells hold kSetsImpure | b0 | n << 20.  Otherwise a
+// cell holds b0 | n << 20 and the mask is sat[b].  The in-cell search runs only for the
+// keys in cells with breakpoints, behind one warp-level branch per column.
+template <int W, bool FOLD, bool I64>
+__device__ __forceinline__ void column_masks(const SetsCol &C, const uint32_t *sm32, const uint64_t *sm64,
+                                             const uint64_t (&uo)[4], uint32_t (&x)[4][W]) {
+    const bool w64 = I64 && C.is64;
+    uint32_t cw[4], slow = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t cell = w64 ? static_cast<uint32_t>(uo[k] >> C.shift) : static_cast<uint32_t>(uo[k]) >> C.shift;
+        cw[k] = sm32[C.cell_off + cell];
+        if (FOLD) slow |= cw[k];
+        else slow |= cw[k] >> kSetsCellB0Bits;
+    }
+    if (FOLD) {
+        if (!(slow & kSetsImpure)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k][0] &= cw[k];
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t b = cw[k] & ((1u << kSetsCellB0Bits) - 1u);
+        const uint32_t n = (cw[k] & ~kSetsImpure) >> kSetsCellB0Bits;
+        if (FOLD && !(cw[k] & kSetsImpure)) {
+            x[k][0] &= cw[k];
+            continue;
+        }
+        if (n) b += count_le(sm64 + C.bps_off + b, n, uo[k]);
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[k][j] &= sm32[C.sat_off + b * W + j];
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void csa_add(uint32_t (&pl)[W][5], const uint32_t (&x)[4][W]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            uint32_t cy = x[k][j];
+#pragma unroll
+            for (int p = 0; p < 5; ++p) {
+                const uint32_t t = pl[j][p] & cy;
+                pl[j][p] ^= cy;
+                cy = t;
+            }
+        }
+}
+
+// One CTA per SM of 1024 threads; each thread owns units of 4 rows.  Column-streamed keys:
+// once column c of the current unit is consumed, its registers are refilled with column c
+// of the thread's next unit, so the next keys are in flight during the rest of the unit.
+template <int W, int NCM, bool I64, bool SAMPLE, bool FOLD>
+__global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_constant__ SetsParams P) {
     extern __shared__ uint4 s_img[];
     __shared__ uint32_t s_cnt[kSetsMaxWords * 32];
     for (uint32_t i = threadIdx.x; i < P.image_u4; i += blockDim.x) s_img[i] = __ldg(P.image + i);
@@ -87,7 +174,7 @@ __global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constan
     const uint64_t *sm64 = reinterpret_cast<const uint64_t *>(s_img);
 
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nfull = P.nrows / 4, nunits = (P.nrows + 3) / 4;   // unit nfull may be partial
+    const uint64_t nfull = P.nrows / 4;
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t pl[W][5], cnt[W];
@@ -99,20 +186,26 @@ __global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constan
     }
     uint32_t kept = 0;
     int pend = 0;
-    // warp-uniform trip count (the flush is warp-collective)
-    for (uint64_t base = gw * 32; base < nunits; base += stride) {
-        const uint64_t u = base + lane;
-        uint32_t keep = 0;
-        if (u < nunits) {
-            keep = u < nfull ? 0xFu : (1u << (uint32_t)(P.nrows - 4 * nfull)) - 1u;
-            if (SAMPLE) {
-                const uint64_t g0 = P.row0 + 4 * u;
-                uint32_t kk = 0;
+    auto quad_keep = [&](uint64_t u) -> uint32_t {
+        if (u >= nfull) return 0u;
+        if (!SAMPLE) return 0xFu;
+        const uint64_t g0 = P.row0 + 4 * u;
+        uint32_t kk = 0;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) kk |= (sets_keep(P.seed, P.thr, g0 + k) ? 1u : 0u) << k;
-                keep &= kk;
-            }
-        }
+        for (int k = 0; k < 4; ++k) kk |= (sets_keep(P.seed, P.thr, g0 + k) ? 1u : 0u) << k;
+        return kk;
+    };
+    int4 r[NCM][I64 ? 2 : 1];
+    uint64_t u = gw * 32 + lane;
+    uint32_t keep = quad_keep(u);
+    if (keep) {
+#pragma unroll
+        for (int c = 0; c < NCM; ++c)
+            if (c < (int)P.ncols) load_col<I64>(P, c, u, r[c]);
+    }
+    // warp-uniform trip count (the flush is warp-collective)
+    for (uint64_t base = gw * 32; base < nfull; base += stride, u += stride) {
+        const uint32_t keep_n = quad_keep(u + stride);
         kept += __popc(keep);
         uint32_t x[4][W];
 #pragma unroll
@@ -120,86 +213,49 @@ __global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constan
 #pragma unroll
             for (int j = 0; j < W; ++j) x[k][j] = ((keep >> k) & 1u) ? 0xFFFFFFFFu : 0u;
         if (keep) {
-            // every probed column's keys of the unit in flight before any is used
-            int4 r[NCM][I64 ? 2 : 1];
 #pragma unroll
             for (int c = 0; c < NCM; ++c) {
                 if (c >= (int)P.ncols) break;
-                const char *p = static_cast<const char *>(P.col[c].ptr);
-                const bool w64 = I64 && P.col[c].is64;
-                if (u < nfull) {
-                    if (!w64) {
-                        r[c][0] = ld_nc128(p + u * 16);
-                    } else {
-                        r[c][0] = ld_nc128(p + u * 32);
-                        r[c][I64 ? 1 : 0] = ld_nc128(p + u * 32 + 16);
-                    }
-                } else {   // partial last unit: missing rows repeat row 0 (a valid key; keep bit 0)
-                    const uint32_t nk = (uint32_t)(P.nrows - 4 * nfull);
-                    if (!w64) {
-                        const int32_t *q = reinterpret_cast<const int32_t *>(p) + 4 * u;
-                        const int32_t a = q[0], b = nk > 1 ? q[1] : a, d = nk > 2 ? q[2] : a;
-                        r[c][0] = make_int4(a, b, d, a);
-                    } else {
-                        const long long *q = reinterpret_cast<const long long *>(p) + 4 * u;
-                        const long long a = q[0], b = nk > 1 ? q[1] : a, d = nk > 2 ? q[2] : a;
-                        r[c][0] = make_int4((int)a, (int)(a >> 32), (int)b, (int)(b >> 32));
-                        r[c][I64 ? 1 : 0] = make_int4((int)d, (int)(d >> 32), (int)a, (int)(a >> 32));
-                    }
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < NCM; ++c) {
-                if (c >= (int)P.ncols) break;
-                const SetsCol &C = P.col[c];
-                const bool w64 = I64 && C.is64;
                 uint64_t uo[4];
-                if (!w64) {
-                    const int4 q = r[c][0];
-                    const uint32_t d = static_cast<uint32_t>(C.dlo);
-                    uo[0] = static_cast<uint32_t>(q.x) - d;
-                    uo[1] = static_cast<uint32_t>(q.y) - d;
-                    uo[2] = static_cast<uint32_t>(q.z) - d;
-                    uo[3] = static_cast<uint32_t>(q.w) - d;
-                } else {
-                    const int4 a = r[c][0], b = r[c][I64 ? 1 : 0];
-                    const uint64_t d = static_cast<uint64_t>(C.dlo);
-                    uo[0] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.y)) << 32) | static_cast<uint32_t>(a.x)) - d;
-                    uo[1] = ((static_cast<uint64_t>(static_cast<uint32_t>(a.w)) << 32) | static_cast<uint32_t>(a.z)) - d;
-                    uo[2] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.y)) << 32) | static_cast<uint32_t>(b.x)) - d;
-                    uo[3] = ((static_cast<uint64_t>(static_cast<uint32_t>(b.w)) << 32) | static_cast<uint32_t>(b.z)) - d;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t cell = w64 ? static_cast<uint32_t>(uo[k] >> C.shift)
-                                              : static_cast<uint32_t>(uo[k]) >> C.shift;
-                    const uint32_t cw = sm32[C.cell_off + cell];
-                    uint32_t b = cw & ((1u << kSetsCellB0Bits) - 1u);
-                    const uint32_t n = cw >> kSetsCellB0Bits;
-                    if (n) b += count_le(sm64 + C.bps_off + b, n, uo[k]);
-#pragma unroll
-                    for (int j = 0; j < W; ++j) x[k][j] &= sm32[C.sat_off + b * W + j];
-                }
+                offsets<I64>(P.col[c], r[c], uo);
+                if (keep_n) load_col<I64>(P, c, u + stride, r[c]);
+                column_masks<W, FOLD, I64>(P.col[c], sm32, sm64, uo, x);
             }
+        } else if (keep_n) {
+#pragma unroll
+            for (int c = 0; c < NCM; ++c)
+                if (c < (int)P.ncols) load_col<I64>(P, c, u + stride, r[c]);
         }
-        // carry-save add of the four row masks into the 5 bit planes (counts <= 28 < 32)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                uint32_t cy = x[k][j];
-#pragma unroll
-                for (int p = 0; p < 5; ++p) {
-                    const uint32_t t = pl[j][p] & cy;
-                    pl[j][p] ^= cy;
-                    cy = t;
-                }
-            }
+        keep = keep_n;
+        csa_add<W>(pl, x);
         pend += 4;
         if (pend >= 28) {
             flush<W>(pl, cnt, lane);
             pend = 0;
         }
+    }
+    // tail rows [4 * nfull, nrows): lanes 0..2 of global warp 0, one row each
+    if (gw == 0 && 4 * nfull < P.nrows) {
+        const uint64_t row = 4 * nfull + lane;
+        uint32_t x[4][W];
+        const bool mine = row < P.nrows && (!SAMPLE || sets_keep(P.seed, P.thr, P.row0 + row));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < W; ++j) x[k][j] = (k == 0 && mine) ? 0xFFFFFFFFu : 0u;
+        if (mine) {
+            kept += 1;
+            for (int c = 0; c < (int)P.ncols; ++c) {
+                const SetsCol &C = P.col[c];
+                uint64_t uo[4];
+                if (I64 && C.is64) uo[0] = static_cast<uint64_t>(static_cast<const long long *>(C.ptr)[row]) - static_cast<uint64_t>(C.dlo);
+                else uo[0] = static_cast<uint32_t>(static_cast<const int32_t *>(C.ptr)[row]) - static_cast<uint32_t>(C.dlo);
+                uo[1] = uo[2] = uo[3] = uo[0];
+                column_masks<W, FOLD, I64>(C, sm32, sm64, uo, x);
+            }
+        }
+        csa_add<W>(pl, x);
+        pend += 1;
     }
     if (pend) flush<W>(pl, cnt, lane);
 #pragma unroll
@@ -215,7 +271,7 @@ __global__ void __launch_bounds__(kSetsThreads) sets_kernel(const __grid_constan
 namespace {
 template <int W, int NCM, bool I64, bool SAMPLE>
 cudaError_t launch_t(const SetsParams &P, int grid, size_t smem, cudaStream_t s) {
-    auto k = sets_kernel<W, NCM, I64, SAMPLE>;
+    auto k = P.fold ? sets_kernel<W, NCM, I64, SAMPLE, W == 1> : sets_kernel<W, NCM, I64, SAMPLE, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kSetsThreads, smem, s>>>(P);

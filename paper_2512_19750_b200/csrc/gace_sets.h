@@ -20,9 +20,10 @@ namespace gace {
 
 constexpr int kSetsMaxCols = 8;       // probed columns per call (GACE_MAX_PROBED_COLS)
 constexpr int kSetsMaxWords = 8;      // 32-set words: nsets <= 256
-constexpr int kSetsThreads = 512;
-constexpr uint32_t kSetsCellB0Bits = 20;          // cell word: b0 | n << 20
-constexpr uint32_t kSetsCellNMax = (1u << 12) - 1;
+constexpr int kSetsThreads = 1024;     // one CTA per SM (<= 64 registers)
+constexpr uint32_t kSetsCellB0Bits = 20;          // cell word: b0 | n << 20 (| kSetsImpure)
+constexpr uint32_t kSetsCellNMax = (1u << 11) - 1;
+constexpr uint32_t kSetsImpure = 0x80000000u;     // folded plans: cell holds breakpoints
 
 struct SetsCol {
     const void *ptr;        // column values of this launch (16-byte aligned)
@@ -40,7 +41,7 @@ struct SetsParams {
     uint32_t ncols;
     uint32_t W;             // 32-set words
     uint32_t image_u4;      // shared-memory image size (uint4)
-    uint32_t pad;
+    uint32_t fold;          // W == 1, nsets <= 31: breakpoint-free cells hold their sat mask
     const uint4 *image;     // cells | breakpoints | sat masks
     uint64_t nrows;         // rows of this launch
     uint64_t row0;          // global id of the first row (sample bit)
