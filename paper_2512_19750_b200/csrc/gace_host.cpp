@@ -1335,9 +1335,11 @@ gace_status make_sets_plan(const gace_table *t, const gace_pred *preds, const ui
             std::vector<uint32_t> cw(nc);
             size_t i = 0;
             bool ok = true;
+            // b0 = #{t <= cell start}: a breakpoint at the cell start does not split the cell;
+            // n = #{t in (start, end]}, searched in bps[b0 .. b0 + n)
             for (uint64_t cell = 0; cell < nc; ++cell) {
                 const uint64_t cs = cell << sh;
-                while (i < B.size() && B[i] < cs) ++i;
+                while (i < B.size() && B[i] <= cs) ++i;
                 size_t e = i;
                 const uint64_t ce_minus1 = cs + ((sh >= 64) ? ~0ull : ((1ull << sh) - 1));   // inclusive end
                 while (e < B.size() && B[e] <= ce_minus1) ++e;

@@ -35,6 +35,14 @@ __device__ __forceinline__ int4 ld_nc128(const void *p) {
     return r;
 }
 
+// Predicated 128-bit load into r (unchanged when !pred): one instruction, no register copies
+__device__ __forceinline__ void ld_nc128_if(bool pred, const void *p, int4 &r) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n"
+                 " @q ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%5];\n}"
+                 : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+                 : "r"((uint32_t)pred), "l"(p));
+}
+
 // #{i < n : bps[i] <= u} over sorted bps (branch-free binary search)
 __device__ __forceinline__ uint32_t count_le(const uint64_t *bps, uint32_t n, uint64_t u) {
     uint32_t lo = 0;
@@ -76,15 +84,16 @@ __device__ __forceinline__ void flush(uint32_t (&pl)[W][5], uint32_t (&cnt)[W], 
 
 }  // namespace
 
-// Keys of unit u of column c (4 rows) into r (int64 columns: two 128-bit loads).
+// Keys of unit u of column c (4 rows) into r when pred (int64 columns: two 128-bit loads).
 template <bool I64>
-__device__ __forceinline__ void load_col(const SetsParams &P, int c, uint64_t u, int4 (&r)[I64 ? 2 : 1]) {
+__device__ __forceinline__ void load_col(const SetsParams &P, int c, uint64_t u, int4 (&r)[I64 ? 2 : 1],
+                                         bool pred = true) {
     const char *p = static_cast<const char *>(P.col[c].ptr);
     if (!(I64 && P.col[c].is64)) {
-        r[0] = ld_nc128(p + u * 16);
+        ld_nc128_if(pred, p + u * 16, r[0]);
     } else {
-        r[0] = ld_nc128(p + u * 32);
-        r[I64 ? 1 : 0] = ld_nc128(p + u * 32 + 16);
+        ld_nc128_if(pred, p + u * 32, r[0]);
+        ld_nc128_if(pred, p + u * 32 + 16, r[I64 ? 1 : 0]);
     }
 }
 
@@ -115,32 +124,38 @@ template <int W, bool FOLD, bool I64>
 __device__ __forceinline__ void column_masks(const SetsCol &C, const uint32_t *sm32, const uint64_t *sm64,
                                              const uint64_t (&uo)[4], uint32_t (&x)[4][W]) {
     const bool w64 = I64 && C.is64;
+    const uint32_t *cells = sm32 + C.cell_off;
     uint32_t cw[4], slow = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const uint32_t cell = w64 ? static_cast<uint32_t>(uo[k] >> C.shift) : static_cast<uint32_t>(uo[k]) >> C.shift;
-        cw[k] = sm32[C.cell_off + cell];
+        cw[k] = cells[cell];
         if (FOLD) slow |= cw[k];
         else slow |= cw[k] >> kSetsCellB0Bits;
     }
-    if (FOLD) {
-        if (!(slow & kSetsImpure)) {
+    if (FOLD && !(slow & kSetsImpure)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) x[k][0] &= cw[k];
-            return;
-        }
+        for (int k = 0; k < 4; ++k) x[k][0] &= cw[k];
+        return;
     }
+    const uint64_t *bps = sm64 + C.bps_off;
+    const uint32_t *sat = sm32 + C.sat_off;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        uint32_t b = cw[k] & ((1u << kSetsCellB0Bits) - 1u);
-        const uint32_t n = (cw[k] & ~kSetsImpure) >> kSetsCellB0Bits;
-        if (FOLD && !(cw[k] & kSetsImpure)) {
-            x[k][0] &= cw[k];
-            continue;
-        }
-        if (n) b += count_le(sm64 + C.bps_off + b, n, uo[k]);
+        uint32_t m = cw[k];                       // FOLD: a breakpoint-free cell's mask
+        if (!FOLD || (cw[k] & kSetsImpure)) {
+            uint32_t b = cw[k] & ((1u << kSetsCellB0Bits) - 1u);
+            const uint32_t n = (cw[k] & ~kSetsImpure) >> kSetsCellB0Bits;
+            if (n == 1) b += bps[b] <= uo[k] ? 1u : 0u;     // the common boundary cell
+            else if (n) b += count_le(bps + b, n, uo[k]);
+            if (FOLD) {
+                m = sat[b];
+            } else {
 #pragma unroll
-        for (int j = 0; j < W; ++j) x[k][j] &= sm32[C.sat_off + b * W + j];
+                for (int j = 0; j < W; ++j) x[k][j] &= sat[b * W + j];
+            }
+        }
+        if (FOLD) x[k][0] &= m;
     }
 }
 
@@ -195,14 +210,12 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
         for (int k = 0; k < 4; ++k) kk |= (sets_keep(P.seed, P.thr, g0 + k) ? 1u : 0u) << k;
         return kk;
     };
-    int4 r[NCM][I64 ? 2 : 1];
+    int4 r[NCM][I64 ? 2 : 1] = {};
     uint64_t u = gw * 32 + lane;
     uint32_t keep = quad_keep(u);
-    if (keep) {
 #pragma unroll
-        for (int c = 0; c < NCM; ++c)
-            if (c < (int)P.ncols) load_col<I64>(P, c, u, r[c]);
-    }
+    for (int c = 0; c < NCM; ++c)
+        if (c < (int)P.ncols) load_col<I64>(P, c, u, r[c], keep != 0u);
     // warp-uniform trip count (the flush is warp-collective)
     for (uint64_t base = gw * 32; base < nfull; base += stride, u += stride) {
         const uint32_t keep_n = quad_keep(u + stride);
@@ -218,13 +231,13 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
                 if (c >= (int)P.ncols) break;
                 uint64_t uo[4];
                 offsets<I64>(P.col[c], r[c], uo);
-                if (keep_n) load_col<I64>(P, c, u + stride, r[c]);
+                load_col<I64>(P, c, u + stride, r[c], keep_n != 0u);
                 column_masks<W, FOLD, I64>(P.col[c], sm32, sm64, uo, x);
             }
-        } else if (keep_n) {
+        } else {
 #pragma unroll
             for (int c = 0; c < NCM; ++c)
-                if (c < (int)P.ncols) load_col<I64>(P, c, u + stride, r[c]);
+                if (c < (int)P.ncols) load_col<I64>(P, c, u + stride, r[c], keep_n != 0u);
         }
         keep = keep_n;
         csa_add<W>(pl, x);
