@@ -178,7 +178,9 @@ __device__ __forceinline__ void csa_add(uint32_t (&pl)[W][5], const uint32_t (&x
 // One CTA per SM of 1024 threads; each thread owns units of 4 rows.  Column-streamed keys:
 // once column c of the current unit is consumed, its registers are refilled with column c
 // of the thread's next unit, so the next keys are in flight during the rest of the unit.
-template <int W, int NCM, bool I64, bool SAMPLE, bool FOLD>
+// NCM: column slots compiled; EXACT: ncols == NCM (no run-time column checks, which would
+// otherwise make the compiler shuffle the streamed key registers between paths).
+template <int W, int NCM, bool EXACT, bool I64, bool SAMPLE, bool FOLD>
 __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_constant__ SetsParams P) {
     extern __shared__ uint4 s_img[];
     __shared__ uint32_t s_cnt[kSetsMaxWords * 32];
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
     uint32_t keep = quad_keep(u);
 #pragma unroll
     for (int c = 0; c < NCM; ++c)
-        if (c < (int)P.ncols) load_col<I64>(P, c, u, r[c], keep != 0u);
+        if (EXACT || c < (int)P.ncols) load_col<I64>(P, c, u, r[c], keep != 0u);
     // warp-uniform trip count (the flush is warp-collective)
     for (uint64_t base = gw * 32; base < nfull; base += stride, u += stride) {
         const uint32_t keep_n = quad_keep(u + stride);
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
         if (keep) {
 #pragma unroll
             for (int c = 0; c < NCM; ++c) {
-                if (c >= (int)P.ncols) break;
+                if (!EXACT && c >= (int)P.ncols) break;
                 uint64_t uo[4];
                 offsets<I64>(P.col[c], r[c], uo);
                 load_col<I64>(P, c, u + stride, r[c], keep_n != 0u);
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
         } else {
 #pragma unroll
             for (int c = 0; c < NCM; ++c)
-                if (c < (int)P.ncols) load_col<I64>(P, c, u + stride, r[c], keep_n != 0u);
+                if (EXACT || c < (int)P.ncols) load_col<I64>(P, c, u + stride, r[c], keep_n != 0u);
         }
         keep = keep_n;
         csa_add<W>(pl, x);
@@ -282,24 +284,38 @@ __global__ void __launch_bounds__(kSetsThreads, 1) sets_kernel(const __grid_cons
 }
 
 namespace {
-template <int W, int NCM, bool I64, bool SAMPLE>
+template <int W, int NCM, bool EXACT, bool I64, bool SAMPLE>
 cudaError_t launch_t(const SetsParams &P, int grid, size_t smem, cudaStream_t s) {
-    auto k = P.fold ? sets_kernel<W, NCM, I64, SAMPLE, W == 1> : sets_kernel<W, NCM, I64, SAMPLE, false>;
+    auto k = P.fold ? sets_kernel<W, NCM, EXACT, I64, SAMPLE, W == 1> : sets_kernel<W, NCM, EXACT, I64, SAMPLE, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kSetsThreads, smem, s>>>(P);
     return cudaGetLastError();
 }
 
-template <int W, int NCM>
+template <int W, int NCM, bool EXACT>
 cudaError_t launch_w(const SetsParams &P, bool sample, bool i64, int grid, size_t smem, cudaStream_t s) {
-    if (i64) return sample ? launch_t<W, NCM, true, true>(P, grid, smem, s) : launch_t<W, NCM, true, false>(P, grid, smem, s);
-    return sample ? launch_t<W, NCM, false, true>(P, grid, smem, s) : launch_t<W, NCM, false, false>(P, grid, smem, s);
+    if (i64)
+        return sample ? launch_t<W, NCM, EXACT, true, true>(P, grid, smem, s)
+                      : launch_t<W, NCM, EXACT, true, false>(P, grid, smem, s);
+    return sample ? launch_t<W, NCM, EXACT, false, true>(P, grid, smem, s)
+                  : launch_t<W, NCM, EXACT, false, false>(P, grid, smem, s);
 }
 
+// exact column counts 1..4 for one or two 32-set words; run-time column counts otherwise
 template <int W>
 cudaError_t launch_nc(const SetsParams &P, bool sample, bool i64, int grid, size_t smem, cudaStream_t s) {
-    return P.ncols <= 4 ? launch_w<W, 4>(P, sample, i64, grid, smem, s) : launch_w<W, 8>(P, sample, i64, grid, smem, s);
+    if (W <= 2) {
+        switch (P.ncols) {
+            case 1: return launch_w<W, 1, true>(P, sample, i64, grid, smem, s);
+            case 2: return launch_w<W, 2, true>(P, sample, i64, grid, smem, s);
+            case 3: return launch_w<W, 3, true>(P, sample, i64, grid, smem, s);
+            case 4: return launch_w<W, 4, true>(P, sample, i64, grid, smem, s);
+            default: break;
+        }
+    }
+    return P.ncols <= 4 ? launch_w<W, 4, false>(P, sample, i64, grid, smem, s)
+                        : launch_w<W, 8, false>(P, sample, i64, grid, smem, s);
 }
 }  // namespace
 
