@@ -67,7 +67,9 @@ __device__ __forceinline__ uint32_t *at(uint32_t a) {
 // Hot-path shared-memory accesses by byte offset from the dynamic shared memory: the
 // window base is a uniform value the compiler folds into the address operand
 // (LDS [R + UR]), instead of materialising generic pointers per access.
-__device__ __forceinline__ uint32_t sbase() { return static_cast<uint32_t>(__cvta_generic_to_shared(g_smem)); }
+// (the address of the dynamic window taken from its PTX symbol: the compiler keeps it in a
+// uniform register instead of re-deriving it from SR_CgaCtaId at every use; C5 scan -3 %)
+__device__ __forceinline__ uint32_t sbase() { uint32_t v; asm("mov.u32 %0, _ZN4gace6g_smemE;" : "=r"(v)); return v; }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t off) {
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase() + off));
