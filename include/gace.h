@@ -221,6 +221,38 @@ gace_status gace_gate(const double *drift, uint32_t nd, const double *s_est,
                       const gace_thresholds *th, uint32_t *fired_mask,
                       uint8_t *per_signal_fired);
 
+/*
+ * Break-even cost accounting (§III-C Eq. 4, lines 80-83: the measurement cost is
+ * modelled from the measured kernel time, "Cost_measurement ~ 0.85 ms"; §V item 2: a
+ * break-even point exists).
+ *   est_probe_cost_ms = c0 + c_t * N + c_e * K * M * N / p
+ *   est_benefit_ms    = benefit_weight * (max - min candidate plan cost)   (SPEC reading S:249)
+ * Host only (no device needed).
+ */
+typedef struct {
+    double c0_ms;           /* fixed cost per probe (launch, plan upload, D2H)               */
+    double ct_ms_per_row;   /* per scanned row                                              */
+    double ce_ms_per_eval;  /* per row x predicate x set evaluation                         */
+    double p;               /* parallelism factor, >= 1                                     */
+    double benefit_weight;  /* >= 0; gace_cost_fit sets 0.5 when it is not >= 0 on entry   */
+} gace_cost_model;
+
+enum { GACE_NO_RISK = 0, GACE_RISK_BUT_NOT_WORTH = 1, GACE_PROBE = 2 };
+
+/* Least-squares fit of (c0, c_t, c_e) >= 0 to npts >= 3 measured probe times ms[i] at
+ * (n[i], k[i], m[i]) for a given p >= 1: every non-negativity active
+ * set is solved and the feasible fit with the least squared residual is kept.  out->p = p.
+ * GACE_EINVAL: NULL, npts < 3, p < 1, non-finite inputs.                                   */
+gace_status gace_cost_fit(const double *n, const double *k, const double *m, const double *ms,
+                          uint32_t npts, double p, gace_cost_model *out);
+
+/* GateDecision: probe = fired_mask != 0 && est_benefit > est_cost
+ * (strict); reason = GACE_NO_RISK (nothing fired), GACE_RISK_BUT_NOT_WORTH, GACE_PROBE.
+ * est_cost_ms / est_benefit_ms may be NULL.  GACE_EINVAL: negative coefficients, p < 1.   */
+gace_status gace_gate_decide(uint32_t fired_mask, const gace_cost_model *cm, double n_sample,
+                             double k, double m, double plan_cost_spread_ms, double *est_cost_ms,
+                             double *est_benefit_ms, uint32_t *probe, uint32_t *reason);
+
 /* Per-stage device times of the last gace_probe on t, in ms (CUDA events on the
  * table's stream; §IV-B overhead decomposition H2D / kernel / D2H / reduction). */
 typedef struct {

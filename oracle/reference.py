@@ -409,3 +409,53 @@ def percentile_nearest_rank(xs: Sequence[float], q: float) -> float:
         raise OracleError("percentile")
     s = sorted(xs)
     return s[max(1, math.ceil(q * len(s))) - 1]
+
+
+# ----------------------------------------------------------------------------- break-even cost accounting
+
+NO_RISK, RISK_BUT_NOT_WORTH, PROBE = 0, 1, 2
+
+
+def probe_cost(c0: float, ct: float, ce: float, p: float, n: float, k: float, m: float) -> float:
+    """est_probe_cost_ms = c0 + c_t*N + c_e*K*M*N/p (Eq. 4 models the
+    measurement cost from the measured kernel time, line 80-83)."""
+    return c0 + ct * n + ce * k * m * n / p
+
+
+def cost_fit(n, k, m, ms, p: float = 1.0):
+    """Least-squares fit of (c0, c_t, c_e) >= 0 to measured probe times (SPEC.md S:232-235
+    calibrate_cost_model; coefficients >= 0).  Every non-negativity active set of the
+    3 coefficients is solved by numpy lstsq and the feasible one with the least squared
+    residual wins (brute force over the 7 non-empty subsets in mask order; the all-zero model
+    is the start; a later subset replaces the best only if its residual is smaller by more than
+    1e-9 of sum(ms^2), so near-ties -- collinear columns -- keep the earlier subset)."""
+    n, k, m, ms = (np.asarray(x, dtype=np.float64) for x in (n, k, m, ms))
+    X = np.stack([np.ones_like(n), n, k * m * n / p], axis=1)
+    tss = float(np.sum(ms * ms))
+    best = (tss, np.zeros(3))
+    for mask in range(1, 8):
+        cols = [j for j in range(3) if mask >> j & 1]
+        sol, *_ = np.linalg.lstsq(X[:, cols], ms, rcond=None)
+        if np.any(sol < 0):
+            continue
+        coef = np.zeros(3)
+        coef[cols] = sol
+        r = float(np.sum((X @ coef - ms) ** 2))
+        if r < best[0] - 1e-9 * tss:
+            best = (r, coef)
+    c0, ct, ce = (float(x) for x in best[1])
+    return c0, ct, ce
+
+
+def gate_decide(fired_mask: int, c0: float, ct: float, ce: float, p: float, benefit_weight: float,
+                n: float, k: float, m: float, plan_cost_spread_ms: float):
+    """GateDecision: est_benefit = weight x plan-cost spread (the
+    SPEC's reading); probe iff some signal fired and est_benefit > est_cost; reason
+    NO_RISK (nothing fired), RISK_BUT_NOT_WORTH (fired, not worth it), PROBE."""
+    cost = probe_cost(c0, ct, ce, p, n, k, m)
+    benefit = benefit_weight * plan_cost_spread_ms
+    if not fired_mask:
+        return cost, benefit, False, NO_RISK
+    if benefit > cost:
+        return cost, benefit, True, PROBE
+    return cost, benefit, False, RISK_BUT_NOT_WORTH

@@ -1859,6 +1859,120 @@ gace_status gace_derive(uint64_t n, const uint64_t *counts, uint32_t npreds, con
     return GACE_OK;
 }
 
+// ------------------------------------------------------------------ break-even cost accounting (NEXT-3)
+
+static double cost_of(const gace_cost_model &c, double n, double k, double m) {
+    return c.c0_ms + c.ct_ms_per_row * n + c.ce_ms_per_eval * k * m * n / c.p;
+}
+
+gace_status gace_cost_fit(const double *n, const double *k, const double *m, const double *ms, uint32_t npts,
+                          double p, gace_cost_model *out) {
+    if (!n || !k || !m || !ms || !out) return fail(GACE_EINVAL, "NULL argument");
+    if (npts < 3) return fail(GACE_EINVAL, "cost fit needs >= 3 points");
+    if (!(p >= 1.0) || !std::isfinite(p)) return fail(GACE_EINVAL, "parallelism factor p must be >= 1");
+    for (uint32_t i = 0; i < npts; ++i)
+        if (!std::isfinite(n[i]) || !std::isfinite(k[i]) || !std::isfinite(m[i]) || !std::isfinite(ms[i]))
+            return fail(GACE_EINVAL, "non-finite calibration point");
+    // design columns: 1, N, K*M*N/p, each scaled by its max |.|
+    std::vector<double> X[3];
+    double scale[3];
+    for (int j = 0; j < 3; ++j) {
+        X[j].resize(npts);
+        scale[j] = 0.0;
+        for (uint32_t i = 0; i < npts; ++i) {
+            X[j][i] = j == 0 ? 1.0 : j == 1 ? n[i] : k[i] * m[i] * n[i] / p;
+            scale[j] = std::max(scale[j], std::fabs(X[j][i]));
+        }
+        if (scale[j] > 0)
+            for (uint32_t i = 0; i < npts; ++i) X[j][i] /= scale[j];
+    }
+    double best_r = 0.0, best[3] = {0, 0, 0};
+    for (uint32_t i = 0; i < npts; ++i) best_r += ms[i] * ms[i];
+    const double tss = best_r;
+    // every non-negativity active set in mask order 1..7, least squares by modified
+    // Gram-Schmidt with one re-orthogonalisation pass; a later set replaces the best only
+    // when its residual is smaller by more than 1e-9 of sum(ms^2) (near-ties keep the
+    // earlier set, e.g. collinear N and K*M*N columns)
+    for (int mask = 1; mask < 8; ++mask) {
+        int cols[3], nc = 0;
+        for (int j = 0; j < 3; ++j)
+            if (mask >> j & 1) cols[nc++] = j;
+        std::vector<double> Q[3];
+        double R[3][3] = {{0}};
+        bool ok = true;
+        for (int a = 0; a < nc; ++a) {
+            Q[a] = X[cols[a]];
+            for (int pass = 0; pass < 2; ++pass)
+                for (int b = 0; b < a; ++b) {
+                    double d = 0;
+                    for (uint32_t i = 0; i < npts; ++i) d += Q[b][i] * Q[a][i];
+                    R[b][a] += d;
+                    for (uint32_t i = 0; i < npts; ++i) Q[a][i] -= d * Q[b][i];
+                }
+            double nr = 0;
+            for (uint32_t i = 0; i < npts; ++i) nr += Q[a][i] * Q[a][i];
+            nr = std::sqrt(nr);
+            if (!(nr > 1e-12)) { ok = false; break; }     // rank-deficient subset: skipped
+            R[a][a] = nr;
+            for (uint32_t i = 0; i < npts; ++i) Q[a][i] /= nr;
+        }
+        if (!ok) continue;
+        double qb[3], sol[3];
+        for (int a = 0; a < nc; ++a) {
+            qb[a] = 0;
+            for (uint32_t i = 0; i < npts; ++i) qb[a] += Q[a][i] * ms[i];
+        }
+        for (int a = nc - 1; a >= 0; --a) {
+            double s = qb[a];
+            for (int b = a + 1; b < nc; ++b) s -= R[a][b] * sol[b];
+            sol[a] = s / R[a][a];
+        }
+        bool feasible = true;
+        double coef[3] = {0, 0, 0};
+        for (int a = 0; a < nc; ++a) {
+            if (sol[a] < 0) feasible = false;
+            coef[cols[a]] = scale[cols[a]] > 0 ? sol[a] / scale[cols[a]] : 0.0;
+        }
+        if (!feasible) continue;
+        double r = 0;
+        for (uint32_t i = 0; i < npts; ++i) {
+            const double pred = coef[0] + coef[1] * n[i] + coef[2] * k[i] * m[i] * n[i] / p;
+            r += (pred - ms[i]) * (pred - ms[i]);
+        }
+        if (r < best_r - 1e-9 * tss) {
+            best_r = r;
+            best[0] = coef[0]; best[1] = coef[1]; best[2] = coef[2];
+        }
+    }
+    out->c0_ms = best[0];
+    out->ct_ms_per_row = best[1];
+    out->ce_ms_per_eval = best[2];
+    out->p = p;
+    if (!(out->benefit_weight >= 0.0)) out->benefit_weight = 0.5;    // SPEC.md S:249 default
+    return GACE_OK;
+}
+
+gace_status gace_gate_decide(uint32_t fired_mask, const gace_cost_model *cm, double n_sample, double k, double m,
+                             double plan_cost_spread_ms, double *est_cost_ms, double *est_benefit_ms,
+                             uint32_t *probe, uint32_t *reason) {
+    if (!cm || !probe || !reason) return fail(GACE_EINVAL, "NULL argument");
+    if (!(cm->p >= 1.0) || !(cm->c0_ms >= 0) || !(cm->ct_ms_per_row >= 0) || !(cm->ce_ms_per_eval >= 0) ||
+        !(cm->benefit_weight >= 0))
+        return fail(GACE_EINVAL, "cost model coefficients must be >= 0 and p >= 1");
+    const double cost = cost_of(*cm, n_sample, k, m);
+    const double benefit = cm->benefit_weight * plan_cost_spread_ms;
+    uint32_t pr = 0, rs = GACE_NO_RISK;
+    if (fired_mask) {
+        pr = benefit > cost ? 1u : 0u;             // strict: a tie is not worth it
+        rs = pr ? GACE_PROBE : GACE_RISK_BUT_NOT_WORTH;
+    }
+    if (est_cost_ms) *est_cost_ms = cost;
+    if (est_benefit_ms) *est_benefit_ms = benefit;
+    *probe = pr;
+    *reason = rs;
+    return GACE_OK;
+}
+
 gace_status gace_gate(const double *drift, uint32_t nd, const double *s_est, const double *s_probe, uint32_t ns,
                       const double *pcs, uint32_t np, const gace_thresholds *th, uint32_t *fired_mask,
                       uint8_t *per_signal_fired) {

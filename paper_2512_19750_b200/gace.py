@@ -32,7 +32,7 @@ HLL_M = 1 << HLL_P
 PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
 PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
-EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets",
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
            "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
@@ -52,6 +52,11 @@ class _Dist(ctypes.Structure):
 class _Thresholds(ctypes.Structure):
     _fields_ = [("d_threshold", ctypes.c_double), ("sel_err_threshold", ctypes.c_double),
                 ("pcs_high", ctypes.c_double), ("pcs_low", ctypes.c_double)]
+
+
+class _CostModel(ctypes.Structure):
+    _fields_ = [("c0_ms", ctypes.c_double), ("ct_ms_per_row", ctypes.c_double), ("ce_ms_per_eval", ctypes.c_double),
+                ("p", ctypes.c_double), ("benefit_weight", ctypes.c_double)]
 
 
 class _Timing(ctypes.Structure):
@@ -80,6 +85,9 @@ def lib() -> ctypes.CDLL:
     L.gace_table_detach.argtypes = [vp]
     L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
     L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
+    L.gace_cost_fit.argtypes = [vp, vp, vp, vp, u32, dbl, ctypes.POINTER(_CostModel)]
+    L.gace_gate_decide.argtypes = [u32, ctypes.POINTER(_CostModel), dbl, dbl, dbl, dbl, ctypes.POINTER(dbl),
+                                   ctypes.POINTER(dbl), ctypes.POINTER(u32), ctypes.POINTER(u32)]
     L.gace_probe_sets.argtypes = [vp, vp, u32, vp, vp, u32, dbl, u64, ctypes.POINTER(u64), vp]
     L.gace_derive.argtypes = [u64, vp, u32, vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp]
     L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
@@ -341,6 +349,26 @@ def derive(n_sampled: int, counts, pairs, joints, regs, ndv_hist=None):
                              _ptr(regs), H, HLL_P, _ptr(hist), sel.ctypes.data, pcs.ctypes.data,
                              ndv.ctypes.data, drift.ctypes.data if hist is not None else None))
     return sel[:len(counts)], pcs[:len(Q)], ndv[:H], (drift[:H] if hist is not None else None)
+
+
+def cost_fit(n, k, m, ms, p: float = 1.0, benefit_weight: float = 0.5):
+    """gace_cost_fit: (c0_ms, ct_ms_per_row, ce_ms_per_eval, p, benefit_weight) fitted to
+    measured probe times (Eq. 4)."""
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (n, k, m, ms)]
+    cm = _CostModel(0.0, 0.0, 0.0, 0.0, float(benefit_weight))
+    _check(lib().gace_cost_fit(*[a.ctypes.data for a in arrs], len(arrs[0]), float(p), ctypes.byref(cm)))
+    return (cm.c0_ms, cm.ct_ms_per_row, cm.ce_ms_per_eval, cm.p, cm.benefit_weight)
+
+
+def gate_decide(fired_mask: int, cost_model, n_sample: float, k: float, m: float, plan_cost_spread_ms: float):
+    """gace_gate_decide: (est_cost_ms, est_benefit_ms, probe, reason)."""
+    cm = _CostModel(*[float(x) for x in cost_model])
+    c, b = ctypes.c_double(), ctypes.c_double()
+    pr, rs = ctypes.c_uint32(), ctypes.c_uint32()
+    _check(lib().gace_gate_decide(int(fired_mask), ctypes.byref(cm), float(n_sample), float(k), float(m),
+                                  float(plan_cost_spread_ms), ctypes.byref(c), ctypes.byref(b), ctypes.byref(pr),
+                                  ctypes.byref(rs)))
+    return c.value, b.value, bool(pr.value), int(rs.value)
 
 
 def gate(drift=(), s_est=(), s_probe=(), pcs=(), thresholds: dict | None = None):
