@@ -4,8 +4,10 @@ prefixes of the Exp. D table, fitted with gace_cost_fit.
 
     python tools/calibrate_cost.py [out.json]       (needs a GPU)
 
-Prints / writes the grid, the fitted (c0, c_t, c_e, p) and the model's relative error per
-point.  p = 148 (SMs: the evaluation term's parallelism)."""
+Every set also holds a tautology on each of the 4 columns (v >= INT64_MIN), so every grid
+point scans the same key bytes per row and only K and M vary the evaluation work (the
+SPEC's model charges per row, not per byte).  Prints / writes the grid, the fitted
+(c0, c_t, c_e, p) and the model's relative error per point.  p = 148 (SMs)."""
 import json
 import statistics
 import sys
@@ -25,17 +27,23 @@ def measure(grid_n=(100_000, 1_000_000, 10_000_000, 100_000_000, 600_037_902), g
     cols = [w.column(c, device="cuda") for c in range(len(w.columns))]
     torch.cuda.synchronize()
     g = np.random.default_rng(7)
+    npool = len(w.preds)
+    taut = np.zeros(4, dtype=w.preds.dtype)
+    for c in range(4):
+        taut[c] = (c, 4, 0, -(2 ** 63), 0)             # GE INT64_MIN: every row
+    preds = np.concatenate([w.preds, taut])
     pts = []
     for n in grid_n:
         t = gace.Table([c[:n] for c in cols], device=0)
         for k in grid_k:
             for m in grid_m:
-                sets = [sorted(int(i) for i in g.choice(len(w.preds), size=k, replace=False)) for _ in range(m)]
-                t.probe_sets(w.preds, sets)                 # plan + warm-up
+                sets = [sorted(int(i) for i in g.choice(npool, size=k, replace=False)) + list(range(npool, npool + 4))
+                        for _ in range(m)]
+                t.probe_sets(preds, sets)                   # plan + warm-up
                 ts = []
                 for _ in range(reps):
                     t0 = time.perf_counter()
-                    t.probe_sets(w.preds, sets)
+                    t.probe_sets(preds, sets)
                     ts.append(1e3 * (time.perf_counter() - t0))
                 pts.append({"n": n, "k": k, "m": m, "ms": statistics.median(ts)})
         t.detach()
