@@ -177,6 +177,20 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
                             double sample_rate, uint64_t seed, uint64_t *n_sampled,
                             uint64_t *set_counts);
 
+/*
+ * Est.CV vs budget (§IV-C "Experiment B: Estimation Stability (Est.CV vs. Budget)",
+ * lines 121-141): run the probe once per seed
+ * (nseeds >= 2, same batch and sample_rate) and report, per predicate, the coefficient of
+ * variation CV = sample standard deviation (R - 1) / mean over the seeds of S_p = count/n;
+ * per pair, the CV of the joint selectivity J/n and of PCS (Eq. 3).  A mean of 0 or a NaN
+ * estimate (n = 0, zero marginal) gives NaN.  Outputs are host arrays [npreds] / [npairs];
+ * cv_joint / cv_pcs may be NULL iff npairs == 0.  Collective with dist, like gace_probe.
+ */
+gace_status gace_estimate_cv(gace_table *t, const gace_pred *preds, uint32_t npreds,
+                             const gace_pair *pairs, uint32_t npairs, double sample_rate,
+                             const uint64_t *seeds, uint32_t nseeds, double *cv_sel,
+                             double *cv_joint, double *cv_pcs);
+
 /* Test hook: the deterministic sample mask of this shard's rows, bit-packed:
  * bit (r % 64) of bits[r / 64] = keep(row_offset + r); bits has ceil(nrows_local/64)
  * words (host).  Device tables only.                                               */

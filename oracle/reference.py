@@ -459,3 +459,41 @@ def gate_decide(fired_mask: int, c0: float, ct: float, ce: float, p: float, bene
     if benefit > cost:
         return cost, benefit, True, PROBE
     return cost, benefit, False, RISK_BUT_NOT_WORTH
+
+
+# ----------------------------------------------------------------------------- Est.CV (Exp. B)
+
+def cv(xs) -> float:
+    """Coefficient of variation: sample standard deviation (R - 1) / mean (SPEC.md S:325);
+    mean 0 or a NaN sample -> NaN.  Loops written out in the order sum, mean, squares."""
+    R = len(xs)
+    mean = 0.0
+    for x in xs:
+        mean += x
+    mean /= float(R)
+    ss = 0.0
+    for x in xs:
+        ss += (x - mean) * (x - mean)
+    sd = math.sqrt(ss / float(R - 1))
+    return float("nan") if mean == 0.0 else sd / mean
+
+
+def estimate_cv(columns, preds, pairs, rate: float, seeds, row_offset: int = 0):
+    """Est.CV over seeded probes (§IV-C Exp. B, lines 121-141):
+    per predicate the CV of S = count/n, per pair the CV of J/n and of PCS (Eq. 3), over one
+    oracle probe per seed."""
+    if len(seeds) < 2:
+        raise OracleError("Est.CV needs >= 2 seeds")
+    P = _as_preds(preds)
+    Q = _as_pairs(pairs)
+    sel, js, pcs = [], [], []
+    for s in seeds:
+        n, c, j, _ = probe(columns, P, Q, rate=rate, seed=s, row_offset=row_offset)
+        sp, pq, _, _ = derive(n, c, Q, j, [], [])
+        sel.append(sp)
+        js.append([(float(x) / float(n)) if n > 0 else float("nan") for x in j])
+        pcs.append(pq)
+    cs = [cv([sel[r][p] for r in range(len(seeds))]) for p in range(len(P))]
+    cj = [cv([js[r][q] for r in range(len(seeds))]) for q in range(len(Q))]
+    cp = [cv([pcs[r][q] for r in range(len(seeds))]) for q in range(len(Q))]
+    return cs, cj, cp

@@ -1782,6 +1782,56 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     return GACE_OK;
 }
 
+// ------------------------------------------------------------------ Est.CV (NEXT-4, PAPER.md Exp. B)
+
+gace_status gace_estimate_cv(gace_table *t, const gace_pred *preds, uint32_t npreds, const gace_pair *pairs,
+                             uint32_t npairs, double sample_rate, const uint64_t *seeds, uint32_t nseeds,
+                             double *cv_sel, double *cv_joint, double *cv_pcs) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    if (nseeds < 2) return fail(GACE_EINVAL, "Est.CV needs >= 2 seeds");
+    if (!seeds) return fail(GACE_EINVAL, "seeds is NULL");
+    if (npreds && !cv_sel) return fail(GACE_EINVAL, "cv_sel is NULL");
+    if (npairs && (!cv_joint || !cv_pcs)) return fail(GACE_EINVAL, "cv_joint / cv_pcs is NULL");
+    st = validate_batch(t, preds, npreds, pairs, npairs, sample_rate, 0, GACE_HLL_P);
+    if (st) return st;
+    // per seed: S_p = count_p / n, S_q = joint_q / n, PCS_q (Eq. 3 order) -- one probe each
+    const size_t P = npreds, Q = npairs;
+    std::vector<double> sel(P * nseeds), js(Q * nseeds), pcs(Q * nseeds);
+    std::vector<uint64_t> counts(std::max<size_t>(P, 1)), joints(std::max<size_t>(Q, 1));
+    for (uint32_t r = 0; r < nseeds; ++r) {
+        uint64_t n = 0;
+        st = gace_probe(t, preds, npreds, pairs, npairs, sample_rate, seeds[r], 0, GACE_HLL_P, &n, counts.data(),
+                        joints.data(), nullptr);
+        if (st) return st;
+        std::vector<double> s(P), pq(Q);
+        st = gace_derive(n, counts.data(), npreds, pairs, joints.data(), npairs, nullptr, 0, GACE_HLL_P, nullptr,
+                         s.data(), pq.data(), nullptr, nullptr);
+        if (st) return st;
+        for (size_t p = 0; p < P; ++p) sel[p * nseeds + r] = s[p];
+        for (size_t q = 0; q < Q; ++q) {
+            js[q * nseeds + r] = n ? (double)joints[q] / (double)n : NAN;
+            pcs[q * nseeds + r] = pq[q];
+        }
+    }
+    // CV = sample standard deviation (R - 1) / mean; mean 0 or any NaN -> NaN
+    auto cv = [&](const double *x) {
+        double mean = 0.0;
+        for (uint32_t r = 0; r < nseeds; ++r) mean += x[r];
+        mean /= (double)nseeds;
+        double ss = 0.0;
+        for (uint32_t r = 0; r < nseeds; ++r) ss += (x[r] - mean) * (x[r] - mean);
+        const double sd = std::sqrt(ss / (double)(nseeds - 1));
+        return mean == 0.0 ? NAN : sd / mean;
+    };
+    for (size_t p = 0; p < P; ++p) cv_sel[p] = cv(&sel[p * nseeds]);
+    for (size_t q = 0; q < Q; ++q) {
+        cv_joint[q] = cv(&js[q * nseeds]);
+        cv_pcs[q] = cv(&pcs[q * nseeds]);
+    }
+    return GACE_OK;
+}
+
 gace_status gace_sample_mask(gace_table *t, double sample_rate, uint64_t seed, uint64_t *bits) {
     gace_status st = check_table(t);
     if (st) return st;

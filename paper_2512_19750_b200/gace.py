@@ -32,7 +32,7 @@ HLL_M = 1 << HLL_P
 PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
 PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
-EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide",
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
            "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
@@ -85,6 +85,7 @@ def lib() -> ctypes.CDLL:
     L.gace_table_detach.argtypes = [vp]
     L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
     L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
+    L.gace_estimate_cv.argtypes = [vp, vp, u32, vp, u32, dbl, vp, u32, vp, vp, vp]
     L.gace_cost_fit.argtypes = [vp, vp, vp, vp, u32, dbl, ctypes.POINTER(_CostModel)]
     L.gace_gate_decide.argtypes = [u32, ctypes.POINTER(_CostModel), dbl, dbl, dbl, dbl, ctypes.POINTER(dbl),
                                    ctypes.POINTER(dbl), ctypes.POINTER(u32), ctypes.POINTER(u32)]
@@ -300,6 +301,19 @@ class Table:
                                      float(sample_rate), int(seed) & ((1 << 64) - 1), ctypes.byref(n),
                                      out.ctypes.data))
         return int(n.value), out[:len(sets)]
+
+    def estimate_cv(self, preds, pairs, sample_rate: float, seeds):
+        """Est.CV over seeded probes (gace_estimate_cv; PAPER.md Exp. B).
+        Returns (cv_sel[P], cv_joint[Q], cv_pcs[Q])."""
+        P = as_preds(preds)
+        Q = as_pairs(pairs)
+        S = np.ascontiguousarray([int(x) & ((1 << 64) - 1) for x in seeds], dtype=np.uint64)
+        cs = np.zeros(max(len(P), 1))
+        cj = np.zeros(max(len(Q), 1))
+        cp = np.zeros(max(len(Q), 1))
+        _check(lib().gace_estimate_cv(self._h, _ptr(P), len(P), _ptr(Q), len(Q), float(sample_rate),
+                                      S.ctypes.data, len(S), cs.ctypes.data, cj.ctypes.data, cp.ctypes.data))
+        return cs[:len(P)], cj[:len(Q)], cp[:len(Q)]
 
     def sample_mask(self, sample_rate: float, seed: int) -> np.ndarray:
         bits = np.zeros(max(1, (self.nrows + 63) // 64), dtype=np.uint64)

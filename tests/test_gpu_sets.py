@@ -170,3 +170,22 @@ def test_full_size_identities(G):
             assert n == r.n_sampled and c.max() <= n
     finally:
         t.detach()
+
+
+def test_estimate_cv_matches_oracle(G, oracle):
+    """Est.CV (gace_estimate_cv, PAPER.md Exp. B) == the oracle's, derived doubles within
+    1e-12 relative (the per-seed counts are bit-exact)."""
+    w = synth.get("C1", 150_001)
+    cols = [x.numpy() for x in w.table()]
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols], device=0)
+    try:
+        seeds = [11, 12, 13, 14, 15]
+        for rate in (0.02, 0.3, 1.0):
+            got = t.estimate_cv(w.preds, w.pairs, rate, seeds)
+            want = oracle.estimate_cv(cols, w.preds, w.pairs, rate, seeds)
+            for g, wv in zip(got, want):
+                np.testing.assert_allclose(g, np.asarray(wv, dtype=np.float64), rtol=1e-12, atol=1e-15)
+        with pytest.raises(G.GaceError):
+            t.estimate_cv(w.preds, w.pairs, 0.5, [1])
+    finally:
+        t.detach()
