@@ -191,6 +191,38 @@ gace_status gace_estimate_cv(gace_table *t, const gace_pred *preds, uint32_t npr
                              const uint64_t *seeds, uint32_t nseeds, double *cv_sel,
                              double *cv_joint, double *cv_pcs);
 
+/*
+ * Probe cache (§V item 3, line 314: "Probing results should be cached by bind value
+ * (or value range) to amortize the measurement cost across subsequent queries"; SPEC.md
+ * S:354-403).  Host-only; thread-safe (one mutex per cache).
+ * Key: table_id + the conjunction's predicates normalised as (col, op, flags, bind bucket of
+ * a, bind bucket of b for BETWEEN), sorted and de-duplicated -- A and B == B and A.  Bind
+ * bucket: with range_buckets > 0 and a domain [lo, hi] per predicate (domains[2i], [2i+1]),
+ * the equal-width bucket of the bind (-1 below lo, range_buckets above hi); otherwise the
+ * exact bind.  Capacity (0 = 4096 entries): least recently inserted evicted first.
+ */
+typedef struct {
+    double s_probe;         /* measured selectivity, in [0, 1] (put: GACE_EINVAL otherwise) */
+    uint64_t count;         /* matching sampled rows                                      */
+    uint64_t n_sampled;     /* sample size used                                           */
+    uint64_t hits;          /* lookups that returned this entry (put resets it)            */
+} gace_cache_entry;
+typedef struct gace_cache gace_cache;
+
+gace_status gace_cache_create(uint32_t capacity, uint32_t range_buckets, gace_cache **out);
+gace_status gace_cache_destroy(gace_cache *c);
+/* Insert or replace (a replaced entry moves to the back of the eviction order). */
+gace_status gace_cache_put(gace_cache *c, uint64_t table_id, const gace_pred *conj, uint32_t k,
+                           const int64_t *domains, const gace_cache_entry *entry);
+/* *hit = 1 and *entry (may be NULL) = the stored entry with its hit count incremented, or
+ * *hit = 0 on a miss. */
+gace_status gace_cache_lookup(gace_cache *c, uint64_t table_id, const gace_pred *conj, uint32_t k,
+                              const int64_t *domains, gace_cache_entry *entry, uint32_t *hit);
+/* Drop every entry of table_id (the table was mutated). */
+gace_status gace_cache_invalidate(gace_cache *c, uint64_t table_id);
+gace_status gace_cache_stats(gace_cache *c, uint64_t *hits, uint64_t *misses, uint64_t *evictions,
+                             uint64_t *size);
+
 /* Test hook: the deterministic sample mask of this shard's rows, bit-packed:
  * bit (r % 64) of bits[r / 64] = keep(row_offset + r); bits has ceil(nrows_local/64)
  * words (host).  Device tables only.                                               */

@@ -497,3 +497,65 @@ def estimate_cv(columns, preds, pairs, rate: float, seeds, row_offset: int = 0):
     cj = [cv([js[r][q] for r in range(len(seeds))]) for q in range(len(Q))]
     cp = [cv([pcs[r][q] for r in range(len(seeds))]) for q in range(len(Q))]
     return cs, cj, cp
+
+
+# ----------------------------------------------------------------------------- probe cache (§V item 3)
+
+class CacheModel:
+    """Plain model of the probe cache (§V item 3, line 314):
+    key = (table, sorted set of (col, op, flags, bucket(a), bucket(b) if BETWEEN else 0));
+    bucket = exact bind, or the equal-width range bucket of [lo, hi] split in `buckets`
+    (-1 below, `buckets` above); FIFO eviction of the least recently inserted key."""
+
+    def __init__(self, capacity: int = 4096, buckets: int = 0):
+        self.capacity = capacity or 4096
+        self.buckets = buckets
+        self.entries = {}           # key -> [s, count, n, hits]
+        self.order = []             # keys, oldest insertion first
+        self.hits = self.misses = self.evictions = 0
+
+    def _bucket(self, x, dom):
+        if not self.buckets or dom is None:
+            return x
+        lo, hi = dom
+        if x < lo:
+            return -1
+        if x > hi:
+            return self.buckets
+        from fractions import Fraction
+        b = int(Fraction(x - lo) * self.buckets / Fraction(hi - lo + 1))
+        return min(max(b, 0), self.buckets - 1)
+
+    def key(self, table, conj, domains=None):
+        items = set()
+        for i, p in enumerate(conj):
+            col, op, fl, a, b = (int(p[f]) for f in ("col", "op", "flags", "a", "b"))
+            dom = None if domains is None else (int(domains[i][0]), int(domains[i][1]))
+            items.add((col, op, fl, self._bucket(a, dom), self._bucket(b, dom) if op == BETWEEN else 0))
+        return (int(table), tuple(sorted(items)))
+
+    def put(self, table, conj, s, count=0, n=0, domains=None):
+        k = self.key(table, conj, domains)
+        if k in self.entries:
+            self.order.remove(k)
+        self.entries[k] = [float(s), int(count), int(n), 0]
+        self.order.append(k)
+        while len(self.entries) > self.capacity:
+            old = self.order.pop(0)
+            del self.entries[old]
+            self.evictions += 1
+
+    def lookup(self, table, conj, domains=None):
+        k = self.key(table, conj, domains)
+        if k not in self.entries:
+            self.misses += 1
+            return None
+        self.hits += 1
+        e = self.entries[k]
+        e[3] += 1
+        return tuple(e)
+
+    def invalidate(self, table):
+        for k in [k for k in self.entries if k[0] == int(table)]:
+            del self.entries[k]
+            self.order.remove(k)

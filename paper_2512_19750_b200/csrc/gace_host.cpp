@@ -14,6 +14,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
+#include <deque>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -1829,6 +1831,148 @@ gace_status gace_estimate_cv(gace_table *t, const gace_pred *preds, uint32_t npr
         cv_joint[q] = cv(&js[q * nseeds]);
         cv_pcs[q] = cv(&pcs[q * nseeds]);
     }
+    return GACE_OK;
+}
+
+// ------------------------------------------------------------------ probe cache (NEXT-4, §V item 3)
+
+struct gace_cache {
+    uint32_t magic = 0x47434348u;   // "GCCH"
+    uint32_t capacity = 4096, buckets = 64;
+    struct Entry {
+        gace_cache_entry v;
+        uint64_t seq;
+        uint64_t table;
+    };
+    std::map<std::string, Entry> map;
+    std::deque<std::pair<uint64_t, std::string>> order;   // insertion order (FIFO eviction)
+    uint64_t seq = 0, hits = 0, misses = 0, evictions = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+gace_status check_cache(const gace_cache *c) {
+    if (!c || c->magic != 0x47434348u) return fail(GACE_EHANDLE, "invalid or destroyed cache handle");
+    return GACE_OK;
+}
+
+// Bind bucket of value x on a column with domain [lo, hi]: buckets equal-width intervals
+// (SPEC.md S:397 reading: 64 per column), -1 below the domain, `buckets` above; exact value
+// when buckets == 0 or no domain is given.
+int64_t bind_bucket(int64_t x, uint32_t buckets, const int64_t *dom) {
+    if (!buckets || !dom) return x;
+    const int64_t lo = dom[0], hi = dom[1];
+    if (x < lo) return -1;
+    if (x > hi) return (int64_t)buckets;
+    const long double w = ((long double)hi - (long double)lo + 1.0L) / (long double)buckets;
+    int64_t b = (int64_t)(((long double)x - (long double)lo) / w);
+    return std::min<int64_t>(std::max<int64_t>(b, 0), (int64_t)buckets - 1);
+}
+
+// CacheKey: table id + the conjunction's predicates as (col, op, flags,
+// bind bucket(a), bind bucket(b) for BETWEEN), sorted -- A and B == B and A.
+std::string cache_key(const gace_cache *c, uint64_t table, const gace_pred *conj, uint32_t k, const int64_t *dom) {
+    std::vector<std::array<int64_t, 5>> items(k);
+    for (uint32_t i = 0; i < k; ++i) {
+        const gace_pred &p = conj[i];
+        const int64_t *d = dom ? dom + 2 * i : nullptr;
+        items[i] = {(int64_t)p.col, (int64_t)p.op, (int64_t)p.flags, bind_bucket(p.a, c->buckets, d),
+                    p.op == GACE_BETWEEN ? bind_bucket(p.b, c->buckets, d) : 0};
+    }
+    std::sort(items.begin(), items.end());
+    items.erase(std::unique(items.begin(), items.end()), items.end());   // A and A == A
+    std::string key(reinterpret_cast<const char *>(&table), 8);
+    for (auto &it : items) key.append(reinterpret_cast<const char *>(it.data()), sizeof(int64_t) * 5);
+    return key;
+}
+
+}  // namespace
+
+gace_status gace_cache_create(uint32_t capacity, uint32_t range_buckets, gace_cache **out) {
+    if (!out) return fail(GACE_EINVAL, "out is NULL");
+    gace_cache *c = new gace_cache();
+    c->capacity = capacity ? capacity : 4096;
+    c->buckets = range_buckets;
+    *out = c;
+    return GACE_OK;
+}
+
+gace_status gace_cache_destroy(gace_cache *c) {
+    gace_status st = check_cache(c);
+    if (st) return st;
+    c->magic = 0;
+    delete c;
+    return GACE_OK;
+}
+
+gace_status gace_cache_put(gace_cache *c, uint64_t table_id, const gace_pred *conj, uint32_t k,
+                           const int64_t *domains, const gace_cache_entry *entry) {
+    gace_status st = check_cache(c);
+    if (st) return st;
+    if ((k && !conj) || !entry) return fail(GACE_EINVAL, "NULL argument");
+    if (!(entry->s_probe >= 0.0 && entry->s_probe <= 1.0)) return fail(GACE_EINVAL, "s_probe must be in [0, 1]");
+    std::lock_guard<std::mutex> lock(c->mu);
+    const std::string key = cache_key(c, table_id, conj, k, domains);
+    auto it = c->map.find(key);
+    const uint64_t seq = ++c->seq;
+    if (it != c->map.end()) {                       // replace: re-inserted at the back
+        it->second.v = *entry;
+        it->second.v.hits = 0;
+        it->second.seq = seq;
+    } else {
+        c->map[key] = {*entry, seq, table_id};
+        c->map[key].v.hits = 0;
+    }
+    c->order.emplace_back(seq, key);
+    while (c->map.size() > c->capacity && !c->order.empty()) {      // least recently inserted
+        auto [s, kk] = c->order.front();
+        c->order.pop_front();
+        auto f = c->map.find(kk);
+        if (f != c->map.end() && f->second.seq == s) {
+            c->map.erase(f);
+            ++c->evictions;
+        }
+    }
+    return GACE_OK;
+}
+
+gace_status gace_cache_lookup(gace_cache *c, uint64_t table_id, const gace_pred *conj, uint32_t k,
+                              const int64_t *domains, gace_cache_entry *entry, uint32_t *hit) {
+    gace_status st = check_cache(c);
+    if (st) return st;
+    if ((k && !conj) || !hit) return fail(GACE_EINVAL, "NULL argument");
+    std::lock_guard<std::mutex> lock(c->mu);
+    auto it = c->map.find(cache_key(c, table_id, conj, k, domains));
+    if (it == c->map.end()) {
+        ++c->misses;
+        *hit = 0;
+        return GACE_OK;
+    }
+    ++c->hits;
+    ++it->second.v.hits;
+    if (entry) *entry = it->second.v;
+    *hit = 1;
+    return GACE_OK;
+}
+
+gace_status gace_cache_invalidate(gace_cache *c, uint64_t table_id) {
+    gace_status st = check_cache(c);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(c->mu);
+    for (auto it = c->map.begin(); it != c->map.end();)
+        it = it->second.table == table_id ? c->map.erase(it) : std::next(it);
+    return GACE_OK;
+}
+
+gace_status gace_cache_stats(gace_cache *c, uint64_t *hits, uint64_t *misses, uint64_t *evictions, uint64_t *size) {
+    gace_status st = check_cache(c);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (hits) *hits = c->hits;
+    if (misses) *misses = c->misses;
+    if (evictions) *evictions = c->evictions;
+    if (size) *size = c->map.size();
     return GACE_OK;
 }
 

@@ -32,7 +32,8 @@ HLL_M = 1 << HLL_P
 PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
 PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
-EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv",
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv", "gace_cache_create", "gace_cache_destroy", "gace_cache_put",
+           "gace_cache_lookup", "gace_cache_invalidate", "gace_cache_stats",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
            "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
@@ -57,6 +58,11 @@ class _Thresholds(ctypes.Structure):
 class _CostModel(ctypes.Structure):
     _fields_ = [("c0_ms", ctypes.c_double), ("ct_ms_per_row", ctypes.c_double), ("ce_ms_per_eval", ctypes.c_double),
                 ("p", ctypes.c_double), ("benefit_weight", ctypes.c_double)]
+
+
+class _CacheEntry(ctypes.Structure):
+    _fields_ = [("s_probe", ctypes.c_double), ("count", ctypes.c_uint64), ("n_sampled", ctypes.c_uint64),
+                ("hits", ctypes.c_uint64)]
 
 
 class _Timing(ctypes.Structure):
@@ -85,6 +91,12 @@ def lib() -> ctypes.CDLL:
     L.gace_table_detach.argtypes = [vp]
     L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
     L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
+    L.gace_cache_create.argtypes = [u32, u32, ctypes.POINTER(vp)]
+    L.gace_cache_destroy.argtypes = [vp]
+    L.gace_cache_put.argtypes = [vp, u64, vp, u32, vp, ctypes.POINTER(_CacheEntry)]
+    L.gace_cache_lookup.argtypes = [vp, u64, vp, u32, vp, ctypes.POINTER(_CacheEntry), ctypes.POINTER(u32)]
+    L.gace_cache_invalidate.argtypes = [vp, u64]
+    L.gace_cache_stats.argtypes = [vp] + [ctypes.POINTER(u64)] * 4
     L.gace_estimate_cv.argtypes = [vp, vp, u32, vp, u32, dbl, vp, u32, vp, vp, vp]
     L.gace_cost_fit.argtypes = [vp, vp, vp, vp, u32, dbl, ctypes.POINTER(_CostModel)]
     L.gace_gate_decide.argtypes = [u32, ctypes.POINTER(_CostModel), dbl, dbl, dbl, dbl, ctypes.POINTER(dbl),
@@ -363,6 +375,55 @@ def derive(n_sampled: int, counts, pairs, joints, regs, ndv_hist=None):
                              _ptr(regs), H, HLL_P, _ptr(hist), sel.ctypes.data, pcs.ctypes.data,
                              ndv.ctypes.data, drift.ctypes.data if hist is not None else None))
     return sel[:len(counts)], pcs[:len(Q)], ndv[:H], (drift[:H] if hist is not None else None)
+
+
+class ProbeCache:
+    """Probe-result cache keyed by (table, normalised conjunction, bind value or range
+    bucket) -- gace_cache_* (§V item 3)."""
+
+    def __init__(self, capacity: int = 4096, range_buckets: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().gace_cache_create(capacity, range_buckets, ctypes.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def _args(conj, domains):
+        P = as_preds(conj)
+        D = None if domains is None else np.ascontiguousarray(domains, dtype=np.int64).reshape(-1)
+        return P, D
+
+    def put(self, table_id: int, conj, s_probe: float, count: int = 0, n_sampled: int = 0, domains=None):
+        P, D = self._args(conj, domains)
+        e = _CacheEntry(float(s_probe), int(count), int(n_sampled), 0)
+        _check(lib().gace_cache_put(self._h, int(table_id), _ptr(P), len(P), _ptr(D), ctypes.byref(e)))
+
+    def lookup(self, table_id: int, conj, domains=None):
+        """(s_probe, count, n_sampled, hits) or None."""
+        P, D = self._args(conj, domains)
+        e = _CacheEntry()
+        hit = ctypes.c_uint32()
+        _check(lib().gace_cache_lookup(self._h, int(table_id), _ptr(P), len(P), _ptr(D), ctypes.byref(e),
+                                       ctypes.byref(hit)))
+        return (e.s_probe, e.count, e.n_sampled, e.hits) if hit.value else None
+
+    def invalidate(self, table_id: int):
+        _check(lib().gace_cache_invalidate(self._h, int(table_id)))
+
+    def stats(self) -> dict:
+        v = [ctypes.c_uint64() for _ in range(4)]
+        _check(lib().gace_cache_stats(self._h, *[ctypes.byref(x) for x in v]))
+        return dict(zip(("hits", "misses", "evictions", "size"), (x.value for x in v)))
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _check(lib().gace_cache_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def cost_fit(n, k, m, ms, p: float = 1.0, benefit_weight: float = 0.5):
