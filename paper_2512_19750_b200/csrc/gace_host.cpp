@@ -1616,7 +1616,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.njobs = (uint32_t)pl.jobs.size();
     F.hll_bytes = pl.hll_bytes;
     F.nparts = (t->nrows == 0) ? 1 : (uint32_t)grid;
-    F.hll_blocks = pl.hll_bytes ? std::min<uint32_t>(std::max<uint32_t>(pl.hll_bytes / 4096, 1) * 4, 64) : 0;
+    F.hll_blocks = pl.hll_bytes ? (pl.hll_bytes / 4 + 63) / 64 : 0;      // fin_prefix: 64 register words per block
     F.g_acc = t->d_acc.as<const unsigned long long>();
     F.g_pre = t->d_pre.as<unsigned long long>();
     F.g_hll_part = t->d_part.as<const uint8_t>();

@@ -55,7 +55,11 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
     return before;
 }
 
+constexpr uint32_t kFinSatSmem = 5632;     // u64 cells of a summed-area table done in shared memory
+constexpr uint32_t kFinHllWords = 64;      // register words per HLL merge block
+
 __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
+    __shared__ unsigned long long s_fin[kFinSatSmem];
     if (blockIdx.x < F.njobs) {
         const FinJob J = F.jobs[blockIdx.x];
         const unsigned long long *src = F.g_acc + J.src;
@@ -73,7 +77,26 @@ __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
                 run += src[i];
             }
             if (threadIdx.x == 0) dst[n] = total;
-        } else {   // JOB_SAT: summed-area table with a zero border, row stride nb + 1
+        } else if (J.na * J.nb <= kFinSatSmem) {   // JOB_SAT in shared memory (row, then column scans)
+            const uint32_t na = J.na, nb = J.nb, st = nb + 1;
+            unsigned long long *g = s_fin;
+            for (uint32_t i = threadIdx.x; i < na * nb; i += blockDim.x) g[i] = src[i];
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
+                unsigned long long run = 0;
+                for (uint32_t j = 0; j < nb; ++j) { run += g[i * nb + j]; g[i * nb + j] = run; }
+            }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j < nb; j += blockDim.x) {
+                unsigned long long run = 0;
+                for (uint32_t i = 0; i < na; ++i) { run += g[i * nb + j]; g[i * nb + j] = run; }
+            }
+            __syncthreads();
+            for (uint32_t k = threadIdx.x; k < (na + 1) * st; k += blockDim.x) {   // zero border, stride nb + 1
+                const uint32_t i = k / st, j = k - i * st;
+                dst[k] = (i && j) ? g[(i - 1) * nb + j - 1] : 0ull;
+            }
+        } else {   // JOB_SAT too large for shared memory: in global memory
             const uint32_t na = J.na, nb = J.nb, st = nb + 1;
             for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) dst[j] = 0;
             for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
@@ -93,23 +116,26 @@ __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
                 }
             }
         }
-    } else {   // HLL: byte-wise max over the per-CTA partials
+    } else {   // HLL: byte-wise max over the per-CTA partials, kFinHllWords words per block,
+               // the partials split over blockDim.x / kFinHllWords slices, then a tree max
         const uint32_t words = F.hll_bytes / 4;
-        const uint32_t b = blockIdx.x - F.njobs;
-        const uint32_t per = (words + F.hll_blocks - 1) / F.hll_blocks;
-        const uint32_t beg = b * per, end = min(words, beg + per);
+        const uint32_t w = (blockIdx.x - F.njobs) * kFinHllWords + threadIdx.x % kFinHllWords;
+        const uint32_t sl = threadIdx.x / kFinHllWords, nsl = blockDim.x / kFinHllWords;
         const uint32_t *part = reinterpret_cast<const uint32_t *>(F.g_hll_part);
-        for (uint32_t w = beg + threadIdx.x; w < end; w += blockDim.x) {
-            uint32_t m = 0;
-            for (uint32_t c = 0; c < F.nparts; ++c) m = __vmaxu4(m, part[(size_t)c * words + w]);
-            reinterpret_cast<uint32_t *>(F.out_regs)[w] = m;
+        uint32_t m = 0;
+        if (w < words)
+            for (uint32_t c = sl; c < F.nparts; c += nsl) m = __vmaxu4(m, part[(size_t)c * words + w]);
+        uint32_t *r = reinterpret_cast<uint32_t *>(s_fin);
+        r[threadIdx.x] = m;
+        __syncthreads();
+        for (uint32_t h = nsl / 2; h > 0; h /= 2) {
+            if (sl < h) r[threadIdx.x] = __vmaxu4(r[threadIdx.x], r[threadIdx.x + h * kFinHllWords]);
+            __syncthreads();
         }
+        if (sl == 0 && w < words) reinterpret_cast<uint32_t *>(F.out_regs)[w] = r[threadIdx.x];
     }
 }
 
-// HLL registers of a presence-bitmap column (one block each): every present value hashed
-// once, p = 12 registers in shared memory, then its block of the output registers.  Same
-// hash and index/rank convention as the probe (fmix32 for int32 keys, DESIGN.md §2 step 6).
 __global__ void __launch_bounds__(1024) fin_bitmap_hll(const FinParams F) {
     __shared__ uint32_t R[kHllM];
     const FinParams::BmJob J = F.bm[blockIdx.x];
