@@ -899,6 +899,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.bm_words = S.bm_words;
         Q.bm_goff = S.bm_goff;
         Q.bm_base = S.bm_base;
+        Q.bm_nvals = S.bm ? (uint32_t)((uint64_t)S.dh - (uint64_t)S.dl + 1) : 0u;
         Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
         Q.prim_b = (int8_t)S.prim_b;
@@ -1207,6 +1208,7 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
          chain([&](int i) { return std::string(P.slot[i].bm_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
     slot_u32("bmaddr", [](const SlotParams &Q) { return Q.bm_addr; });
     slot_u32("bmbase", [](const SlotParams &Q) { return (uint32_t)Q.bm_base; });
+    slot_u32("bmnv", [](const SlotParams &Q) { return Q.bm_nvals; });
     slot_u32("hllout", [](const SlotParams &Q) { return Q.hll_out; });
     slot_u32("sb", [](const SlotParams &Q) { return (uint32_t)Q.sb; });
     slot_u32("bmask", [](const SlotParams &Q) { return Q.bmask; });
@@ -1495,7 +1497,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
 
     const int grid = t->sms;
     // + merged HLL bound registers + merged presence bitmaps
-    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 16;
+    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 4ull * kMaxSlots + 16;
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
@@ -1518,6 +1520,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.g_acc = t->d_acc.as<unsigned long long>();
     P.g_hll_glob = t->d_acc.as<uint32_t>(8ull * pl.acc_words);
     P.g_bm = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes);
+    P.g_bmcnt = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords);
     P.g_hll_part = t->d_part.as<uint8_t>();
     P.g_nsamp = t->d_nsamp.as<unsigned long long>();
     P.thr = threshold_of(sample_rate);

@@ -137,6 +137,26 @@ __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s)
     return __reduce_min_sync(0xFFFFFFFFu, L);
 }
 
+// Presence-bitmap slot s: this warp ORs its 1/nwarps slice of the CTA's bitmap into the
+// merged bitmap g_bm, counting the bits it sets there for the first time, and reports
+// whether the merged bitmap now holds every value of the column domain.  The registers
+// depend only on the union of the bitmaps, so once it is complete no row can change the
+// result and the CTAs stop testing keys (exact; C4: after the first ~8 iterations).
+__device__ __noinline__ bool bm_push(const uint32_t *src, uint32_t *dst, uint32_t words, uint32_t *cnt,
+                                     uint32_t nvals) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t fresh = 0;
+    for (uint32_t i = warp * 32 + lane; i < words; i += kThreads) {
+        const uint32_t w = *reinterpret_cast<const volatile uint32_t *>(src + i);
+        if (w) fresh += __popc(w & ~atomicOr(dst + i, w));
+    }
+    fresh = __reduce_add_sync(0xFFFFFFFFu, fresh);
+    uint32_t total = 0;
+    if (lane == 0) total = fresh ? atomicAdd(cnt, fresh) + fresh : __ldcg(cnt);
+    total = __shfl_sync(0xFFFFFFFFu, total, 0);
+    return nvals && total >= nvals;
+}
+
 // #{t in bps : t <= v}, branch-free binary search (MODE_SEARCH fallback; out of line).
 __device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, int64_t v) {
     uint32_t lo = 0;
@@ -204,6 +224,7 @@ struct RtShape {
     __device__ static bool hllbm(const ProbeParams &P, int s) { return P.slot[s].bm_addr != kNone; }
     __device__ static uint32_t bmaddr(const ProbeParams &P, int s) { return P.slot[s].bm_addr; }
     __device__ static uint32_t bmbase(const ProbeParams &P, int s) { return (uint32_t)P.slot[s].bm_base; }
+    __device__ static uint32_t bmnv(const ProbeParams &P, int s) { return P.slot[s].bm_nvals; }
     __device__ static uint32_t hllout(const ProbeParams &P, int s) { return P.slot[s].hll_out; }
     __device__ static uint32_t sb(const ProbeParams &P, int s) { return P.slot[s].sb; }
     __device__ static uint32_t bmask(const ProbeParams &P, int s) { return P.slot[s].bmask; }
@@ -472,7 +493,8 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NC][4], uint32_t s,
 // column of a row quad.
 template <class Sh, int NK>
 __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_t keep, const uint32_t *wlim,
-                                            const KeyT<Sh> (&v)[4], const uint32_t (&bs)[4], const uint32_t (&ex)[4]) {
+                                            uint32_t bmfull, const KeyT<Sh> (&v)[4], const uint32_t (&bs)[4],
+                                            const uint32_t (&ex)[4]) {
     constexpr bool same = NK == 1;
     uint32_t *sm = smem32();
     const uint32_t dbg = Sh::dbg(P);
@@ -486,6 +508,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
     // which the rest of the loop leaves idle); survivors do a predicated ATOMS.MAX.
     if (Sh::hll(P, s) && Sh::hllbm(P, s) && !(dbg & 8)) {
+        if ((bmfull >> s) & 1u) return;        // merged bitmap complete: nothing left to record
         // presence bitmap: set the bit of each kept value (test first: after the first rows
         // nearly every value is present, so the quad costs four loads and no atomics)
         uint32_t wa[4], bit[4], need = 0;
@@ -614,7 +637,8 @@ __device__ __forceinline__ void pair_work(const ProbeParams &P, uint32_t keep, c
 constexpr uint32_t kNoUnit = 0xFFFFFFFFu;
 template <class Sh>
 __device__ __forceinline__ void quad_work(const ProbeParams &P, int4 (&r)[Sh::NC][Sh::I64 ? 2 : 1],
-                                          uint32_t keep, const uint32_t *wlim, uint32_t unext = kNoUnit) {
+                                          uint32_t keep, const uint32_t *wlim, uint32_t bmfull,
+                                          uint32_t unext = kNoUnit) {
     constexpr int NC = Sh::NC;
     uint32_t *sm = smem32();
     const uint32_t dbg = Sh::dbg(P);
@@ -633,10 +657,10 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, int4 (&r)[Sh::NC
         uint32_t ex[4];
         if (Sh::clust(P, s) && v[0] == v[1] && v[1] == v[2] && v[2] == v[3]) {
             bucket_col<Sh, 1>(P, s, v, bs[s], ex);
-            column_tail<Sh, 1>(P, s, keep, wlim, v, bs[s], ex);
+            column_tail<Sh, 1>(P, s, keep, wlim, bmfull, v, bs[s], ex);
         } else {
             bucket_col<Sh, 4>(P, s, v, bs[s], ex);
-            column_tail<Sh, 4>(P, s, keep, wlim, v, bs[s], ex);
+            column_tail<Sh, 4>(P, s, keep, wlim, bmfull, v, bs[s], ex);
         }
         if (unext != kNoUnit) load_col<Sh>(P, s, unext, r[s]);
     }
@@ -664,7 +688,7 @@ __device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
             rj[s][Sh::I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
         }
     }
-    quad_work<Sh>(P, rj, 1u, s_wlim[kThreads / 32]);
+    quad_work<Sh>(P, rj, 1u, s_wlim[kThreads / 32], 0u);
     return 1;
 }
 
@@ -686,6 +710,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     uint32_t kept = 0;
     uint32_t *wlim = s_wlim[threadIdx.x >> 5];
     uint32_t it = 0, next_refresh = 4;
+    uint32_t bmfull = 0;       // bit s: slot s's merged presence bitmap is complete (warp-uniform)
     auto body = [&](const Unit<Sh> &X, uint32_t u) {
         if (it == next_refresh) {
             next_refresh = it + min(it, 32u);
@@ -696,6 +721,10 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                         const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
                         if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
                     }
+                    else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
+                             bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
+                                     P.slot[s].bm_words, P.g_bmcnt + s, Sh::bmnv(P, s)))
+                        bmfull |= 1u << s;
                 __syncwarp();
             }
         }
@@ -716,7 +745,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 rj[s][0] = X.r[s][j][0];
                 if (Sh::I64) rj[s][Sh::I64 ? 1 : 0] = X.r[s][j][Sh::I64 ? 1 : 0];
             }
-            quad_work<Sh>(P, rj, keep, wlim);
+            quad_work<Sh>(P, rj, keep, wlim, bmfull);
         }
         ++it;
     };
@@ -753,13 +782,17 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                             const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
                             if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
                         }
+                        else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
+                                 bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
+                                         P.slot[s].bm_words, P.g_bmcnt + s, Sh::bmnv(P, s)))
+                            bmfull |= 1u << s;
                     __syncwarp();
                 }
             }
             ++it;
             if (Sh::SAMPLE) kept += __popc(keep);
             if (keep) {
-                quad_work<Sh>(P, r, keep, wlim, un);
+                quad_work<Sh>(P, r, keep, wlim, bmfull, un);
             } else if (un != kNoUnit) {        // nothing kept here: start the next unit's loads
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
