@@ -168,7 +168,7 @@ struct gace_table {
     // same batch skip planning and the H2D of the tables)
     std::string plan_key;
     std::shared_ptr<void> plan;
-    size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0;
+    size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0, o_hce = 0;
     // candidate-set probe (gace_probe_sets): plan cache and buffers
     std::string sets_key;
     std::shared_ptr<void> sets_plan;
@@ -397,6 +397,7 @@ struct Plan {
     std::vector<FinPred> fpreds;
     std::vector<FinPair> fpairs;
     std::vector<int64_t> bps;          // MODE_SEARCH breakpoints, concatenated
+    std::vector<uint8_t> hceil;        // HLL register ceilings, 4096 bytes per eligible column
     ProbeParams P{};
 };
 
@@ -900,6 +901,22 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.bm_goff = S.bm_goff;
         Q.bm_base = S.bm_base;
         Q.bm_nvals = S.bm ? (uint32_t)((uint64_t)S.dh - (uint64_t)S.dl + 1) : 0u;
+        // register ceilings: R[j] can never exceed the largest rank among the domain values
+        // with index j, so once the merged registers reach them the column is complete and
+        // the scan stops hashing its keys (int32 register columns, domains <= 2^25 values)
+        Q.hceil_off = kNone;
+        if (S.has_hll && !S.bm && S.dtype == GACE_I32 && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX) &&
+            (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL")) {
+            Q.hceil_off = (uint32_t)pl.hceil.size();
+            pl.hceil.resize(pl.hceil.size() + kHllM, 0);
+            uint8_t *ce = pl.hceil.data() + Q.hceil_off;
+            for (int64_t v = S.dl; v <= S.dh; ++v) {
+                const uint32_t h = host_fmix32((uint32_t)(int32_t)v);
+                const uint32_t r = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
+                uint8_t &c = ce[h >> (32 - kHllP)];
+                if (r > c) c = (uint8_t)r;
+            }
+        }
         Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
         Q.prim_b = (int8_t)S.prim_b;
@@ -1478,6 +1495,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         t->o_fp = off; off = align16(off + q.fpreds.size() * sizeof(FinPred));
         t->o_fq = off; off = align16(off + q.fpairs.size() * sizeof(FinPair));
         t->o_bps = off; off = align16(off + q.bps.size() * sizeof(int64_t));
+        t->o_hce = off; off = align16(off + q.hceil.size());
         t->blob = std::max<size_t>(off, 16);
         if (t->h_plan.ensure(t->blob) != cudaSuccess || t->d_plan.ensure(t->blob) != cudaSuccess)
             return fail(GACE_ENOMEM, "plan buffers");
@@ -1488,6 +1506,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         if (!q.fpreds.empty()) memcpy(hb + t->o_fp, q.fpreds.data(), q.fpreds.size() * sizeof(FinPred));
         if (!q.fpairs.empty()) memcpy(hb + t->o_fq, q.fpairs.data(), q.fpairs.size() * sizeof(FinPair));
         if (!q.bps.empty()) memcpy(hb + t->o_bps, q.bps.data(), q.bps.size() * sizeof(int64_t));
+        if (!q.hceil.empty()) memcpy(hb + t->o_hce, q.hceil.data(), q.hceil.size());
         CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, t->blob, cudaMemcpyHostToDevice, t->stream));
         t->plan = fresh;
         t->plan_key.swap(key);
@@ -1515,6 +1534,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     ProbeParams P = pl.P;
     P.image = t->d_plan.as<const uint4>(o_img);
     P.direct = t->d_plan.as<const DirectPair>(o_dir);
+    P.g_hceil = t->d_plan.as<const uint8_t>(t->o_hce);
     for (size_t i = 0; i < pl.slots.size(); ++i)
         if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
     P.g_acc = t->d_acc.as<unsigned long long>();

@@ -202,7 +202,7 @@ struct SlotParams {
     uint32_t bm_goff;       // word offset of this column's merged bitmap in g_bm
     uint32_t hll_out;       // output register block (ascending HLL column order)
     uint32_t bm_nvals;      // values in the column domain: the merged bitmap is complete at this count
-    uint32_t bm_pad;
+    uint32_t hceil_off;     // byte offset of the column's register ceilings in g_hceil, or kNone
     int64_t bm_base;        // multiple of 32
 };
 
@@ -243,6 +243,7 @@ struct ProbeParams {
     unsigned long long *g_nsamp;
     uint32_t *g_bm;                        // merged presence bitmaps (OR over CTAs; zeroed per probe)
     uint32_t *g_bmcnt;                     // [kMaxSlots] bits set in each merged bitmap (zeroed per probe)
+    const uint8_t *g_hceil;                // per-column HLL register ceilings (max rank over the domain)
     uint32_t *g_hll_glob;                  // u32[hll_bytes]: registers merged across CTAs while the
                                            // scan runs (max; zeroed per probe) -> HLL skip bound
     uint64_t nrows;                        // rows in this launch

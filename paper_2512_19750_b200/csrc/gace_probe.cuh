@@ -106,12 +106,16 @@ __device__ __forceinline__ void lds128_if(bool pred, const uint4 *addr, uint4 &r
 // merged registers only grow and every value in them came from some CTA's own rows, so a
 // key whose rank is <= L cannot change the final max: skipping it is exact.
 __shared__ uint8_t s_slmin[kMaxSlots][kThreads / 32];   // register values are < 64
+__shared__ uint8_t s_slfull[kMaxSlots][kThreads / 32];  // warp slice reached the register ceilings
 // Per-warp skip limit ~0 >> L (bit 0 cleared) of each HLL slot; row kThreads/32 stays ~1
 // (no skipping) for the tail rows.  Kept in shared memory (a broadcast load per use)
 // rather than in registers, which the hot loop needs for its keys.
 __shared__ uint32_t s_wlim[kThreads / 32 + 1][kMaxSlots];
 
-__device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s) {
+// Returns L | complete << 8: complete when ceil != nullptr and every warp's last slice check
+// found the merged registers at their ceilings (the largest rank any domain value can
+// give; registers only grow, so a slice once complete stays complete).
+__device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s, const uint8_t *ceil) {
     // this warp's registers: i = warp * 32 + lane + j * kThreads (the warps cover all 4096)
     constexpr uint32_t kNw = kThreads / 32, kPer = (kHllM + kThreads - 1) / kThreads;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -122,19 +126,28 @@ __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s)
     for (uint32_t j = 0; j < kPer; ++j)                  // all loads in flight at once
         glob[j] = i0 + j * kThreads < kHllM ? __ldcg(G + i0 + j * kThreads) : 0xFFFFFFFFu;
     uint32_t m = 0xFFFFFFFFu;
+    bool below = false;
 #pragma unroll
     for (uint32_t j = 0; j < kPer; ++j) {
         const uint32_t i = i0 + j * kThreads;
         if (i >= kHllM) break;
         const uint32_t mine = R[i];
         if (mine > glob[j]) atomicMax(G + i, mine);
-        m = min(m, max(mine, glob[j]));
+        const uint32_t merged = max(mine, glob[j]);
+        m = min(m, merged);
+        if (ceil && merged < __ldg(ceil + i)) below = true;
     }
     m = __reduce_min_sync(0xFFFFFFFFu, m);
-    if (lane == 0) s_slmin[s][warp] = (uint8_t)min(m, 255u);
+    const bool slice_full = ceil != nullptr && !__any_sync(0xFFFFFFFFu, below);
+    if (lane == 0) {
+        s_slmin[s][warp] = (uint8_t)min(m, 255u);
+        s_slfull[s][warp] = slice_full ? 1 : 0;
+    }
     __syncwarp();
     uint32_t L = lane < kNw ? *reinterpret_cast<volatile uint8_t *>(&s_slmin[s][lane]) : 0xFFFFFFFFu;
-    return __reduce_min_sync(0xFFFFFFFFu, L);
+    const bool f = lane < kNw ? *reinterpret_cast<volatile uint8_t *>(&s_slfull[s][lane]) != 0 : true;
+    const bool complete = ceil != nullptr && __all_sync(0xFFFFFFFFu, f);
+    return min(__reduce_min_sync(0xFFFFFFFFu, L), 255u) | (complete ? 256u : 0u);
 }
 
 // Presence-bitmap slot s: this warp ORs its 1/nwarps slice of the CTA's bitmap into the
@@ -528,6 +541,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
                     asm volatile("red.shared.or.b32 [%0], %1;" :: "r"(sbase() + wa[k]), "r"(bit[k]) : "memory");
         }
     } else if (Sh::hll(P, s) && !(dbg & 8)) {
+        if ((bmfull >> s) & 1u) return;        // registers at their ceilings: nothing can change
         uint32_t *R = sm + Sh::hllw(P, s);
         if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
             // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
@@ -701,6 +715,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     for (uint32_t i = P.image_u4 + threadIdx.x; i < P.smem_bytes / 16; i += blockDim.x)
         g_smem[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x < kMaxSlots * (kThreads / 32)) (&s_slmin[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxSlots * (kThreads / 32)) (&s_slfull[0][0])[threadIdx.x] = 0;
     if (threadIdx.x < kMaxSlots * (kThreads / 32 + 1)) (&s_wlim[0][0])[threadIdx.x] = 0xFFFFFFFEu;
     __syncthreads();
 
@@ -710,16 +725,21 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     uint32_t kept = 0;
     uint32_t *wlim = s_wlim[threadIdx.x >> 5];
     uint32_t it = 0, next_refresh = 4;
-    uint32_t bmfull = 0;       // bit s: slot s's merged presence bitmap is complete (warp-uniform)
+    uint32_t bmfull = 0;       // bit s: slot s's HLL is complete -- merged presence bitmap full, or
+                               // merged registers at their ceilings (warp-uniform)
     auto body = [&](const Unit<Sh> &X, uint32_t u) {
         if (it == next_refresh) {
             next_refresh = it + min(it, 32u);
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
-                    if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s)) {
-                        const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
+                    if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s) && !((bmfull >> s) & 1u)) {
+                        const uint32_t hc = P.slot[s].hceil_off;
+                        const uint32_t hb = hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s,
+                                                      hc != kNone ? P.g_hceil + hc : nullptr);
+                        const uint32_t L = min(hb & 255u, 31u);
                         if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
+                        if (hb >> 8) bmfull |= 1u << s;       // registers at their ceilings: column complete
                     }
                     else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
                              bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
@@ -778,9 +798,13 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
                     for (int s = 0; s < NC; ++s)
-                        if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s)) {
-                            const uint32_t L = min(hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s), 31u);
+                        if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s) && !((bmfull >> s) & 1u)) {
+                            const uint32_t hc = P.slot[s].hceil_off;
+                            const uint32_t hb = hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s,
+                                                          hc != kNone ? P.g_hceil + hc : nullptr);
+                            const uint32_t L = min(hb & 255u, 31u);
                             if ((threadIdx.x & 31) == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
+                            if (hb >> 8) bmfull |= 1u << s;       // registers at their ceilings: column complete
                         }
                         else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
                                  bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
