@@ -903,17 +903,28 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.bm_nvals = S.bm ? (uint32_t)((uint64_t)S.dh - (uint64_t)S.dl + 1) : 0u;
         // register ceilings: R[j] can never exceed the largest rank among the domain values
         // with index j, so once the merged registers reach them the column is complete and
-        // the scan stops hashing its keys (int32 register columns, domains <= 2^25 values)
+        // the scan stops hashing its keys (register columns, domains <= 2^25 values)
         Q.hceil_off = kNone;
-        if (S.has_hll && !S.bm && S.dtype == GACE_I32 && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX) &&
+        if (S.has_hll && !S.bm && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX) &&
             (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL")) {
             Q.hceil_off = (uint32_t)pl.hceil.size();
             pl.hceil.resize(pl.hceil.size() + kHllM, 0);
             uint8_t *ce = pl.hceil.data() + Q.hceil_off;
             for (int64_t v = S.dl; v <= S.dh; ++v) {
-                const uint32_t h = host_fmix32((uint32_t)(int32_t)v);
-                const uint32_t r = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
-                uint8_t &c = ce[h >> (32 - kHllP)];
+                uint32_t idx, r;
+                if (S.dtype == GACE_I32) {             // fmix32 (DESIGN.md §2 step 6)
+                    const uint32_t h = host_fmix32((uint32_t)(int32_t)v);
+                    idx = h >> (32 - kHllP);
+                    r = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
+                } else {                               // mix64(x + gamma)
+                    uint64_t z = (uint64_t)v + 0x9E3779B97F4A7C15ULL;
+                    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+                    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+                    z ^= z >> 31;
+                    idx = (uint32_t)(z >> (64 - kHllP));
+                    r = (uint32_t)__builtin_clzll((z << kHllP) | (1ull << (kHllP - 1))) + 1;
+                }
+                uint8_t &c = ce[idx];
                 if (r > c) c = (uint8_t)r;
             }
         }
