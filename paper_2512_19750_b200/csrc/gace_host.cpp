@@ -163,11 +163,16 @@ struct gace_table {
     cudaEvent_t ev[kNumEv]{};
     cudaEvent_t ev_copied[2]{}, ev_free[2]{}, ev_c0{}, ev_c1{};
     gace_timing last{};
+    // stage times are read from the events only when asked (gace_last_timing): 0 none,
+    // 1 probe (ev[0..5]), 2 candidate sets (no finalize stage); host tables add the copy span
+    int timing_kind = 0;
+    bool dirty = false;     // a call returned mid-way: its work may still be queued
     std::mutex mu;
     // plan cache: the last batch's plan and its uploaded device blob (repeated probes of the
     // same batch skip planning and the H2D of the tables)
     std::string plan_key;
     std::shared_ptr<void> plan;
+    void *jit_fn[2] = {nullptr, nullptr};   // specialised kernel of the cached plan (index: sampled)
     size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0, o_hce = 0;
     // candidate-set probe (gace_probe_sets): plan cache and buffers
     std::string sets_key;
@@ -1487,7 +1492,9 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (nh && !hll_regs) return fail(GACE_EINVAL, "hll_regs is NULL");
 
     CUDA_TRY(cudaSetDevice(t->device));
-    CUDA_TRY(cudaStreamSynchronize(t->stream));   // previous call fully done with the staging buffers
+    if (t->dirty) CUDA_TRY(cudaStreamSynchronize(t->stream));   // an aborted call's work is done
+    t->dirty = true;                                             // (a completed call synchronised)
+    t->timing_kind = 0;
     std::string key;
     key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 8);
     key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
@@ -1521,6 +1528,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, t->blob, cudaMemcpyHostToDevice, t->stream));
         t->plan = fresh;
         t->plan_key.swap(key);
+        t->jit_fn[0] = t->jit_fn[1] = nullptr;
     }
     const Plan &pl = *static_cast<const Plan *>(t->plan.get());
     const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
@@ -1577,13 +1585,17 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     int jit_used = 0;
     auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
         if (PP.nslots > 0 && (jm == 1 || (jm == 2 && n >= (1ull << 24)))) {
-            if (shape.empty()) {
-                std::vector<uint8_t> cl(pl.slots.size(), 0);
-                for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
-                shape = jit_shape_source(pl, sample, i64, cl);
-            }
             std::string err;
-            if (jit_launch(PP, t->device, shape, grid, s, &jit_ms, &err)) {
+            void *&fn = t->jit_fn[sample ? 1 : 0];
+            if (!fn) {
+                if (shape.empty()) {
+                    std::vector<uint8_t> cl(pl.slots.size(), 0);
+                    for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
+                    shape = jit_shape_source(pl, sample, i64, cl);
+                }
+                if (!jit_get(t->device, shape, &fn, &jit_ms, &err)) fn = nullptr;
+            }
+            if (fn && jit_launch_fn(fn, PP, grid, s, &err)) {
                 jit_used = 1;
                 return cudaSuccess;
             }
@@ -1697,18 +1709,10 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (nh) memcpy(hll_regs, t->h_out.as<uint8_t>(align16(8 * out_words)), pl.hll_bytes);
 
     gace_timing &T = t->last;
-    float ms;
-    cudaEventElapsedTime(&ms, t->ev[0], t->ev[1]); T.plan_upload_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[1], t->ev[2]); T.scan_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[2], t->ev[3]); T.finalize_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[3], t->ev[4]); T.merge_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[4], t->ev[5]); T.d2h_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[0], t->ev[5]); T.total_ms = ms;
-    if (t->host && t->nrows) {
-        cudaEventElapsedTime(&ms, t->ev_c0, t->ev_c1);
-        h2d_ms = ms;
-    }
-    T.h2d_ms = h2d_ms;
+    T = gace_timing{};
+    (void)h2d_ms;
+    t->timing_kind = 1;          // stage times from the events in gace_last_timing
+    t->dirty = false;
     T.scan_launches = launches;
     T.jit = jit_used;
     T.jit_compile_ms = jit_ms;
@@ -1738,7 +1742,9 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     if (t->host) return fail(GACE_EUNSUPPORTED, "gace_probe_sets needs a device table");
 
     CUDA_TRY(cudaSetDevice(t->device));
-    CUDA_TRY(cudaStreamSynchronize(t->stream));
+    if (t->dirty) CUDA_TRY(cudaStreamSynchronize(t->stream));
+    t->dirty = true;
+    t->timing_kind = 0;
     std::string key;
     key.append(reinterpret_cast<const char *>(&nsets), 4);
     if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
@@ -1807,12 +1813,8 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
 
     gace_timing &T = t->last;
     T = gace_timing{};
-    float ms;
-    cudaEventElapsedTime(&ms, t->ev[0], t->ev[1]); T.plan_upload_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[1], t->ev[2]); T.scan_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[3], t->ev[4]); T.merge_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[4], t->ev[5]); T.d2h_ms = ms;
-    cudaEventElapsedTime(&ms, t->ev[0], t->ev[5]); T.total_ms = ms;
+    t->timing_kind = 2;
+    t->dirty = false;
     T.scan_launches = launches;
     T.bytes_scanned = t->nrows * pl.bytes_per_row;
     return GACE_OK;
@@ -2034,6 +2036,17 @@ gace_status gace_last_timing(const gace_table *t, gace_timing *out) {
     if (st) return st;
     if (!out) return fail(GACE_EINVAL, "out is NULL");
     *out = t->last;
+    if (t->timing_kind) {        // the call synchronised its stream: every event has completed
+        float ms;
+        cudaSetDevice(t->device);
+        cudaEventElapsedTime(&ms, t->ev[0], t->ev[1]); out->plan_upload_ms = ms;
+        cudaEventElapsedTime(&ms, t->ev[1], t->ev[2]); out->scan_ms = ms;
+        if (t->timing_kind == 1) { cudaEventElapsedTime(&ms, t->ev[2], t->ev[3]); out->finalize_ms = ms; }
+        cudaEventElapsedTime(&ms, t->ev[3], t->ev[4]); out->merge_ms = ms;
+        cudaEventElapsedTime(&ms, t->ev[4], t->ev[5]); out->d2h_ms = ms;
+        cudaEventElapsedTime(&ms, t->ev[0], t->ev[5]); out->total_ms = ms;
+        if (t->timing_kind == 1 && t->host && t->nrows) { cudaEventElapsedTime(&ms, t->ev_c0, t->ev_c1); out->h2d_ms = ms; }
+    }
     return GACE_OK;
 }
 

@@ -20,6 +20,12 @@ bool jit_available(std::string *why);
 bool jit_launch(const ProbeParams &P, int device, const std::string &shape_src, int grid, cudaStream_t s,
                 double *compile_ms, std::string *err);
 
+// The specialised kernel for (device, shape), compiled and cached on first use; and a launch
+// of a kernel obtained that way (tables keep the handle of their cached plan, so repeated
+// probes skip regenerating the shape source and the cache lookup).
+bool jit_get(int device, const std::string &shape_src, void **fn, double *compile_ms, std::string *err);
+bool jit_launch_fn(void *fn, const ProbeParams &P, int grid, cudaStream_t s, std::string *err);
+
 // NVRTC compile only (no device needed): the test hook gace_debug_jit_compile.
 bool jit_compile_check(const std::string &shape_src, size_t *cubin_bytes, std::string *err);
 
