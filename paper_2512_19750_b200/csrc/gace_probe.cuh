@@ -21,6 +21,9 @@
 #ifndef GACE_PREFETCH
 #define GACE_PREFETCH 0
 #endif
+#ifndef GACE_L2_PREFETCH
+#define GACE_L2_PREFETCH 1
+#endif
 
 namespace gace {
 
@@ -790,6 +793,21 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 if (Sh::active(P, s)) load_col<Sh>(P, s, u, r[s]);
         }
         for (; u < nunits; u += stride) {
+#if GACE_L2_PREFETCH
+            // keys two iterations ahead pulled into L2 (one PREFETCH per column: the warp's 32
+            // lanes cover 512 contiguous bytes), so the register loads of the next iteration
+            // hit L2 (full scans only: a sampled probe must not fetch the rows it skips)
+            if (!Sh::SAMPLE && u + 2 * stride < nunits) {
+#pragma unroll
+                for (int s = 0; s < NC; ++s) {
+                    if (!Sh::active(P, s)) continue;
+                    const uint32_t w = Sh::is32(P, s) ? 16u : 32u;
+                    const char *a = static_cast<const char *>(P.slot[s].ptr) + (uint64_t)(u + 2 * stride) * w;
+                    asm volatile("prefetch.global.L2 [%0];" :: "l"(a));
+                    if (w == 32u) asm volatile("prefetch.global.L2 [%0];" :: "l"(a + 16));
+                }
+            }
+#endif
             uint32_t un = u + stride < nunits ? u + stride : kNoUnit;
             const uint32_t keep_n = un != kNoUnit ? quad_keep(un) : 0u;
             if (!keep_n) un = kNoUnit;
