@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graphs", action="store_true",
+                    help="replay each repeated probe as a CUDA graph (gace_table_set_graphs; side stream)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -210,8 +212,13 @@ def main():
         cols = [c if len(c) == nloc else torch.zeros(nloc, dtype=c.dtype, device="cuda") for c in cols]
     torch.cuda.synchronize()
     dinfo = gdist.dist_info(w.nrows) if world > 1 else None
+    if args.graphs:                    # graphs need a capturable (non-legacy) stream
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
     stream = torch.cuda.current_stream()
     table = gace.Table(cols, dist=dinfo, stream=stream)
+    if args.graphs:
+        table.set_graphs(True)
 
     flush = None
     if nloc * w.bytes_per_row < 2 * L2_BYTES:
@@ -281,6 +288,7 @@ def main():
             w.columns[c].dtype == "i32" for c in probed) else "int32/int64",
         "data": "synthetic",
         "config": dict(describe(w), parallelism=f"dp{world}: contiguous row shards, NCCL sum/max merge",
+                       cuda_graphs=bool(args.graphs),
                        l2=("flushed between steps (2x L2 buffer write)" if flush is not None
                            else f"inputs larger than L2 ({nloc * w.bytes_per_row / 1e9:.2f} GB per GPU)")),
         "hbm_gbs": w.nrows * w.bytes_per_row / (ms_per_step * 1e-3) / 1e9,

@@ -129,6 +129,20 @@ gace_status gace_table_attach_host(const void *const *col_host_ptrs, const gace_
 gace_status gace_table_detach(gace_table *t);
 
 /*
+ * CUDA-graph replay of repeated probes (graph half; BJ:5-11: the
+ * probe's fixed per-call cost).  enable != 0: on a device table attached on a non-default
+ * stream with one rank, the second gace_probe with the same plan (predicates, pairs, HLL
+ * mask), sample_rate, seed and scratch buffers captures the probe's device work (memsets,
+ * scan, finalize, result D2H, stage events) into one graph; later identical calls launch
+ * that graph.  Results are the same as without graphs (the same kernels run); host tables,
+ * multi-rank tables and the legacy default stream always run eagerly.  enable == 0 frees
+ * the graph.  Default: disabled.  Errors: GACE_EHANDLE on an invalid handle.
+ * gace_table_graph_stats: captures and replays so far (either pointer may be NULL).
+ */
+gace_status gace_table_set_graphs(gace_table *t, int enable);
+gace_status gace_table_graph_stats(const gace_table *t, uint64_t *captures, uint64_t *replays);
+
+/*
  * The probe (north star: counts, joint_counts, hll_regs).
  *   preds[npreds], pairs[npairs]   host arrays (validated before any launch)
  *   sample_rate                    in [0,1]; 1 = every row (NaN / out of range: EINVAL)

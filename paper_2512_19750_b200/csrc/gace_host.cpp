@@ -138,6 +138,25 @@ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 }  // namespace
 
 constexpr uint32_t kMagic = 0x47414345u;   // "GACE"
+
+// what a captured probe graph bakes in: plan, sampling, seed, ablation bits, scratch buffers
+struct GraphKey {
+    uint64_t plan = 0;       // plan generation of the table (never reused, unlike addresses)
+    double rate = 0;
+    uint64_t seed = 0;
+    uint32_t dbg = 0;
+    const void *buf[7] = {};
+    GraphKey() = default;
+    GraphKey(uint64_t pl, double r, uint64_t sd, uint32_t d, const void *a, const void *b, const void *c,
+             const void *e, const void *f, const void *g, const void *h)
+        : plan(pl), rate(r), seed(sd), dbg(d), buf{a, b, c, e, f, g, h} {}
+    bool operator==(const GraphKey &o) const {
+        if (plan != o.plan || rate != o.rate || seed != o.seed || dbg != o.dbg) return false;
+        for (int i = 0; i < 7; ++i)
+            if (buf[i] != o.buf[i]) return false;
+        return true;
+    }
+};
 constexpr int kNumEv = 8;
 
 struct gace_table {
@@ -173,6 +192,14 @@ struct gace_table {
     std::string plan_key;
     std::shared_ptr<void> plan;
     void *jit_fn[2] = {nullptr, nullptr};   // specialised kernel of the cached plan (index: sampled)
+    // CUDA-graph replay of repeated identical probes (gace_table_set_graphs)
+    bool graphs = false;
+    uint64_t plan_gen = 0;
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey, gprev;
+    bool gprev_ok = false;
+    uint64_t g_scan_launches = 0, g_nl = 0, g_captures = 0, g_replays = 0;
+    int g_jit = 0;
     size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0, o_hce = 0;
     // candidate-set probe (gace_probe_sets): plan cache and buffers
     std::string sets_key;
@@ -1466,6 +1493,7 @@ gace_status gace_table_detach(gace_table *t) {
     }
     if (t->ev_c0) cudaEventDestroy(t->ev_c0);
     if (t->ev_c1) cudaEventDestroy(t->ev_c1);
+    if (t->gexec) cudaGraphExecDestroy(t->gexec);
     t->d_plan.release(); t->d_acc.release(); t->d_pre.release(); t->d_part.release();
     t->d_out.release(); t->d_nsamp.release(); t->d_mask.release();
     t->h_plan.release(); t->h_out.release();
@@ -1474,6 +1502,29 @@ gace_status gace_table_detach(gace_table *t) {
     if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
     t->magic = 0;
     delete t;
+    return GACE_OK;
+}
+
+gace_status gace_table_set_graphs(gace_table *t, int enable) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    std::lock_guard<std::mutex> lock(t->mu);
+    t->graphs = enable != 0;
+    t->gprev_ok = false;
+    if (!t->graphs && t->gexec) {
+        cudaSetDevice(t->device);
+        if (t->stream) cudaStreamSynchronize(t->stream);
+        cudaGraphExecDestroy(t->gexec);
+        t->gexec = nullptr;
+    }
+    return GACE_OK;
+}
+
+gace_status gace_table_graph_stats(const gace_table *t, uint64_t *captures, uint64_t *replays) {
+    gace_status st = check_table(t);
+    if (st) return st;
+    if (captures) *captures = t->g_captures;
+    if (replays) *replays = t->g_replays;
     return GACE_OK;
 }
 
@@ -1528,6 +1579,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, t->blob, cudaMemcpyHostToDevice, t->stream));
         t->plan = fresh;
         t->plan_key.swap(key);
+        t->plan_gen++;
         t->jit_fn[0] = t->jit_fn[1] = nullptr;
     }
     const Plan &pl = *static_cast<const Plan *>(t->plan.get());
@@ -1545,10 +1597,45 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         return fail(GACE_ENOMEM, "probe scratch");
 
     cudaStream_t s = t->stream;
-    CUDA_TRY(cudaEventRecord(t->ev[0], s));
+    // CUDA-graph replay (gace_table_set_graphs): the second call with the same plan, sample,
+    // seed and scratch buffers captures the enqueue below (memsets, scan, finalize, D2H and
+    // the stage events as external records); later identical calls launch the graph.
+    uint64_t nl = 0;                 // our kernel launches enqueued by this call
+    uint64_t launches = 0;
+    double jit_ms = 0;
+    int jit_used = 0;
+    uint64_t bytes_per_row = 0;
+    for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
+    const char *ab_env = getenv("GACE_ABLATE");
+    GraphKey gk{t->plan_gen, sample_rate, seed, ab_env ? (uint32_t)strtoul(ab_env, nullptr, 0) : 0u,
+                t->d_acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, t->d_nsamp.p, t->d_plan.p};
+    const bool use_graph = t->graphs && !t->host && t->nrows > 0 && s != nullptr &&
+                           !(t->has_dist && t->dist.nranks > 1);
+    const bool replay = use_graph && t->gexec && gk == t->gkey;
+    bool capt = use_graph && !replay && t->gprev_ok && gk == t->gprev;
+    if (use_graph && !replay) {
+        t->gprev = gk;
+        t->gprev_ok = true;
+    }
+    if (replay) {
+        CUDA_TRY(cudaGraphLaunch(t->gexec, s));
+        launches = t->g_scan_launches;
+        jit_used = t->g_jit;
+        g_launches += t->g_nl;
+        t->g_replays++;
+    } else {
+    if (capt && cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+        (void)cudaGetLastError();
+        capt = false;
+    }
+    auto rec = [&](cudaEvent_t e, cudaStream_t st) {
+        return capt ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+    };
+    const gace_status est = [&]() -> gace_status {
+    CUDA_TRY(rec(t->ev[0], s));
     CUDA_TRY(cudaMemsetAsync(t->d_acc.p, 0, acc_bytes, s));
     CUDA_TRY(cudaMemsetAsync(t->d_nsamp.p, 0, 8, s));
-    CUDA_TRY(cudaEventRecord(t->ev[1], s));
+    CUDA_TRY(rec(t->ev[1], s));
 
     ProbeParams P = pl.P;
     P.image = t->d_plan.as<const uint4>(o_img);
@@ -1565,24 +1652,18 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
-    if (const char *ab = getenv("GACE_ABLATE")) P.dbg = (uint32_t)strtoul(ab, nullptr, 0);   // design experiments only
+    if (ab_env) P.dbg = (uint32_t)strtoul(ab_env, nullptr, 0);   // design experiments only
     const bool sample = sample_rate < 1.0;
     bool i64 = false;
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
-    uint64_t bytes_per_row = 0;
-    for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
 
     // rows per launch: keep every CTA's u32 bins below 2^31
     // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
     const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
-    uint64_t launches = 0;
-    double h2d_ms = 0;
     // specialised (NVRTC) kernel for large launches, generic precompiled kernel otherwise
     const int jm = jit_mode();
     std::string shape;
-    double jit_ms = 0;
-    int jit_used = 0;
     auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
         if (PP.nslots > 0 && (jm == 1 || (jm == 2 && n >= (1ull << 24)))) {
             std::string err;
@@ -1654,8 +1735,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         }
         CUDA_TRY(cudaEventRecord(t->ev_c1, t->copy_stream));
     }
-    g_launches += launches;
-    CUDA_TRY(cudaEventRecord(t->ev[2], s));
+    nl += launches;
+    CUDA_TRY(rec(t->ev[2], s));
 
     FinParams F{};
     F.jobs = t->d_plan.as<const FinJob>(o_job);
@@ -1685,8 +1766,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         J.base = S.bm_base;
     }
     CUDA_TRY(launch_finalize(F, s));
-    g_launches += (F.njobs + F.hll_blocks ? 2 : 1) + (F.nbm ? 1 : 0);
-    CUDA_TRY(cudaEventRecord(t->ev[3], s));
+    nl += (F.njobs + F.hll_blocks ? 2 : 1) + (F.nbm ? 1 : 0);
+    CUDA_TRY(rec(t->ev[3], s));
 
     if (t->has_dist && t->dist.nranks > 1) {
         Nccl *n = nccl();
@@ -1697,9 +1778,38 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         int r3 = n->GroupEnd();
         if (r1 || r2 || r3) return fail(GACE_ENCCL, "ncclAllReduce failed");
     }
-    CUDA_TRY(cudaEventRecord(t->ev[4], s));
+    CUDA_TRY(rec(t->ev[4], s));
     CUDA_TRY(cudaMemcpyAsync(t->h_out.p, t->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaEventRecord(t->ev[5], s));
+    CUDA_TRY(rec(t->ev[5], s));
+    return GACE_OK;
+    }();
+    if (capt) {
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (est) {
+            if (g) cudaGraphDestroy(g);
+            return est;
+        }
+        if (ce != cudaSuccess || !g) return fail(GACE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        if (t->gexec) cudaGraphExecDestroy(t->gexec);
+        t->gexec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&t->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            t->gexec = nullptr;
+            return fail(GACE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+        }
+        t->gkey = gk;
+        t->g_scan_launches = launches;
+        t->g_jit = jit_used;
+        t->g_nl = nl;
+        t->g_captures++;
+        CUDA_TRY(cudaGraphLaunch(t->gexec, s));
+    } else if (est) {
+        return est;
+    }
+    g_launches += nl;
+    }
     CUDA_TRY(cudaStreamSynchronize(s));
 
     const uint64_t *ho = t->h_out.as<uint64_t>();
@@ -1710,7 +1820,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
 
     gace_timing &T = t->last;
     T = gace_timing{};
-    (void)h2d_ms;
     t->timing_kind = 1;          // stage times from the events in gace_last_timing
     t->dirty = false;
     T.scan_launches = launches;

@@ -32,7 +32,8 @@ HLL_M = 1 << HLL_P
 PRED_DTYPE = np.dtype([("col", "<u4"), ("op", "<u2"), ("flags", "<u2"), ("a", "<i8"), ("b", "<i8")])
 PAIR_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4")])
 
-EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv", "gace_cache_create", "gace_cache_destroy", "gace_cache_put",
+EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "gace_table_set_graphs",
+           "gace_table_graph_stats", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv", "gace_cache_create", "gace_cache_destroy", "gace_cache_put",
            "gace_cache_lookup", "gace_cache_invalidate", "gace_cache_stats",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
            "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
@@ -89,6 +90,8 @@ def lib() -> ctypes.CDLL:
     L.gace_table_attach.argtypes = [vp, vp, u32, u64, vp, i32, vp, ctypes.POINTER(vp)]
     L.gace_table_attach_host.argtypes = [vp, vp, u32, u64, vp, i32, vp, ctypes.POINTER(vp)]
     L.gace_table_detach.argtypes = [vp]
+    L.gace_table_set_graphs.argtypes = [vp, i32]
+    L.gace_table_graph_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
     L.gace_probe.argtypes = [vp, vp, u32, vp, u32, dbl, u64, u64, u32, ctypes.POINTER(u64), vp, vp, vp]
     L.gace_sample_mask.argtypes = [vp, dbl, u64, vp]
     L.gace_cache_create.argtypes = [u32, u32, ctypes.POINTER(vp)]
@@ -332,6 +335,16 @@ class Table:
         _check(lib().gace_sample_mask(self._h, float(sample_rate), int(seed) & ((1 << 64) - 1),
                                       bits.ctypes.data))
         return bits[:(self.nrows + 63) // 64]
+
+    def set_graphs(self, enable: bool = True):
+        """gace_table_set_graphs: CUDA-graph replay of repeated identical probes."""
+        _check(lib().gace_table_set_graphs(self._h, 1 if enable else 0))
+
+    def graph_stats(self) -> tuple[int, int]:
+        """gace_table_graph_stats: (captures, replays)."""
+        c, r = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _check(lib().gace_table_graph_stats(self._h, ctypes.byref(c), ctypes.byref(r)))
+        return c.value, r.value
 
     def last_timing(self) -> dict:
         t = _Timing()
