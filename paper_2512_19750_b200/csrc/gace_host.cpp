@@ -1752,8 +1752,13 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.npreds = npreds;
     F.pairs = t->d_plan.as<const FinPair>(o_fq);
     F.npairs = npairs;
-    F.out = t->d_out.as<unsigned long long>();
-    F.out_regs = t->d_out.as<uint8_t>(align16(8 * out_words));
+    // one rank: the finalize kernels write the packed result straight into the pinned host
+    // buffer (mapped under UVA, same address), so no D2H copy is queued; with several ranks
+    // the result stays on the device for the NCCL merge and is copied back after it
+    const bool zero_copy = !(t->has_dist && t->dist.nranks > 1) && !getenv("GACE_NO_ZERO_COPY");
+    char *out_base = zero_copy ? t->h_out.as<char>() : t->d_out.as<char>();
+    F.out = reinterpret_cast<unsigned long long *>(out_base);
+    F.out_regs = reinterpret_cast<uint8_t *>(out_base + align16(8 * out_words));
     F.g_bm = P.g_bm;
     F.nbm = 0;
     for (auto &S : pl.slots) {
@@ -1779,7 +1784,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         if (r1 || r2 || r3) return fail(GACE_ENCCL, "ncclAllReduce failed");
     }
     CUDA_TRY(rec(t->ev[4], s));
-    CUDA_TRY(cudaMemcpyAsync(t->h_out.p, t->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s));
+    if (!zero_copy) CUDA_TRY(cudaMemcpyAsync(t->h_out.p, t->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(rec(t->ev[5], s));
     return GACE_OK;
     }();
