@@ -1587,13 +1587,15 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
 
     const int grid = t->sms;
     // + merged HLL bound registers + merged presence bitmaps
-    const size_t acc_bytes = 8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 4ull * kMaxSlots + 16;
+    // + n_sampled counter at the end, so one memset clears the whole accumulator
+    const size_t nsamp_off = align16(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 4ull * kMaxSlots + 16);
+    const size_t acc_bytes = nsamp_off + 16;
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
     if (t->d_acc.ensure(acc_bytes) != cudaSuccess || t->d_pre.ensure(std::max<size_t>(8ull * pl.pre_words, 8)) != cudaSuccess ||
         t->d_part.ensure(part_bytes) != cudaSuccess || t->d_out.ensure(out_bytes) != cudaSuccess ||
-        t->d_nsamp.ensure(8) != cudaSuccess || t->h_out.ensure(out_bytes) != cudaSuccess)
+        t->h_out.ensure(out_bytes) != cudaSuccess)
         return fail(GACE_ENOMEM, "probe scratch");
 
     cudaStream_t s = t->stream;
@@ -1608,7 +1610,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
     const char *ab_env = getenv("GACE_ABLATE");
     GraphKey gk{t->plan_gen, sample_rate, seed, ab_env ? (uint32_t)strtoul(ab_env, nullptr, 0) : 0u,
-                t->d_acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, t->d_nsamp.p, t->d_plan.p};
+                t->d_acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, nullptr, t->d_plan.p};
     const bool use_graph = t->graphs && !t->host && t->nrows > 0 && s != nullptr &&
                            !(t->has_dist && t->dist.nranks > 1);
     const bool replay = use_graph && t->gexec && gk == t->gkey;
@@ -1634,7 +1636,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const gace_status est = [&]() -> gace_status {
     CUDA_TRY(rec(t->ev[0], s));
     CUDA_TRY(cudaMemsetAsync(t->d_acc.p, 0, acc_bytes, s));
-    CUDA_TRY(cudaMemsetAsync(t->d_nsamp.p, 0, 8, s));
     CUDA_TRY(rec(t->ev[1], s));
 
     ProbeParams P = pl.P;
@@ -1648,7 +1649,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.g_bm = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes);
     P.g_bmcnt = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords);
     P.g_hll_part = t->d_part.as<uint8_t>();
-    P.g_nsamp = t->d_nsamp.as<unsigned long long>();
+    P.g_nsamp = t->d_acc.as<unsigned long long>(nsamp_off);
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
@@ -1747,7 +1748,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.g_acc = t->d_acc.as<const unsigned long long>();
     F.g_pre = t->d_pre.as<unsigned long long>();
     F.g_hll_part = t->d_part.as<const uint8_t>();
-    F.g_nsamp = t->d_nsamp.as<const unsigned long long>();
+    F.g_nsamp = t->d_acc.as<const unsigned long long>(nsamp_off);
     F.preds = t->d_plan.as<const FinPred>(o_fp);
     F.npreds = npreds;
     F.pairs = t->d_plan.as<const FinPair>(o_fq);

@@ -58,8 +58,15 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
 constexpr uint32_t kFinSatSmem = 5632;     // u64 cells of a summed-area table done in shared memory
 constexpr uint32_t kFinHllWords = 64;      // register words per HLL merge block
 
+// Programmatic dependent launch: the finalize kernels are launched with programmatic stream
+// serialisation, so their launch overlaps the previous kernel's tail; each waits here for
+// the previous grid to complete (no early trigger: its writes are all visible) before
+// touching anything it produced.  A no-op when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
     __shared__ unsigned long long s_fin[kFinSatSmem];
+    pdl_wait();
     if (blockIdx.x < F.njobs) {
         const FinJob J = F.jobs[blockIdx.x];
         const unsigned long long *src = F.g_acc + J.src;
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(1024) fin_prefix(const FinParams F) {
 
 __global__ void __launch_bounds__(1024) fin_bitmap_hll(const FinParams F) {
     __shared__ uint32_t R[kHllM];
+    pdl_wait();
     const FinParams::BmJob J = F.bm[blockIdx.x];
     for (uint32_t i = threadIdx.x; i < kHllM; i += blockDim.x) R[i] = 0;
     __syncthreads();
@@ -185,6 +193,7 @@ __device__ __forceinline__ unsigned long long combine(unsigned long long n, unsi
 }
 
 __global__ void fin_output(const FinParams F) {
+    pdl_wait();
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long n = *F.g_nsamp;
     if (t == 0) F.out[0] = n;
@@ -292,21 +301,33 @@ cudaError_t launch_probe(const ProbeParams &P, bool sample, bool i64, int grid, 
     return launch_nc<8>(P, sample, i64, grid, s);
 }
 
+template <class K>
+static cudaError_t launch_pdl(K kern, unsigned blocks, unsigned threads, cudaStream_t s, const FinParams &F) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, F);
+}
+
 cudaError_t launch_finalize(const FinParams &F, cudaStream_t s) {
     const uint32_t blocks = F.njobs + F.hll_blocks;
     if (blocks) {
-        fin_prefix<<<blocks, 1024, 0, s>>>(F);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(fin_prefix, blocks, 1024, s, F);
         if (e != cudaSuccess) return e;
     }
     if (F.nbm) {                         // after fin_prefix wrote the register blocks
-        fin_bitmap_hll<<<F.nbm, 1024, 0, s>>>(F);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(fin_bitmap_hll, F.nbm, 1024, s, F);
         if (e != cudaSuccess) return e;
     }
     const uint32_t outs = 1 + F.npreds + F.npairs;
-    fin_output<<<(outs + 255) / 256, 256, 0, s>>>(F);
-    return cudaGetLastError();
+    return launch_pdl(fin_output, (outs + 255) / 256, 256, s, F);
 }
 
 cudaError_t launch_minmax(const void *col, int dtype, uint64_t n, long long *mm, int sms, cudaStream_t s) {
