@@ -21,6 +21,9 @@
 #ifndef GACE_PREFETCH
 #define GACE_PREFETCH 0
 #endif
+#ifndef GACE_L2_PF_DIST
+#define GACE_L2_PF_DIST 2      // L2 prefetch distance in grid-stride iterations
+#endif
 #ifndef GACE_L2_PREFETCH
 #define GACE_L2_PREFETCH 1
 #endif
@@ -797,12 +800,12 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             // keys two iterations ahead pulled into L2 (one PREFETCH per column: the warp's 32
             // lanes cover 512 contiguous bytes), so the register loads of the next iteration
             // hit L2 (full scans only: a sampled probe must not fetch the rows it skips)
-            if (!Sh::SAMPLE && u + 2 * stride < nunits) {
+            if (!Sh::SAMPLE && u + GACE_L2_PF_DIST * stride < nunits) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s) {
                     if (!Sh::active(P, s)) continue;
                     const uint32_t w = Sh::is32(P, s) ? 16u : 32u;
-                    const char *a = static_cast<const char *>(P.slot[s].ptr) + (uint64_t)(u + 2 * stride) * w;
+                    const char *a = static_cast<const char *>(P.slot[s].ptr) + (uint64_t)(u + GACE_L2_PF_DIST * stride) * w;
                     asm volatile("prefetch.global.L2 [%0];" :: "l"(a));
                     if (w == 32u) asm volatile("prefetch.global.L2 [%0];" :: "l"(a + 16));
                 }
