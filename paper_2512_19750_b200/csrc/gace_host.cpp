@@ -176,7 +176,7 @@ struct gace_table {
     void *comm = nullptr;
     bool own_comm = false;
     int sms = 148;
-    DevBuf d_plan, d_acc, d_pre, d_part, d_out, d_nsamp, d_mask, d_stage[2];
+    DevBuf d_plan, d_accb[2], d_pre, d_part, d_out, d_nsamp, d_mask, d_stage[2];
     HostBuf h_plan, h_out;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[kNumEv]{};
@@ -195,6 +195,10 @@ struct gace_table {
     // CUDA-graph replay of repeated identical probes (gace_table_set_graphs)
     bool graphs = false;
     uint64_t plan_gen = 0;
+    // double-buffered accumulators: each call's fin_output zeroes the other buffer, so the
+    // next call needs no memset (a buffer is "clean" only after a call that zeroed it completed)
+    int acc_next = 0;
+    bool acc_clean[2] = {false, false};
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey, gprev;
     bool gprev_ok = false;
@@ -1494,7 +1498,7 @@ gace_status gace_table_detach(gace_table *t) {
     if (t->ev_c0) cudaEventDestroy(t->ev_c0);
     if (t->ev_c1) cudaEventDestroy(t->ev_c1);
     if (t->gexec) cudaGraphExecDestroy(t->gexec);
-    t->d_plan.release(); t->d_acc.release(); t->d_pre.release(); t->d_part.release();
+    t->d_plan.release(); t->d_accb[0].release(); t->d_accb[1].release(); t->d_pre.release(); t->d_part.release();
     t->d_out.release(); t->d_nsamp.release(); t->d_mask.release();
     t->h_plan.release(); t->h_out.release();
     t->d_sets_img.release(); t->d_sets_out.release(); t->h_sets_img.release(); t->h_sets_out.release();
@@ -1593,7 +1597,16 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
-    if (t->d_acc.ensure(acc_bytes) != cudaSuccess || t->d_pre.ensure(std::max<size_t>(8ull * pl.pre_words, 8)) != cudaSuccess ||
+    const bool use_graph = t->graphs && !t->host && t->nrows > 0 && t->stream != nullptr &&
+                           !(t->has_dist && t->dist.nranks > 1);
+    // graphs bake in one accumulator buffer and keep the memset; eager calls alternate
+    const bool dbuf = !use_graph && !getenv("GACE_NO_ACC_DBUF");
+    const int ab = dbuf ? t->acc_next : 0, ob = ab ^ 1;
+    DevBuf &acc = t->d_accb[ab];
+    const bool need_memset = !(dbuf && t->acc_clean[ab] && acc.cap >= acc_bytes);
+    t->acc_clean[0] = t->acc_clean[1] = false;
+    if (dbuf && t->d_accb[ob].ensure(acc_bytes) != cudaSuccess) return fail(GACE_ENOMEM, "probe scratch");
+    if (acc.ensure(acc_bytes) != cudaSuccess || t->d_pre.ensure(std::max<size_t>(8ull * pl.pre_words, 8)) != cudaSuccess ||
         t->d_part.ensure(part_bytes) != cudaSuccess || t->d_out.ensure(out_bytes) != cudaSuccess ||
         t->h_out.ensure(out_bytes) != cudaSuccess)
         return fail(GACE_ENOMEM, "probe scratch");
@@ -1610,9 +1623,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
     const char *ab_env = getenv("GACE_ABLATE");
     GraphKey gk{t->plan_gen, sample_rate, seed, ab_env ? (uint32_t)strtoul(ab_env, nullptr, 0) : 0u,
-                t->d_acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, nullptr, t->d_plan.p};
-    const bool use_graph = t->graphs && !t->host && t->nrows > 0 && s != nullptr &&
-                           !(t->has_dist && t->dist.nranks > 1);
+                acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, nullptr, t->d_plan.p};
     const bool replay = use_graph && t->gexec && gk == t->gkey;
     bool capt = use_graph && !replay && t->gprev_ok && gk == t->gprev;
     if (use_graph && !replay) {
@@ -1635,7 +1646,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     };
     const gace_status est = [&]() -> gace_status {
     CUDA_TRY(rec(t->ev[0], s));
-    CUDA_TRY(cudaMemsetAsync(t->d_acc.p, 0, acc_bytes, s));
+    if (need_memset) CUDA_TRY(cudaMemsetAsync(acc.p, 0, acc_bytes, s));
     CUDA_TRY(rec(t->ev[1], s));
 
     ProbeParams P = pl.P;
@@ -1644,12 +1655,12 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.g_hceil = t->d_plan.as<const uint8_t>(t->o_hce);
     for (size_t i = 0; i < pl.slots.size(); ++i)
         if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
-    P.g_acc = t->d_acc.as<unsigned long long>();
-    P.g_hll_glob = t->d_acc.as<uint32_t>(8ull * pl.acc_words);
-    P.g_bm = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes);
-    P.g_bmcnt = t->d_acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords);
+    P.g_acc = acc.as<unsigned long long>();
+    P.g_hll_glob = acc.as<uint32_t>(8ull * pl.acc_words);
+    P.g_bm = acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes);
+    P.g_bmcnt = acc.as<uint32_t>(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords);
     P.g_hll_part = t->d_part.as<uint8_t>();
-    P.g_nsamp = t->d_acc.as<unsigned long long>(nsamp_off);
+    P.g_nsamp = acc.as<unsigned long long>(nsamp_off);
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
@@ -1745,10 +1756,10 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.hll_bytes = pl.hll_bytes;
     F.nparts = (t->nrows == 0) ? 1 : (uint32_t)grid;
     F.hll_blocks = pl.hll_bytes ? (pl.hll_bytes / 4 + 63) / 64 : 0;      // fin_prefix: 64 register words per block
-    F.g_acc = t->d_acc.as<const unsigned long long>();
+    F.g_acc = acc.as<const unsigned long long>();
     F.g_pre = t->d_pre.as<unsigned long long>();
     F.g_hll_part = t->d_part.as<const uint8_t>();
-    F.g_nsamp = t->d_acc.as<const unsigned long long>(nsamp_off);
+    F.g_nsamp = acc.as<const unsigned long long>(nsamp_off);
     F.preds = t->d_plan.as<const FinPred>(o_fp);
     F.npreds = npreds;
     F.pairs = t->d_plan.as<const FinPair>(o_fq);
@@ -1761,6 +1772,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     F.out = reinterpret_cast<unsigned long long *>(out_base);
     F.out_regs = reinterpret_cast<uint8_t *>(out_base + align16(8 * out_words));
     F.g_bm = P.g_bm;
+    F.zero = dbuf ? t->d_accb[ob].as<uint4>() : nullptr;          // the next call's accumulators
+    F.zero_vec = dbuf ? t->d_accb[ob].cap / 16 : 0;
     F.nbm = 0;
     for (auto &S : pl.slots) {
         if (!S.bm) continue;
@@ -1828,6 +1841,10 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     T = gace_timing{};
     t->timing_kind = 1;          // stage times from the events in gace_last_timing
     t->dirty = false;
+    if (dbuf) {                  // this call's fin_output zeroed the other buffer
+        t->acc_clean[ob] = true;
+        t->acc_next = ob;
+    }
     T.scan_launches = launches;
     T.jit = jit_used;
     T.jit_compile_ms = jit_ms;

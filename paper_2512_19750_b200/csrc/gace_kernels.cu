@@ -1,3 +1,4 @@
+#include <algorithm>
 // gace_kernels.cu -- sm_100a kernels of the GACE selectivity probe.
 //
 // probe_kernel (device code in gace_probe.cuh) streams every probed key column once
@@ -221,6 +222,8 @@ __global__ void fin_output(const FinParams F) {
         }
         F.out[t] = r;
     }
+    // the other accumulator buffer (unused by this call) -> zero for the next call
+    for (uint64_t i = t; i < F.zero_vec; i += (uint64_t)gridDim.x * blockDim.x) F.zero[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // ------------------------------------------------------------------ attach / test hook
@@ -327,7 +330,8 @@ cudaError_t launch_finalize(const FinParams &F, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     const uint32_t outs = 1 + F.npreds + F.npairs;
-    return launch_pdl(fin_output, (outs + 255) / 256, 256, s, F);
+    const uint64_t zb = std::min<uint64_t>((F.zero_vec + 255) / 256, 296);
+    return launch_pdl(fin_output, (unsigned)std::max<uint64_t>((outs + 255) / 256, zb), 256, s, F);
 }
 
 cudaError_t launch_minmax(const void *col, int dtype, uint64_t n, long long *mm, int sms, cudaStream_t s) {

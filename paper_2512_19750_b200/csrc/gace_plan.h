@@ -305,6 +305,8 @@ struct FinParams {
     uint32_t npairs;
     unsigned long long *out;    // [1 + npreds + npairs]: n_sampled, counts, joints
     uint8_t *out_regs;          // [hll_bytes]
+    uint4 *zero;                // fin_output zeroes zero[0, zero_vec): the next call's accumulators
+    uint64_t zero_vec;
     // presence-bitmap HLL columns: registers from the merged bitmap (fin_bitmap_hll)
     uint32_t nbm;
     const uint32_t *g_bm;
