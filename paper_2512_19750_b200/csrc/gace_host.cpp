@@ -25,8 +25,10 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <chrono>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gace.h"
@@ -64,9 +66,12 @@ struct Nccl {
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     int (*CommDestroy)(void *) = nullptr;
+    int (*CommAbort)(void *) = nullptr;
+    int (*CommGetAsyncError)(void *, int *) = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
 };
-constexpr int kNcclUint8 = 1, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2;
+constexpr int kNcclUint8 = 1, kNcclInt64 = 4, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3;
+constexpr int kNcclInProgress = 7;
 
 Nccl *nccl() {
     static Nccl n;
@@ -84,8 +89,11 @@ Nccl *nccl() {
         n.GroupStart = (int (*)())dlsym(n.h, "ncclGroupStart");
         n.GroupEnd = (int (*)())dlsym(n.h, "ncclGroupEnd");
         n.CommDestroy = (int (*)(void *))dlsym(n.h, "ncclCommDestroy");
+        n.CommAbort = (int (*)(void *))dlsym(n.h, "ncclCommAbort");
+        n.CommGetAsyncError = (int (*)(void *, int *))dlsym(n.h, "ncclCommGetAsyncError");
         n.GetErrorString = (const char *(*)(int))dlsym(n.h, "ncclGetErrorString");
-        if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.GroupStart || !n.GroupEnd || !n.CommDestroy)
+        if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.GroupStart || !n.GroupEnd || !n.CommDestroy ||
+            !n.CommAbort || !n.CommGetAsyncError)
             n.h = nullptr;
     });
     return n.h ? &n : nullptr;
@@ -173,8 +181,13 @@ struct gace_table {
     std::vector<uint8_t> clustered;    // >= half of the aligned row quads hold one key (device tables)
     bool has_dist = false;
     gace_dist dist{};
+    // NCCL merge: whenever the caller gave a communicator or a unique id (any nranks,
+    // including 1), the results are merged by the grouped all-reduce before the D2H copy
+    bool use_nccl = false;
     void *comm = nullptr;
     bool own_comm = false;
+    bool comm_dead = false;            // aborted after an asynchronous NCCL error / timeout
+    DevBuf d_coll;                     // small collective scratch (attach domains, plan agreement)
     int sms = 148;
     DevBuf d_plan, d_accb[2], d_pre, d_part, d_out, d_nsamp, d_mask, d_stage[2];
     HostBuf h_plan, h_out;
@@ -204,7 +217,10 @@ struct gace_table {
     bool gprev_ok = false;
     uint64_t g_scan_launches = 0, g_nl = 0, g_captures = 0, g_replays = 0;
     int g_jit = 0;
-    size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0, o_hce = 0;
+    size_t blob = 0, o_img = 0, o_dir = 0, o_job = 0, o_fp = 0, o_fq = 0, o_bps = 0;
+    // HLL register ceilings per column (u8[ncols][4096]), computed on first use
+    DevBuf d_hceil, d_hceil32;
+    std::vector<uint8_t> hceil_ready;
     // candidate-set probe (gace_probe_sets): plan cache and buffers
     std::string sets_key;
     std::shared_ptr<void> sets_plan;
@@ -213,6 +229,43 @@ struct gace_table {
 };
 
 namespace {
+
+// ------------------------------------------------------------------ NCCL-aware waits
+
+// Wait for the table's stream.  Tables merged over NCCL poll instead of blocking: an
+// asynchronous NCCL error (a peer died, a network fault) or a collective that does not
+// finish within GACE_NCCL_TIMEOUT_MS (default 300000) aborts the communicator -- which
+// releases the kernels blocked in it -- and the call returns GACE_ENCCL instead of hanging.
+gace_status wait_stream(gace_table *t, cudaStream_t s) {
+    if (!t->use_nccl || !t->comm) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return GACE_OK;
+    }
+    if (t->comm_dead) return fail(GACE_ENCCL, "NCCL communicator was aborted by an earlier error");
+    Nccl *n = nccl();
+    static const double limit_ms = [] {
+        const char *e = getenv("GACE_NCCL_TIMEOUT_MS");
+        return e ? atof(e) : 300000.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return GACE_OK;
+        if (q != cudaErrorNotReady) return fail(GACE_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+        int async = 0;
+        const int r = n->CommGetAsyncError(t->comm, &async);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (r != 0 || (async != 0 && async != kNcclInProgress) || ms > limit_ms) {
+            n->CommAbort(t->comm);
+            t->comm_dead = true;
+            const int code = r ? r : async;
+            return fail(GACE_ENCCL, ms > limit_ms ? std::string("NCCL collective timed out; communicator aborted")
+                                                  : std::string("NCCL asynchronous error: ") +
+                                                        (n->GetErrorString ? n->GetErrorString(code) : "?"));
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(spin > 4096 ? 200 : 5));
+    }
+}
 
 // ------------------------------------------------------------------ planner
 
@@ -433,7 +486,6 @@ struct Plan {
     std::vector<FinPred> fpreds;
     std::vector<FinPair> fpairs;
     std::vector<int64_t> bps;          // MODE_SEARCH breakpoints, concatenated
-    std::vector<uint8_t> hceil;        // HLL register ceilings, 4096 bytes per eligible column
     ProbeParams P{};
 };
 
@@ -940,30 +992,13 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         // register ceilings: R[j] can never exceed the largest rank among the domain values
         // with index j, so once the merged registers reach them the column is complete and
         // the scan stops hashing its keys (register columns, domains <= 2^25 values)
+        // (a property of the column, not of the batch: computed once per attached column on
+        // the GPU -- gace_probe launches it the first time a plan needs it -- and kept in the
+        // table's d_hceil at byte offset col * 4096)
         Q.hceil_off = kNone;
         if (S.has_hll && !S.bm && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX) &&
-            (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL")) {
-            Q.hceil_off = (uint32_t)pl.hceil.size();
-            pl.hceil.resize(pl.hceil.size() + kHllM, 0);
-            uint8_t *ce = pl.hceil.data() + Q.hceil_off;
-            for (int64_t v = S.dl; v <= S.dh; ++v) {
-                uint32_t idx, r;
-                if (S.dtype == GACE_I32) {             // fmix32 (DESIGN.md §2 step 6)
-                    const uint32_t h = host_fmix32((uint32_t)(int32_t)v);
-                    idx = h >> (32 - kHllP);
-                    r = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
-                } else {                               // mix64(x + gamma)
-                    uint64_t z = (uint64_t)v + 0x9E3779B97F4A7C15ULL;
-                    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-                    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-                    z ^= z >> 31;
-                    idx = (uint32_t)(z >> (64 - kHllP));
-                    r = (uint32_t)__builtin_clzll((z << kHllP) | (1ull << (kHllP - 1))) + 1;
-                }
-                uint8_t &c = ce[idx];
-                if (r > c) c = (uint8_t)r;
-            }
-        }
+            (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL"))
+            Q.hceil_off = (uint32_t)S.col * kHllM;
         Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
         Q.prim_b = (int8_t)S.prim_b;
@@ -1077,6 +1112,8 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
             return fail(GACE_EINVAL, "bad rank / nranks");
         if (dist->nranks > 1 && !dist->nccl_unique_id && !dist->nccl_comm)
             return fail(GACE_EINVAL, "multi-rank attach needs an NCCL unique id or comm");
+        if (dist->row_offset > dist->nrows_total || nrows > dist->nrows_total - dist->row_offset)
+            return fail(GACE_EINVAL, "row_offset + nrows_local exceeds nrows_total");
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(GACE_ECUDA, "no CUDA device");
@@ -1111,6 +1148,9 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
         t->dhi[c] = dtypes[c] == GACE_I32 ? INT32_MAX : INT64_MAX;
     }
     t->clustered.assign(ncols, 0);
+    t->hceil_ready.assign(ncols, 0);
+    if (!host && (t->d_hceil.ensure((size_t)ncols * kHllM) != cudaSuccess || t->d_hceil32.ensure(4 * kHllM) != cudaSuccess))
+        return bail(fail(GACE_ENOMEM, "HLL ceiling buffers"));
     if (!host && nrows) {
         DevBuf mm;
         if (mm.ensure(24 * ncols) != cudaSuccess) return bail(fail(GACE_ENOMEM, "minmax scratch"));
@@ -1149,7 +1189,8 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
         t->has_dist = true;
         t->dist = *dist;
         t->dist.nccl_unique_id = nullptr;
-        if (dist->nranks > 1) {
+        t->use_nccl = dist->nranks > 1 || dist->nccl_unique_id || dist->nccl_comm;
+        if (t->use_nccl) {
             if (dist->nccl_comm) {
                 t->comm = dist->nccl_comm;
             } else {
@@ -1161,9 +1202,69 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
                 if (r != 0) return bail(fail(GACE_ENCCL, std::string("ncclCommInitRank: ") + (n->GetErrorString ? n->GetErrorString(r) : "")));
                 t->own_comm = true;
             }
+            // every rank plans over the same global value domains (min of the minima, max of
+            // the maxima), so identical batches give identical plans -- the same lookup
+            // tables, grids, limits and errors -- on every rank; an empty shard is neutral
+            if (!host) {
+                std::vector<long long> dom(2 * ncols);
+                for (uint32_t c = 0; c < ncols; ++c) {
+                    dom[c] = nrows ? t->dlo[c] : LLONG_MAX;
+                    dom[ncols + c] = nrows ? t->dhi[c] : LLONG_MIN;
+                }
+                Nccl *n = nccl();
+                if (t->d_coll.ensure(std::max<size_t>(16ull * ncols, 64)) != cudaSuccess)
+                    return bail(fail(GACE_ENOMEM, "collective scratch"));
+                long long *d = t->d_coll.as<long long>();
+                if (cudaMemcpyAsync(d, dom.data(), 16ull * ncols, cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
+                    return bail(fail(GACE_ECUDA, "domain agreement copy"));
+                n->GroupStart();
+                const int r1 = n->AllReduce(d, d, ncols, kNcclInt64, kNcclMin, t->comm, t->stream);
+                const int r2 = n->AllReduce(d + ncols, d + ncols, ncols, kNcclInt64, kNcclMax, t->comm, t->stream);
+                const int r3 = n->GroupEnd();
+                if (r1 || r2 || r3) return bail(fail(GACE_ENCCL, "domain agreement all-reduce failed"));
+                if (cudaMemcpyAsync(dom.data(), d, 16ull * ncols, cudaMemcpyDeviceToHost, t->stream) != cudaSuccess)
+                    return bail(fail(GACE_ECUDA, "domain agreement copy"));
+                const gace_status ws = wait_stream(t, t->stream);
+                if (ws) return bail(ws);
+                for (uint32_t c = 0; c < ncols; ++c) {
+                    if (dom[c] > dom[ncols + c]) continue;          // every shard empty: dtype range
+                    t->dlo[c] = dom[c];
+                    t->dhi[c] = dom[ncols + c];
+                }
+            }
         }
     }
     *out = t;
+    return GACE_OK;
+}
+
+// Planning is deterministic in (global domains, batch), so ranks given the same batch
+// build the same plan.  A new plan is still agreed on before any data collective: every
+// rank contributes its planning status and a hash of its batch; if any rank failed, or
+// the batches differ, every rank returns an error instead of entering the merge that the
+// others would never join (identical arguments are part of the collective contract).
+gace_status agree_plan(gace_table *t, gace_status local, const std::string &key) {
+    if (!t->use_nccl || !t->comm) return local;
+    if (t->comm_dead) return fail(GACE_ENCCL, "NCCL communicator was aborted by an earlier error");
+    Nccl *n = nccl();
+    const std::string err = local ? g_err : std::string();
+    const long long h = (long long)(std::hash<std::string>{}(key) >> 1);
+    long long v[4] = {local ? 1 : 0, h, h, 0};
+    CUDA_TRY(cudaSetDevice(t->device));
+    if (t->d_coll.ensure(64) != cudaSuccess) return fail(GACE_ENOMEM, "collective scratch");
+    long long *d = t->d_coll.as<long long>();
+    CUDA_TRY(cudaMemcpyAsync(d, v, 32, cudaMemcpyHostToDevice, t->stream));
+    n->GroupStart();
+    const int r1 = n->AllReduce(d, d, 2, kNcclInt64, kNcclMax, t->comm, t->stream);
+    const int r2 = n->AllReduce(d + 2, d + 2, 1, kNcclInt64, kNcclMin, t->comm, t->stream);
+    const int r3 = n->GroupEnd();
+    if (r1 || r2 || r3) return fail(GACE_ENCCL, "plan agreement all-reduce failed");
+    CUDA_TRY(cudaMemcpyAsync(v, d, 32, cudaMemcpyDeviceToHost, t->stream));
+    const gace_status ws = wait_stream(t, t->stream);
+    if (ws) return ws;
+    if (local) return fail(local, err);
+    if (v[0]) return fail(GACE_EINVAL, "another rank failed to plan this batch (collective call aborted)");
+    if (v[1] != v[2]) return fail(GACE_EINVAL, "ranks passed different batches to a collective probe");
     return GACE_OK;
 }
 
@@ -1485,10 +1586,13 @@ gace_status gace_table_detach(gace_table *t) {
     cudaSetDevice(t->device);
     if (t->stream) cudaStreamSynchronize(t->stream);
     if (t->copy_stream) cudaStreamSynchronize(t->copy_stream);
-    if (t->own_comm && t->comm) {
+    if (t->own_comm && t->comm && !t->comm_dead) {
         Nccl *n = nccl();
         if (n) n->CommDestroy(t->comm);
     }
+    t->d_coll.release();
+    t->d_hceil.release();
+    t->d_hceil32.release();
     for (auto &e : t->ev) if (e) cudaEventDestroy(e);
     for (int b = 0; b < 2; ++b) {
         if (t->ev_copied[b]) cudaEventDestroy(t->ev_copied[b]);
@@ -1547,7 +1651,10 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (nh && !hll_regs) return fail(GACE_EINVAL, "hll_regs is NULL");
 
     CUDA_TRY(cudaSetDevice(t->device));
-    if (t->dirty) CUDA_TRY(cudaStreamSynchronize(t->stream));   // an aborted call's work is done
+    if (t->dirty) {                                              // an aborted call's work is done
+        st = wait_stream(t, t->stream);
+        if (st) return st;
+    }
     t->dirty = true;                                             // (a completed call synchronised)
     t->timing_kind = 0;
     std::string key;
@@ -1557,9 +1664,13 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
     if (!t->plan || key != t->plan_key) {
         auto fresh = std::make_shared<Plan>();
-        st = make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh);
+        st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh), key);
         if (st) return st;
         const Plan &q = *fresh;
+        // the cached plan is replaced below: until then (and on any failure) no plan is
+        // current, so a later call can never launch the old plan over a half-written blob
+        t->plan.reset();
+        t->plan_key.clear();
         // ---- one pinned blob -> one H2D copy: image | direct | jobs | fpreds | fpairs | bps
         size_t off = 0;
         t->o_img = off; off = align16(off + q.image.size());
@@ -1568,7 +1679,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         t->o_fp = off; off = align16(off + q.fpreds.size() * sizeof(FinPred));
         t->o_fq = off; off = align16(off + q.fpairs.size() * sizeof(FinPair));
         t->o_bps = off; off = align16(off + q.bps.size() * sizeof(int64_t));
-        t->o_hce = off; off = align16(off + q.hceil.size());
         t->blob = std::max<size_t>(off, 16);
         if (t->h_plan.ensure(t->blob) != cudaSuccess || t->d_plan.ensure(t->blob) != cudaSuccess)
             return fail(GACE_ENOMEM, "plan buffers");
@@ -1579,7 +1689,6 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         if (!q.fpreds.empty()) memcpy(hb + t->o_fp, q.fpreds.data(), q.fpreds.size() * sizeof(FinPred));
         if (!q.fpairs.empty()) memcpy(hb + t->o_fq, q.fpairs.data(), q.fpairs.size() * sizeof(FinPair));
         if (!q.bps.empty()) memcpy(hb + t->o_bps, q.bps.data(), q.bps.size() * sizeof(int64_t));
-        if (!q.hceil.empty()) memcpy(hb + t->o_hce, q.hceil.data(), q.hceil.size());
         CUDA_TRY(cudaMemcpyAsync(t->d_plan.p, hb, t->blob, cudaMemcpyHostToDevice, t->stream));
         t->plan = fresh;
         t->plan_key.swap(key);
@@ -1597,8 +1706,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const size_t part_bytes = std::max<size_t>((size_t)grid * pl.hll_bytes, 16);
     const size_t out_words = 1 + npreds + npairs;
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
-    const bool use_graph = t->graphs && !t->host && t->nrows > 0 && t->stream != nullptr &&
-                           !(t->has_dist && t->dist.nranks > 1);
+    const bool use_graph = t->graphs && !t->host && t->nrows > 0 && t->stream != nullptr && !t->use_nccl;
     // graphs bake in one accumulator buffer and keep the memset; eager calls alternate
     const bool dbuf = !use_graph && !getenv("GACE_NO_ACC_DBUF");
     const int ab = dbuf ? t->acc_next : 0, ob = ab ^ 1;
@@ -1652,7 +1760,15 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     ProbeParams P = pl.P;
     P.image = t->d_plan.as<const uint4>(o_img);
     P.direct = t->d_plan.as<const DirectPair>(o_dir);
-    P.g_hceil = t->d_plan.as<const uint8_t>(t->o_hce);
+    P.g_hceil = t->d_hceil.as<const uint8_t>();
+    for (size_t i = 0; i < pl.slots.size(); ++i) {       // ceilings of the columns that need them
+        const int c = pl.slots[i].col;
+        if (P.slot[i].hceil_off == kNone || t->hceil_ready[c]) continue;
+        CUDA_TRY(launch_hll_ceilings(t->dlo[c], (uint64_t)t->dhi[c] - (uint64_t)t->dlo[c], t->dtypes[c] == GACE_I64,
+                                     t->d_hceil32.as<uint32_t>(), t->d_hceil.as<uint8_t>((size_t)c * kHllM), t->sms, s));
+        nl += 2;
+        t->hceil_ready[c] = 1;
+    }
     for (size_t i = 0; i < pl.slots.size(); ++i)
         if (P.slot[i].mode == MODE_SEARCH) P.slot[i].bps = t->d_plan.as<const int64_t>(o_bps) + pl.slots[i].bps_off;
     P.g_acc = acc.as<unsigned long long>();
@@ -1767,7 +1883,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // one rank: the finalize kernels write the packed result straight into the pinned host
     // buffer (mapped under UVA, same address), so no D2H copy is queued; with several ranks
     // the result stays on the device for the NCCL merge and is copied back after it
-    const bool zero_copy = !(t->has_dist && t->dist.nranks > 1) && !getenv("GACE_NO_ZERO_COPY");
+    const bool zero_copy = !t->use_nccl && !getenv("GACE_NO_ZERO_COPY");
     char *out_base = zero_copy ? t->h_out.as<char>() : t->d_out.as<char>();
     F.out = reinterpret_cast<unsigned long long *>(out_base);
     F.out_regs = reinterpret_cast<uint8_t *>(out_base + align16(8 * out_words));
@@ -1788,7 +1904,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     nl += (F.njobs + F.hll_blocks ? 2 : 1) + (F.nbm ? 1 : 0);
     CUDA_TRY(rec(t->ev[3], s));
 
-    if (t->has_dist && t->dist.nranks > 1) {
+    if (t->use_nccl) {
         Nccl *n = nccl();
         if (!n) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
         n->GroupStart();
@@ -1829,7 +1945,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     }
     g_launches += nl;
     }
-    CUDA_TRY(cudaStreamSynchronize(s));
+    st = wait_stream(t, s);
+    if (st) return st;
 
     const uint64_t *ho = t->h_out.as<uint64_t>();
     *n_sampled = ho[0];
@@ -1874,7 +1991,10 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     if (t->host) return fail(GACE_EUNSUPPORTED, "gace_probe_sets needs a device table");
 
     CUDA_TRY(cudaSetDevice(t->device));
-    if (t->dirty) CUDA_TRY(cudaStreamSynchronize(t->stream));
+    if (t->dirty) {
+        st = wait_stream(t, t->stream);
+        if (st) return st;
+    }
     t->dirty = true;
     t->timing_kind = 0;
     std::string key;
@@ -1886,7 +2006,7 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     CUDA_TRY(cudaEventRecord(t->ev[0], s));
     if (!t->sets_plan || key != t->sets_key) {
         auto fresh = std::make_shared<SetsPlan>();
-        st = make_sets_plan(t, preds, set_offsets, set_members, nsets, *fresh);
+        st = agree_plan(t, make_sets_plan(t, preds, set_offsets, set_members, nsets, *fresh), key);
         if (st) return st;
         const size_t n = fresh->image.size();
         if (t->h_sets_img.ensure(n) != cudaSuccess || t->d_sets_img.ensure(n) != cudaSuccess)
@@ -1928,7 +2048,7 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     g_launches += launches;
     CUDA_TRY(cudaEventRecord(t->ev[2], s));
     CUDA_TRY(cudaEventRecord(t->ev[3], s));
-    if (t->has_dist && t->dist.nranks > 1) {
+    if (t->use_nccl) {
         Nccl *nc = nccl();
         if (!nc) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
         void *buf = t->d_sets_out.p;
@@ -1938,7 +2058,8 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
     CUDA_TRY(cudaEventRecord(t->ev[4], s));
     CUDA_TRY(cudaMemcpyAsync(t->h_sets_out.p, t->d_sets_out.p, 8 * out_words, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaEventRecord(t->ev[5], s));
-    CUDA_TRY(cudaStreamSynchronize(s));
+    st = wait_stream(t, s);
+    if (st) return st;
     const uint64_t *ho = t->h_sets_out.as<uint64_t>();
     *n_sampled = ho[0];
     if (nsets) memcpy(set_counts, ho + 1, 8ull * nsets);
@@ -2101,6 +2222,14 @@ gace_status gace_cache_put(gace_cache *c, uint64_t table_id, const gace_pred *co
             c->map.erase(f);
             ++c->evictions;
         }
+    }
+    if (c->order.size() > 2ull * c->capacity + 64) {       // re-puts leave stale entries: compact
+        std::deque<std::pair<uint64_t, std::string>> live;
+        for (auto &e : c->order) {
+            auto f = c->map.find(e.second);
+            if (f != c->map.end() && f->second.seq == e.first) live.push_back(std::move(e));
+        }
+        c->order.swap(live);
     }
     return GACE_OK;
 }

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 
 #include "gace_kernels.h"
 #include "gace_plan.h"
@@ -280,11 +282,19 @@ __global__ void sample_mask_kernel(uint64_t nrows, uint64_t row0, uint64_t seed,
 template <int NC, bool SAMPLE, bool I64>
 static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
     auto k = probe_kernel<NC, SAMPLE, I64>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 2048);
-        if (e != cudaSuccess) return e;
-        configured = true;
+    // the attribute is per device: set it for each device this instantiation runs on
+    static std::mutex mu;
+    static uint64_t configured = 0;      // bit d: device d done
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev >= 64 || !((configured >> dev) & 1ull)) {
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 2048);
+            if (e != cudaSuccess) return e;
+            if (dev < 64) configured |= 1ull << dev;
+        }
     }
     k<<<grid, kThreads, P.smem_bytes, s>>>(P);
     return cudaGetLastError();
@@ -338,6 +348,52 @@ cudaError_t launch_minmax(const void *col, int dtype, uint64_t n, long long *mm,
     const uint64_t want = (n + 255) / 256;
     const int grid = (int)(want < (uint64_t)sms * 8 ? (want ? want : 1) : (uint64_t)sms * 8);
     minmax_kernel<<<grid, 256, 0, s>>>(col, dtype, n, mm);
+    return cudaGetLastError();
+}
+
+// HLL register ceilings of one column (the largest rank any value of the domain
+// [dl, dl + span] can put into each register; DESIGN.md §6 "HLL completion"): per-CTA
+// shared maxima over a grid-stride range of the domain, merged into ce32 (u32[4096], zeroed
+// by the caller) and packed to u8 by ceil_pack_kernel.  Hashes as in the probe (fmix32 for
+// int32 columns, mix64(x + gamma) for int64).
+__global__ void ceil_kernel(long long dl, unsigned long long span, int is64, uint32_t *ce32) {
+    __shared__ uint32_t R[kHllM];
+    for (uint32_t i = threadIdx.x; i < kHllM; i += blockDim.x) R[i] = 0;
+    __syncthreads();
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k <= span; k += stride) {
+        const uint64_t v = (uint64_t)dl + k;
+        uint32_t idx, r;
+        if (!is64) {
+            const uint32_t h = fmix32((uint32_t)v);
+            idx = h >> (32 - kHllP);
+            r = __clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
+        } else {
+            const uint64_t h = mix64(v + GACE_GAMMA);
+            idx = (uint32_t)(h >> (64 - kHllP));
+            r = __clzll((h << kHllP) | (1ull << (kHllP - 1))) + 1;
+        }
+        if (r > R[idx]) atomicMax(&R[idx], r);
+        if (k + stride < k) break;       // span near 2^64: no wrap-around
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kHllM; i += blockDim.x)
+        if (R[i]) atomicMax(ce32 + i, R[i]);
+}
+
+__global__ void ceil_pack_kernel(const uint32_t *ce32, uint8_t *ce8) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kHllM) ce8[i] = (uint8_t)ce32[i];
+}
+
+cudaError_t launch_hll_ceilings(long long dl, unsigned long long span, bool is64, uint32_t *scratch32,
+                                uint8_t *out8, int sms, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(scratch32, 0, 4 * kHllM, s);
+    if (e != cudaSuccess) return e;
+    const unsigned long long want = span / 1024 + 1;
+    const unsigned grid = (unsigned)(want < (unsigned long long)sms * 2 ? want : (unsigned long long)sms * 2);
+    ceil_kernel<<<grid, 1024, 0, s>>>(dl, span, is64 ? 1 : 0, scratch32);
+    ceil_pack_kernel<<<kHllM / 256, 256, 0, s>>>(scratch32, out8);
     return cudaGetLastError();
 }
 

@@ -867,7 +867,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     }
     if (!Sh::SAMPLE) kept += 4 * U * it;   // every row of every unit this thread processed
     // tail rows [nunits * 4U, nrows): one row per thread of the last CTA
-    const uint64_t tail0 = nunits * 4 * U;
+    const uint64_t tail0 = (uint64_t)nunits * (4 * U);   // 64-bit: a launch may hold 2^33 rows
     if (blockIdx.x == gridDim.x - 1 && tail0 + threadIdx.x < P.nrows) kept += tail_row<Sh>(P, tail0 + threadIdx.x);
     __syncthreads();
 

@@ -147,8 +147,10 @@ def test_errors(G, oracle):
 
 def test_full_size_identities(G):
     """Exp. D at BASELINE size (600M rows): sets of one / two members and the empty set
-    equal the probe's counts / joints / n_sampled (both through the C-ABI; the probe is
-    oracle-checked at this size by test_gpu_parity's full-size tests)."""
+    equal the probe's counts / joints / n_sampled (both through the C-ABI).  The sets
+    kernel itself is oracle-checked at this size by
+    tests/test_gpu_fullsize.py::test_exp_d_full_size_vs_oracle, the probe by
+    test_bench_config_full_size_vs_oracle."""
     w = synth.get("D")
     cols = [w.column(c, device="cuda") for c in range(len(w.columns))]
     torch.cuda.synchronize()
