@@ -53,6 +53,36 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+NOMINAL_HBM_GBS = 8000.0      # BASELINE.json north_star "~8 TB/s" (B200_PROFILING.md: 7.7 HGX / 8 DGX)
+
+
+def read_ceiling():
+    """Measured read-only streaming ceiling (tools/stream_read.cu on a B200, profiles/stream_read.json)."""
+    p = os.path.join(ROOT, "profiles", "stream_read.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["read_ceiling_gbs"]), d.get("read_ceiling_variant", "")
+    return None, None
+
+
+def fresh_batch(w, b: int):
+    """Batch b of a bind-variable sweep over w's query template (the
+    bind centre moves per query): the same predicates and pairs with every bound shifted,
+    so each batch is new to the library (new plan, new lookup tables), its structure is
+    the template's.  EQ binds move by 37 values per batch (C3's sliding bind window);
+    range bounds by 0.05 % of the column's domain per batch."""
+    P = w.preds.copy()
+    for c, col in enumerate(w.columns):
+        m = P["col"] == c
+        if not m.any():
+            continue
+        step = 37 if np.all(P["op"][m] == 0) else max(1, int((col.hi - col.lo) * 5e-4))
+        P["a"][m] += b * step
+        P["b"][m] += b * step
+    return P
+
+
 def describe(w) -> dict:
     if w.sets:
         ks = sorted(set(len(x) for x in w.sets))
@@ -153,17 +183,41 @@ def run_reference(args, w, rank, world):
         _, dt, cores = oracle_rate(w, rows)
         times.append(dt)
     value = rows * len(times) / sum(times)
-    cfg = describe(w)
-    cfg["parallelism"] = f"oracle on {cores} host threads"
-    sample = f"rows [0, {rows:,}) of {w.name} per step ({rows / w.nrows:.2%} of the table)"
+    cfg = run_config(w, world, args)
+    sample = (f"rows [0, {rows:,}) of {w.name} per step ({rows / w.nrows:.2%} of the table; every predicate, "
+              f"pair and HLL column), oracle C scan on {cores} host threads ({cpu_model()})")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times) * w.nrows / rows,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_of(w), "data": "synthetic",
         "config": cfg,
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "rows_per_step": rows},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def dtype_of(w) -> str:
+    return "int32" if all(w.columns[c].dtype == "i32" for c in w.probed_cols) else "int32/int64"
+
+
+def run_config(w, world, args) -> dict:
+    """The `config` object both arms print (identical for the same workload and N)."""
+    return dict(describe(w), parallelism=f"dp{world}: contiguous row shards, NCCL sum/max merge",
+                cuda_graphs=bool(args.graphs),
+                l2=("flushed between steps (2x L2 buffer write)"
+                    if (w.nrows // max(world, 1)) * w.bytes_per_row < 2 * L2_BYTES
+                    else f"inputs larger than L2 ({w.nrows // max(world, 1) * w.bytes_per_row / 1e9:.2f} GB per GPU)"))
 
 
 # ------------------------------------------------------------------ GPU leg
@@ -181,6 +235,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graphs", action="store_true",
                     help="replay each repeated probe as a CUDA graph (gace_table_set_graphs; side stream)")
+    ap.add_argument("--cold-batches", type=int, default=24,
+                    help="after the timed region: wall latency of this many NEW batches of the same query "
+                         "template (bind-variable sweep; planning, upload and kernel choice inside)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -229,10 +286,13 @@ def main():
             return table.probe_sets(w.preds, w.sets, w.rate, w.sample_seed)
         return table.probe(w.preds, w.pairs, w.rate, w.sample_seed, w.hll_cols)
 
-    for _ in range(args.warmup):
+    for k in range(2 * args.warmup):
         if flush is not None:
             flush.fill_(1)
         step()
+        if k == args.warmup - 1:
+            gace.jit_sync()         # the background compiles of the batch's specialised kernels
+    jit_kind = table.last_timing()["jit"] if not w.sets else None
 
     clocks = ClockSampler(local)
     L0 = gace.kernel_launches()
@@ -281,28 +341,27 @@ def main():
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
 
+    rc, rc_src = read_ceiling()
     out = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int32" if all(
-            w.columns[c].dtype == "i32" for c in probed) else "int32/int64",
+        "scaling": "strong", "vs_baseline": None, "dtype": dtype_of(w),
         "data": "synthetic",
-        "config": dict(describe(w), parallelism=f"dp{world}: contiguous row shards, NCCL sum/max merge",
-                       cuda_graphs=bool(args.graphs),
-                       l2=("flushed between steps (2x L2 buffer write)" if flush is not None
-                           else f"inputs larger than L2 ({nloc * w.bytes_per_row / 1e9:.2f} GB per GPU)")),
+        "config": run_config(w, world, args),
         "hbm_gbs": w.nrows * w.bytes_per_row / (ms_per_step * 1e-3) / 1e9,
         "latency_ms": {"p50": nearest_rank(lat, 0.5), "p99": nearest_rank(lat, 0.99), "kind": "wall, per gace_probe"},
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": ("sets_kernel (candidate-set conjunction kernel)" if w.sets
-                                else "gace_jit_probe (plan-specialised probe kernel)"),
+                                else {0: "probe_kernel (generic)", 1: "gace_jit_probe (structure-specialised)",
+                                      2: "gace_jit_probe (layout-specialised)"}.get(jit_kind, str(jit_kind))),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_scanned,
-                     "note": "HBM roofline of the north-star target; the measured limiter is instruction "
-                             "issue / shared-memory pipe (profiles/r01_ncu_C5.md), a read-only scan of the "
-                             "same columns runs at ~8 TB/s"},
+                     "frac_of_nominal": achieved / NOMINAL_HBM_GBS, "nominal_gbs": NOMINAL_HBM_GBS,
+                     "frac_of_read_ceiling": (achieved / rc) if rc else None, "read_ceiling_gbs": rc,
+                     "read_ceiling_source": (f"tools/stream_read.cu {rc_src} (profiles/stream_read.json)"
+                                             if rc else None)},
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -314,6 +373,8 @@ def main():
         hcols = [c.cpu().pin_memory() if len(c) == nloc else c.cpu() for c in cols]
         htable = gace.Table(hcols, host=True, dist=dinfo, device=local, stream=stream)
         hstep = lambda: htable.probe(w.preds, w.pairs, w.rate, w.sample_seed, w.hll_cols)  # noqa: E731
+        hstep()
+        gace.jit_sync()             # the host table's plan has its own specialised kernels
         hstep()
         if world > 1:
             dist.barrier()
@@ -338,12 +399,37 @@ def main():
         htable.detach()
         del hcols
 
+    # cold batches: new predicate batches of the same template, one probe each (wall latency
+    # through the C-ABI: planning, plan upload, kernel choice -- no call waits for a compile)
+    if args.cold_batches and not w.sets:
+        cl, ck = [], []
+        for b in range(1, args.cold_batches + 1):
+            Pb = fresh_batch(w, b)
+            if flush is not None:
+                flush.fill_(b)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            table.probe(Pb, w.pairs, w.rate, w.sample_seed, w.hll_cols)
+            cl.append(1e3 * (time.perf_counter() - t0))
+            ck.append(table.last_timing()["jit"])
+        warm = nearest_rank(lat, 0.5)
+        out["cold_batches"] = {"n": len(cl), "p50_ms": nearest_rank(cl, 0.5), "p99_ms": nearest_rank(cl, 0.99),
+                               "warm_p50_ms": warm, "ratio_p50": nearest_rank(cl, 0.5) / warm,
+                               "kernels": {str(k): ck.count(k) for k in sorted(set(ck))},
+                               "kind": "wall per gace_probe, a new bind-sweep batch each call (bench.fresh_batch)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows = calibrate_oracle_rows(w, budget_s=15.0)
         r, dt, cores = oracle_rate(w, rows)
         out["cpu_baseline"] = {"value": r, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                               "cpu_model": cpu_model(),
                                "sample": f"rows [0, {rows:,}) of {w.name} ({dt:.1f} s, "
                                          f"{'all sets' if w.sets else 'all predicates/pairs/HLL'})"}
+        if w.name == "C1" or args.config == "C1":
+            r1, dt1, _ = oracle_rate(w, min(w.nrows, rows), threads=1)
+            out["cpu_baseline"]["single_thread"] = {"value": r1, "unit": "rows/s", "cores": 1,
+                                                    "seconds": dt1}
     table.detach()
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -325,13 +325,28 @@ typedef struct {
     double total_ms;        /* first to last event                                     */
     uint64_t scan_launches; /* probe-kernel launches in that call                      */
     uint64_t bytes_scanned; /* algorithmic bytes: rows x sum of probed column widths   */
-    int32_t jit;            /* 1: plan-specialised (NVRTC) kernel, 0: generic kernel,
-                               -1: specialisation failed, generic kernel used           */
+    int32_t jit;            /* scan kernel of the call's large launches: 0 generic
+                               (precompiled) kernel, 1 specialised for the plan's
+                               structure, 2 specialised for its structure and layout,
+                               -1 specialisation failed, generic kernel used            */
     int32_t pad;
     double jit_compile_ms;  /* NVRTC compile time spent in that call (0 when cached)   */
 } gace_timing;
 
 gace_status gace_last_timing(const gace_table *t, gace_timing *out);
+
+/*
+ * Plan-specialised scan kernels are compiled with NVRTC off the call path:
+ * a probe whose specialised kernel is not compiled yet runs the precompiled generic kernel
+ * (same results) and queues the compile on a background thread; the kernel specialised
+ * for the batch's structure serves every later batch of that structure, the one
+ * specialised for its layout too replaces it for repeats of the same batch.  (Env
+ * GACE_JIT=1 compiles synchronously instead; GACE_JIT=0 never specialises.)
+ * gace_jit_sync waits up to timeout_ms until no compile is queued or running
+ * (GACE_EUNSUPPORTED on timeout); the counters (each may be NULL) report compiles
+ * finished, failed and still pending.  GACE_EINVAL: timeout_ms negative or NaN.
+ */
+gace_status gace_jit_sync(double timeout_ms, uint64_t *compiled, uint64_t *failed, uint64_t *pending);
 
 /* Rank 0 of a multi-GPU job: fill id[128] with a fresh ncclUniqueId to broadcast to
  * the other ranks (GACE_ENCCL if libnccl.so.2 cannot be loaded). */

@@ -204,7 +204,12 @@ struct gace_table {
     // same batch skip planning and the H2D of the tables)
     std::string plan_key;
     std::shared_ptr<void> plan;
-    void *jit_fn[2] = {nullptr, nullptr};   // specialised kernel of the cached plan (index: sampled)
+    // specialised kernel of the cached plan (index: sampled): kind 1 = keyed on the plan
+    // structure, 2 = keyed on its layout too; the layout-keyed one is compiled in the
+    // background (jit_lsrc) and replaces the structure-keyed one once it is loaded
+    void *jit_fn[2] = {nullptr, nullptr};
+    int jit_kind[2] = {0, 0};
+    std::string jit_ssrc[2], jit_lsrc[2];
     // CUDA-graph replay of repeated identical probes (gace_table_set_graphs)
     bool graphs = false;
     uint64_t plan_gen = 0;
@@ -509,6 +514,15 @@ void dump_plan(const Plan &pl) {
     }
     fprintf(stderr, "smem %u image %zu acc_words %u hll_bytes %u\n", pl.smem_bytes, pl.image.size(), pl.acc_words,
             pl.hll_bytes);
+}
+
+// Folded addressing (int32 lookup column without clamp, FMTEX, or FMT1T whose cells are
+// aligned key multiples): the specialised kernel indexes the level-1 table with the key
+// itself and the base folded into fold_b / fold_z (gace_plan.h SlotParams).
+bool slot_foldable(const SlotParams &Q) {
+    if (Q.dtype != 0 || Q.mode != MODE_LUT || Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX) return false;
+    if (Q.fmt == FMTEX) return true;
+    return Q.fmt == FMT1T && Q.s1 >= 1 && ((uint64_t)Q.base & ((1ull << Q.s1) - 1)) == 0 && Q.base >= 0;
 }
 
 gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
@@ -1029,6 +1043,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             Q.clamp_hi = S.clamp_hi;
             pl.clamp = true;
         }
+        if (slot_foldable(Q)) {
+            Q.fold_b = 4 * Q.lut_w - 4 * (uint32_t)((uint64_t)Q.base >> Q.s1);
+            Q.fold_z = Q.fmt == FMT1T ? Q.t1_ones - (uint32_t)Q.base * Q.t1_mul : 0u;
+        }
         if (S.has_preds && S.mode == MODE_SEARCH) {
             S.bps_off = bps;
             Q.nbp = (uint32_t)S.T.size();
@@ -1274,7 +1292,11 @@ namespace {
 
 // Source of `struct JitShape` for gace_probe.cuh: the plan's structural decisions as
 // constexpr answers (predicate values stay in the kernel parameters).
-std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::vector<uint8_t> &clustered) {
+// layout = false: the structure only (layout read from the parameters, gace_probe.cuh
+// RtLayout), so every batch with this structure shares one compiled kernel; layout = true:
+// offsets, shifts and masks baked in as immediates too (one kernel per batch layout).
+std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::vector<uint8_t> &clustered,
+                             bool layout) {
     const ProbeParams &P = pl.P;
     const int nc = (int)P.nslots;
     auto chain = [&](auto f, int n) {
@@ -1282,7 +1304,7 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
         for (int i = 0; i < n; ++i) r += "s == " + std::to_string(i) + " ? " + f(i) + " : ";
         return r + "0";
     };
-    std::string o = "namespace gace {\nstruct JitShape {\n";
+    std::string o = "namespace gace {\nstruct JitShape : RtLayout {\n";
     o += "  static constexpr int NC = " + std::to_string(nc) + ";\n";
     o += "  static constexpr bool SAMPLE = " + std::string(sample ? "true" : "false") + ";\n";
     o += "  static constexpr bool I64 = " + std::string(i64 ? "true" : "false") + ";\n";
@@ -1341,6 +1363,10 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
         o += std::string("  __device__ static constexpr uint32_t dbg(const ProbeParams &) { return ") +
              std::to_string(ab ? (uint32_t)strtoul(ab, nullptr, 0) : 0u) + "u; }\n";
     }
+    o += "  __device__ static constexpr bool hllbm(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].bm_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool fold(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(slot_foldable(P.slot[i]) ? "1" : "0"); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool sclamp(const ProbeParams &, int s) { return " +
          chain([&](int i) {
              const SlotParams &Q = P.slot[i];
@@ -1348,29 +1374,19 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
                                          : (Q.clamp_lo != INT64_MIN || Q.clamp_hi != INT64_MAX);
              return std::string(c ? "1" : "0");
          }, nc) + "; }\n";
+    if (!layout) {
+        o += "};\n}  // namespace gace\n";
+        return o;
+    }
     slot_i64("base", [](const SlotParams &Q) { return Q.base; });
-    // folded addressing (int32, no clamp): FMTEX always; FMT1T when its cells are aligned keys
-    auto foldable = [](const SlotParams &Q) {
-        if (Q.dtype != 0 || Q.mode != MODE_LUT || Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX) return false;
-        if (Q.fmt == FMTEX) return true;
-        return Q.fmt == FMT1T && Q.s1 >= 1 && ((uint64_t)Q.base & ((1ull << Q.s1) - 1)) == 0 && Q.base >= 0;
-    };
-    o += "  __device__ static constexpr bool fold(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(foldable(P.slot[i]) ? "1" : "0"); }, nc) + "; }\n";
-    slot_u32("foldb", [&](const SlotParams &Q) {
-        return foldable(Q) ? 4 * Q.lut_w - 4 * (uint32_t)((uint64_t)Q.base >> Q.s1) : 0u;
-    });
-    slot_u32("foldz", [&](const SlotParams &Q) {
-        return foldable(Q) && Q.fmt == FMT1T ? Q.t1_ones - (uint32_t)Q.base * Q.t1_mul : 0u;
-    });
+    slot_u32("foldb", [&](const SlotParams &Q) { return Q.fold_b; });
+    slot_u32("foldz", [&](const SlotParams &Q) { return Q.fold_z; });
     slot_i64("clo", [](const SlotParams &Q) { return Q.clamp_lo; });
     slot_i64("chi", [](const SlotParams &Q) { return Q.clamp_hi; });
     slot_u32("s1", [](const SlotParams &Q) { return Q.s1; });
     slot_u32("lutb", [](const SlotParams &Q) { return 4 * Q.lut_w; });
     slot_u32("histb", [](const SlotParams &Q) { return Q.hist_addr; });
     slot_u32("hllw", [](const SlotParams &Q) { return Q.hll_idx; });
-    o += "  __device__ static constexpr bool hllbm(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].bm_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
     slot_u32("bmaddr", [](const SlotParams &Q) { return Q.bm_addr; });
     slot_u32("bmbase", [](const SlotParams &Q) { return (uint32_t)Q.bm_base; });
     slot_u32("bmnv", [](const SlotParams &Q) { return Q.bm_nvals; });
@@ -1394,7 +1410,27 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
     return o;
 }
 
-// GACE_JIT=0: never specialise; 1: always; unset: for launches of >= 2^24 rows.
+// Which specialised kernels (GACE_JIT_LAYOUT): 0 the structure-keyed one only; 1 the
+// layout-keyed one only (compiled per batch layout); unset / 2: the structure-keyed one at
+// once and the layout-keyed one compiled in the background, used once it is loaded.
+int jit_layout_mode() {
+    const char *e = getenv("GACE_JIT_LAYOUT");
+    if (!e) return 2;
+    const int v = atoi(e);
+    return v < 0 || v > 2 ? 2 : v;
+}
+bool jit_layout() { return jit_layout_mode() == 1; }
+
+// Launches of at least this many rows use a specialised kernel (GACE_JIT_MIN_ROWS, default
+// 2^24: below it the generic kernel's extra instructions cost less than a launch).
+uint64_t jit_min_rows() {
+    const char *e = getenv("GACE_JIT_MIN_ROWS");
+    return e ? strtoull(e, nullptr, 10) : (1ull << 24);
+}
+
+// GACE_JIT=0: never specialise; 1: always, compiling a missing kernel synchronously; unset:
+// launches of >= 2^24 rows use a specialised kernel if one is compiled, else the generic
+// kernel while the specialised one compiles in the background (no call waits for NVRTC).
 int jit_mode() {
     const char *e = getenv("GACE_JIT");
     if (!e) return 2;
@@ -1693,7 +1729,12 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         t->plan = fresh;
         t->plan_key.swap(key);
         t->plan_gen++;
-        t->jit_fn[0] = t->jit_fn[1] = nullptr;
+        for (int i = 0; i < 2; ++i) {
+            t->jit_fn[i] = nullptr;
+            t->jit_kind[i] = 0;
+            t->jit_ssrc[i].clear();
+            t->jit_lsrc[i].clear();
+        }
     }
     const Plan &pl = *static_cast<const Plan *>(t->plan.get());
     const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
@@ -1730,8 +1771,59 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     uint64_t bytes_per_row = 0;
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
     const char *ab_env = getenv("GACE_ABLATE");
+    // ---- scan kernel for this call's large launches (gace_probe.cuh)
+    const bool sample = sample_rate < 1.0;
+    bool i64 = false;
+    for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
+    const int jm = jit_mode(), jl = jit_layout_mode();
+    // rows per launch: keep every CTA's u32 bins below 2^31
+    // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
+    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
+    const uint64_t big_launch = t->host ? std::min<uint64_t>(t->nrows, 1ull << 24) : std::min(t->nrows, max_rows);
+    void *scan_fn = nullptr;
+    int scan_kind = 0;
+    std::string jit_err;
+    if (pl.P.nslots > 0 && (jm == 1 || (jm == 2 && big_launch >= jit_min_rows()))) {
+        const int si = sample ? 1 : 0;
+        void *&fn = t->jit_fn[si];
+        if (fn && t->jit_kind[si] == 1 && !t->jit_lsrc[si].empty()) {     // layout-keyed kernel loaded yet?
+            void *f2 = nullptr;
+            if (jit_lookup(t->device, t->jit_lsrc[si], &f2)) {
+                fn = f2;
+                t->jit_kind[si] = 2;
+                t->jit_lsrc[si].clear();
+            }
+        }
+        if (!fn) {
+            std::vector<uint8_t> cl(pl.slots.size(), 0);
+            for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
+            if (t->jit_ssrc[si].empty()) {
+                t->jit_ssrc[si] = jit_shape_source(pl, sample, i64, cl, jl == 1);
+                if (jl == 2) t->jit_lsrc[si] = jit_shape_source(pl, sample, i64, cl, true);
+            }
+            if (jl == 2 && !t->jit_lsrc[si].empty() && jit_lookup(t->device, t->jit_lsrc[si], &fn)) {
+                t->jit_kind[si] = 2;                               // repeat of a batch seen before
+                t->jit_lsrc[si].clear();
+            } else if (!jit_lookup(t->device, t->jit_ssrc[si], &fn)) {
+                fn = nullptr;
+                if (jm == 1) {
+                    if (!jit_get(t->device, t->jit_ssrc[si], &fn, &jit_ms, &jit_err)) fn = nullptr;
+                } else {
+                    jit_prefetch(t->device, t->jit_ssrc[si]);      // generic kernel meanwhile
+                }
+            }
+            if (fn && t->jit_kind[si] != 2) t->jit_kind[si] = jl == 1 ? 2 : 1;
+            if (jl == 2 && !t->jit_lsrc[si].empty()) jit_prefetch(t->device, t->jit_lsrc[si]);
+        }
+        scan_fn = fn;
+        scan_kind = fn ? t->jit_kind[si] : 0;
+        if (!fn && jm == 1) {
+            scan_kind = -1;
+            g_err = "jit unavailable, generic kernel used: " + jit_err;
+        }
+    }
     GraphKey gk{t->plan_gen, sample_rate, seed, ab_env ? (uint32_t)strtoul(ab_env, nullptr, 0) : 0u,
-                acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, nullptr, t->d_plan.p};
+                acc.p, t->d_pre.p, t->d_part.p, t->d_out.p, t->h_out.p, scan_fn, t->d_plan.p};
     const bool replay = use_graph && t->gexec && gk == t->gkey;
     bool capt = use_graph && !replay && t->gprev_ok && gk == t->gprev;
     if (use_graph && !replay) {
@@ -1781,35 +1873,20 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
     if (ab_env) P.dbg = (uint32_t)strtoul(ab_env, nullptr, 0);   // design experiments only
-    const bool sample = sample_rate < 1.0;
-    bool i64 = false;
-    for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
 
-    // rows per launch: keep every CTA's u32 bins below 2^31
-    // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
-    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
-    // specialised (NVRTC) kernel for large launches, generic precompiled kernel otherwise
-    const int jm = jit_mode();
-    std::string shape;
+    // the specialised kernel (resolved above) for large launches, generic precompiled otherwise
     auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
-        if (PP.nslots > 0 && (jm == 1 || (jm == 2 && n >= (1ull << 24)))) {
+        if (scan_fn && (jm == 1 || n >= jit_min_rows())) {
             std::string err;
-            void *&fn = t->jit_fn[sample ? 1 : 0];
-            if (!fn) {
-                if (shape.empty()) {
-                    std::vector<uint8_t> cl(pl.slots.size(), 0);
-                    for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
-                    shape = jit_shape_source(pl, sample, i64, cl);
-                }
-                if (!jit_get(t->device, shape, &fn, &jit_ms, &err)) fn = nullptr;
-            }
-            if (fn && jit_launch_fn(fn, PP, grid, s, &err)) {
-                jit_used = 1;
+            if (jit_launch_fn(scan_fn, PP, grid, s, &err)) {
+                jit_used = scan_kind;
                 return cudaSuccess;
             }
             jit_used = -1;     // fall back to the generic GPU kernel; reason in gace_last_error()
-            g_err = "jit unavailable, generic kernel used: " + err;
+            g_err = "jit launch failed, generic kernel used: " + err;
+        } else if (scan_kind < 0) {
+            jit_used = -1;
         }
         return launch_probe(PP, sample, i64, grid, s);
     };
@@ -2292,6 +2369,13 @@ gace_status gace_sample_mask(gace_table *t, double sample_rate, uint64_t seed, u
     return GACE_OK;
 }
 
+gace_status gace_jit_sync(double timeout_ms, uint64_t *compiled, uint64_t *failed, uint64_t *pending) {
+    if (!(timeout_ms >= 0)) return fail(GACE_EINVAL, "timeout_ms must be >= 0");
+    const bool ok = jit_bg_wait(timeout_ms);
+    jit_bg_stats(compiled, failed, pending);
+    return ok ? GACE_OK : fail(GACE_EUNSUPPORTED, "background kernel compiles still running at the timeout");
+}
+
 gace_status gace_last_timing(const gace_table *t, gace_timing *out) {
     gace_status st = check_table(t);
     if (st) return st;
@@ -2625,8 +2709,12 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     std::string err;
     size_t n = 0;
-    std::vector<uint8_t> cl(pl.slots.size(), getenv("GACE_DEBUG_CLUSTERED") ? 1 : 0);   // compile that path too
-    if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64, cl), &n, &err)) return fail(GACE_EUNSUPPORTED, err);
+    // GACE_DEBUG_CLUSTERED = bit mask of slots compiled with the clustered-column path
+    const unsigned long clm = getenv("GACE_DEBUG_CLUSTERED") ? strtoul(getenv("GACE_DEBUG_CLUSTERED"), nullptr, 0) : 0ul;
+    std::vector<uint8_t> cl(pl.slots.size(), 0);
+    for (size_t i = 0; i < cl.size(); ++i) cl[i] = (clm >> i) & 1ul;
+    if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64, cl, jit_layout()), &n, &err))
+        return fail(GACE_EUNSUPPORTED, err);
     if (cubin_bytes) *cubin_bytes = n;
     return GACE_OK;
 }

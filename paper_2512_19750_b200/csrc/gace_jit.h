@@ -26,6 +26,15 @@ bool jit_launch(const ProbeParams &P, int device, const std::string &shape_src, 
 bool jit_get(int device, const std::string &shape_src, void **fn, double *compile_ms, std::string *err);
 bool jit_launch_fn(void *fn, const ProbeParams &P, int grid, cudaStream_t s, std::string *err);
 
+// Non-blocking: the cached kernel for (device, shape) if it is compiled.
+bool jit_lookup(int device, const std::string &shape_src, void **fn);
+// Queue a background compile of (device, shape) (no-op if cached or already queued); a later
+// jit_lookup finds it once the worker thread has loaded it.
+void jit_prefetch(int device, const std::string &shape_src);
+// Wait until no background compile is queued or running (false on timeout).
+bool jit_bg_wait(double timeout_ms);
+void jit_bg_stats(uint64_t *done, uint64_t *failed, uint64_t *pending);
+
 // NVRTC compile only (no device needed): the test hook gace_debug_jit_compile.
 bool jit_compile_check(const std::string &shape_src, size_t *cubin_bytes, std::string *err);
 

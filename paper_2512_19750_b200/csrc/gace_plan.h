@@ -203,6 +203,11 @@ struct SlotParams {
     uint32_t hll_out;       // output register block (ascending HLL column order)
     uint32_t bm_nvals;      // values in the column domain: the merged bitmap is complete at this count
     uint32_t hceil_off;     // byte offset of the column's register ceilings in g_hceil, or kNone
+    // folded addressing (specialised kernels, int32 lookup columns whose cells are aligned
+    // key multiples): level-1 byte address = (key >> s1) * 4 + fold_b; FMT1T in-cell offset
+    // compare word = key * t1_mul + fold_z
+    uint32_t fold_b;
+    uint32_t fold_z;
     int64_t bm_base;        // multiple of 32
 };
 

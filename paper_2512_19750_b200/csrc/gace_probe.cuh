@@ -205,9 +205,47 @@ __device__ __forceinline__ bool keep_row(const ProbeParams &P, uint64_t g) {
 
 // ------------------------------------------------------------------ plan shapes
 
+// Plan layout read from the kernel parameters (shared-memory offsets, shifts, masks,
+// multipliers): the generic kernels and the structure-keyed specialised kernels use it, so
+// a new batch with the same plan structure reuses the compiled kernel; the layout-keyed
+// variant (GACE_JIT_LAYOUT=1, design comparisons) bakes these in as immediates instead.
+struct RtLayout {
+    __device__ static uint32_t dbg(const ProbeParams &P) { return P.dbg; }
+    __device__ static int64_t base(const ProbeParams &P, int s) { return P.slot[s].base; }
+    __device__ static int64_t clo(const ProbeParams &P, int s) { return P.slot[s].clamp_lo; }
+    __device__ static int64_t chi(const ProbeParams &P, int s) { return P.slot[s].clamp_hi; }
+    __device__ static uint32_t s1(const ProbeParams &P, int s) { return P.slot[s].s1; }
+    __device__ static uint32_t lutb(const ProbeParams &P, int s) { return 4 * P.slot[s].lut_w; }
+    __device__ static uint32_t histb(const ProbeParams &P, int s) { return P.slot[s].hist_addr; }
+    __device__ static uint32_t hllw(const ProbeParams &P, int s) { return P.slot[s].hll_idx; }
+    __device__ static uint32_t bmaddr(const ProbeParams &P, int s) { return P.slot[s].bm_addr; }
+    __device__ static uint32_t bmbase(const ProbeParams &P, int s) { return (uint32_t)P.slot[s].bm_base; }
+    __device__ static uint32_t bmnv(const ProbeParams &P, int s) { return P.slot[s].bm_nvals; }
+    __device__ static uint32_t hllout(const ProbeParams &P, int s) { return P.slot[s].hll_out; }
+    __device__ static uint32_t sb(const ProbeParams &P, int s) { return P.slot[s].sb; }
+    __device__ static uint32_t bmask(const ProbeParams &P, int s) { return P.slot[s].bmask; }
+    __device__ static uint32_t t1mul(const ProbeParams &P, int s) { return P.slot[s].t1_mul; }
+    __device__ static uint32_t t1ones(const ProbeParams &P, int s) { return P.slot[s].t1_ones; }
+    __device__ static uint32_t t1dmask(const ProbeParams &P, int s) { return P.slot[s].t1_dmask; }
+    __device__ static uint32_t t1sp(const ProbeParams &P, int s) { return P.slot[s].t1_sp; }
+    __device__ static uint32_t t1cutsh(const ProbeParams &P, int s) { return P.slot[s].t1_cutsh; }
+    __device__ static uint32_t t1cutmul(const ProbeParams &P, int s) { return P.slot[s].t1_cutmul; }
+    __device__ static uint32_t submask(const ProbeParams &P, int s) { return P.slot[s].submask; }
+    __device__ static uint32_t submul(const ProbeParams &P, int s) { return P.slot[s].sub_mul; }
+    __device__ static uint32_t cellmul(const ProbeParams &P, int s) { return P.slot[s].cell_mul; }
+    __device__ static uint32_t foldb(const ProbeParams &P, int s) { return P.slot[s].fold_b; }
+    __device__ static uint32_t foldz(const ProbeParams &P, int s) { return P.slot[s].fold_z; }
+    __device__ static uint32_t mapb(const ProbeParams &P, int s) {      // packed group's map, or kNone
+        return P.slot[s].prim_b >= 0 ? P.grp[P.slot[s].prim_b].map_addr : kNone;
+    }
+    __device__ static uint32_t ggridb(const ProbeParams &P, int g) { return P.grp[g].grid_addr; }
+    __device__ static uint32_t gnbs(const ProbeParams &P, int g) { return P.grp[g].nbs; }
+    __device__ static uint32_t gmapb(const ProbeParams &P, int g) { return P.grp[g].map_addr; }
+};
+
 // Generic shape: only NC / SAMPLE / I64 are compile-time.
 template <int NC_, bool SAMPLE_, bool I64_>
-struct RtShape {
+struct RtShape : RtLayout {
     static constexpr int NC = NC_;
     static constexpr bool SAMPLE = SAMPLE_;
     static constexpr bool I64 = I64_;
@@ -230,41 +268,9 @@ struct RtShape {
     __device__ static constexpr int gb(int) { return 0; }
     __device__ static constexpr bool ggrid(int) { return false; }
     __device__ static constexpr bool gdirect(int) { return false; }
-    // plan layout (read from the parameters; JitShape bakes them in as immediates)
     __device__ static bool sclamp(const ProbeParams &P, int) { return P.clamp; }
-    __device__ static uint32_t dbg(const ProbeParams &P) { return P.dbg; }
-    __device__ static int64_t base(const ProbeParams &P, int s) { return P.slot[s].base; }
-    __device__ static int64_t clo(const ProbeParams &P, int s) { return P.slot[s].clamp_lo; }
-    __device__ static int64_t chi(const ProbeParams &P, int s) { return P.slot[s].clamp_hi; }
-    __device__ static uint32_t s1(const ProbeParams &P, int s) { return P.slot[s].s1; }
-    __device__ static uint32_t lutb(const ProbeParams &P, int s) { return 4 * P.slot[s].lut_w; }
-    __device__ static uint32_t histb(const ProbeParams &P, int s) { return P.slot[s].hist_addr; }
-    __device__ static uint32_t hllw(const ProbeParams &P, int s) { return P.slot[s].hll_idx; }
     __device__ static bool hllbm(const ProbeParams &P, int s) { return P.slot[s].bm_addr != kNone; }
-    __device__ static uint32_t bmaddr(const ProbeParams &P, int s) { return P.slot[s].bm_addr; }
-    __device__ static uint32_t bmbase(const ProbeParams &P, int s) { return (uint32_t)P.slot[s].bm_base; }
-    __device__ static uint32_t bmnv(const ProbeParams &P, int s) { return P.slot[s].bm_nvals; }
-    __device__ static uint32_t hllout(const ProbeParams &P, int s) { return P.slot[s].hll_out; }
-    __device__ static uint32_t sb(const ProbeParams &P, int s) { return P.slot[s].sb; }
-    __device__ static uint32_t bmask(const ProbeParams &P, int s) { return P.slot[s].bmask; }
-    __device__ static uint32_t t1mul(const ProbeParams &P, int s) { return P.slot[s].t1_mul; }
-    __device__ static uint32_t t1ones(const ProbeParams &P, int s) { return P.slot[s].t1_ones; }
-    __device__ static uint32_t t1dmask(const ProbeParams &P, int s) { return P.slot[s].t1_dmask; }
-    __device__ static uint32_t t1sp(const ProbeParams &P, int s) { return P.slot[s].t1_sp; }
-    __device__ static uint32_t t1cutsh(const ProbeParams &P, int s) { return P.slot[s].t1_cutsh; }
-    __device__ static uint32_t t1cutmul(const ProbeParams &P, int s) { return P.slot[s].t1_cutmul; }
-    __device__ static uint32_t submask(const ProbeParams &P, int s) { return P.slot[s].submask; }
-    __device__ static uint32_t submul(const ProbeParams &P, int s) { return P.slot[s].sub_mul; }
-    __device__ static uint32_t cellmul(const ProbeParams &P, int s) { return P.slot[s].cell_mul; }
     __device__ static constexpr bool fold(const ProbeParams &, int) { return false; }
-    __device__ static constexpr uint32_t foldb(const ProbeParams &, int) { return 0u; }
-    __device__ static constexpr uint32_t foldz(const ProbeParams &, int) { return 0u; }
-    __device__ static uint32_t mapb(const ProbeParams &P, int s) {      // packed group's map, or kNone
-        return P.slot[s].prim_b >= 0 ? P.grp[P.slot[s].prim_b].map_addr : kNone;
-    }
-    __device__ static uint32_t ggridb(const ProbeParams &P, int g) { return P.grp[g].grid_addr; }
-    __device__ static uint32_t gnbs(const ProbeParams &P, int g) { return P.grp[g].nbs; }
-    __device__ static uint32_t gmapb(const ProbeParams &P, int g) { return P.grp[g].map_addr; }
 };
 
 // ------------------------------------------------------------------ row units

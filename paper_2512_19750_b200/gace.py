@@ -36,7 +36,7 @@ EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "
            "gace_table_graph_stats", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv", "gace_cache_create", "gace_cache_destroy", "gace_cache_put",
            "gace_cache_lookup", "gace_cache_invalidate", "gace_cache_stats",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
-           "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
+           "gace_jit_sync", "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
 
 class GaceError(RuntimeError):
@@ -109,6 +109,7 @@ def lib() -> ctypes.CDLL:
     L.gace_gate.argtypes = [vp, u32, vp, vp, u32, vp, u32, vp, ctypes.POINTER(u32), vp]
     L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
     L.gace_nccl_unique_id.argtypes = [vp]
+    L.gace_jit_sync.argtypes = [dbl, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
     L.gace_debug_jit_compile.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, dbl, ctypes.POINTER(u64)]
     L.gace_debug_buckets.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, u32, vp, u64, vp,
                                      ctypes.POINTER(u32), vp, u32, ctypes.POINTER(u32)]
@@ -183,6 +184,13 @@ def debug_jit_compile(dtypes, dlo, dhi, host: bool, preds, pairs, hll_cols, samp
                                         _ptr(P), len(P), _ptr(Q), len(Q), mask, float(sample_rate),
                                         ctypes.byref(n)))
     return int(n.value)
+
+
+def jit_sync(timeout_ms: float = 120_000.0) -> dict:
+    """Wait for the background compiles of specialised scan kernels (gace_jit_sync)."""
+    c, f, p = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib().gace_jit_sync(float(timeout_ms), ctypes.byref(c), ctypes.byref(f), ctypes.byref(p)))
+    return {"compiled": c.value, "failed": f.value, "pending": p.value}
 
 
 def kernel_launches() -> int:

@@ -271,22 +271,56 @@ def force_jit(monkeypatch):
     yield
 
 
+@pytest.mark.parametrize("layout", ["0", "1"])
 @pytest.mark.parametrize("name,nrows,rate", [
     ("C1", 100_003, 1.0), ("C1", 50_001, 0.3), ("C2", 100_001, 0.01), ("C3", 200_002, 1.0),
     ("C4", 60_003, 1.0), ("C5", 120_001, 1.0), ("C5_i64", 60_007, 1.0), ("C5", 50_000, 0.05),
 ])
-def test_specialised_kernel_parity(G, oracle, force_jit, name, nrows, rate):
-    """The NVRTC plan-specialised kernel (the one large scans run) against the oracle."""
+def test_specialised_kernel_parity(G, oracle, force_jit, monkeypatch, name, nrows, rate, layout):
+    """The NVRTC plan-specialised kernels (the ones large scans run) against the oracle:
+    layout "0" = specialised for the plan structure (layout from the kernel parameters,
+    jit == 1), "1" = structure and layout baked in (jit == 2)."""
+    monkeypatch.setenv("GACE_JIT_LAYOUT", layout)
     w = synth.get(name, nrows)
     cols = [x.numpy() for x in w.table()]
     want = oracle.probe(cols, w.preds, w.pairs, rate=rate, seed=23, hll_cols=w.hll_cols)
     t = G.Table([torch.from_numpy(c).cuda() for c in cols])
     try:
         got = t.probe(w.preds, w.pairs, rate, 23, w.hll_cols)
-        assert t.last_timing()["jit"] == 1, G.lib().gace_last_error()
+        assert t.last_timing()["jit"] == 1 + int(layout), G.lib().gace_last_error()
     finally:
         t.detach()
     _assert_same(got, want)
+
+
+def test_background_specialisation(G, oracle, monkeypatch):
+    """Default JIT policy on a small table forced over the size threshold: the first probe
+    runs the generic kernel while both specialised kernels compile in the background, the
+    next ones run the structure-keyed and then the layout-keyed kernel; a second batch of
+    the same structure (shifted bind values) reuses the structure-keyed kernel at once.
+    Every result equals the oracle."""
+    monkeypatch.delenv("GACE_JIT", raising=False)
+    monkeypatch.delenv("GACE_JIT_LAYOUT", raising=False)
+    monkeypatch.setenv("GACE_JIT_MIN_ROWS", "1")
+    w = synth.get("C5", 90_001)
+    cols = [x.numpy() for x in w.table()]
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols])
+    try:
+        want = oracle.probe(cols, w.preds, w.pairs, rate=1.0, seed=0, hll_cols=w.hll_cols)
+        kinds = []
+        for k in range(3):
+            _assert_same(t.probe(w.preds, w.pairs, 1.0, 0, w.hll_cols), want)
+            kinds.append(t.last_timing()["jit"])
+            if k == 0:
+                G.jit_sync()
+        assert kinds[0] in (0, 1, 2) and kinds[2] == 2, kinds
+        P2 = w.preds.copy()
+        P2["a"] += 3
+        P2["b"] += 3
+        want2 = oracle.probe(cols, P2, w.pairs, rate=1.0, seed=0, hll_cols=w.hll_cols)
+        _assert_same(t.probe(P2, w.pairs, 1.0, 0, w.hll_cols), want2)
+    finally:
+        t.detach()
 
 
 def test_specialised_kernel_edge_shapes(G, oracle, force_jit):

@@ -10,11 +10,13 @@ import synth  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
 out = sys.argv[2] if len(sys.argv) > 2 else f"build/jit_{name}.cu"
+rows = int(sys.argv[3]) if len(sys.argv) > 3 else None     # default: the workload's full size
+# GACE_DEBUG_CLUSTERED=<slot mask> compiles the clustered-column path (C5: l_orderkey = 1)
 os.makedirs("build", exist_ok=True)
 os.environ["GACE_JIT_SRC"] = out
 from paper_2512_19750_b200 import gace  # noqa: E402
 
-w = synth.get(name, 1 << 20)
+w = synth.get(name, rows)
 dt = [0 if c.dtype == "i32" else 1 for c in w.columns]
 gace.debug_jit_compile(dt, [c.lo for c in w.columns], [c.hi for c in w.columns], False, w.preds, w.pairs,
                        w.hll_cols, w.rate)
