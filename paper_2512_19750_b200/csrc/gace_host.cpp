@@ -210,6 +210,7 @@ struct gace_table {
     void *jit_fn[2] = {nullptr, nullptr};
     int jit_kind[2] = {0, 0};
     std::string jit_ssrc[2], jit_lsrc[2];
+    uint64_t plan_calls = 0;           // probes of the cached plan (layout-keyed compile on the 2nd)
     // CUDA-graph replay of repeated identical probes (gace_table_set_graphs)
     bool graphs = false;
     uint64_t plan_gen = 0;
@@ -596,7 +597,11 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                 const int A = o ? G.s1 : G.s0, B = o ? G.s0 : G.s1;
                 std::vector<int64_t> TB = side_bps(G, B);
                 const double cells = (double)pl.slots[A].nb * (double)(TB.size() + 1);
-                const double score = 4.0 * !has_hist[A] + 2.0 * (!has_prim[B] && TB.size() + 1 <= kSubMax) - cells * 1e-6;
+                // ties go to the lower slot as the A side -- not to the smaller grid: the
+                // orientation is part of the specialised kernel's structure, so it must not
+                // change when a bind sweep moves the predicate bounds (same template, same kernel)
+                (void)cells;
+                const double score = 4.0 * !has_hist[A] + 2.0 * (!has_prim[B] && TB.size() + 1 <= kSubMax) - 0.5 * o;
                 if (score > best) {
                     best = score;
                     G.a = A;
@@ -1729,6 +1734,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         t->plan = fresh;
         t->plan_key.swap(key);
         t->plan_gen++;
+        t->plan_calls = 0;
         for (int i = 0; i < 2; ++i) {
             t->jit_fn[i] = nullptr;
             t->jit_kind[i] = 0;
@@ -1776,6 +1782,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     bool i64 = false;
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     const int jm = jit_mode(), jl = jit_layout_mode();
+    ++t->plan_calls;
     // rows per launch: keep every CTA's u32 bins below 2^31
     // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
     const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
@@ -1813,8 +1820,11 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
                 }
             }
             if (fn && t->jit_kind[si] != 2) t->jit_kind[si] = jl == 1 ? 2 : 1;
-            if (jl == 2 && !t->jit_lsrc[si].empty()) jit_prefetch(t->device, t->jit_lsrc[si]);
         }
+        // a batch probed again is worth its own layout-keyed kernel (compiled in the
+        // background; a stream of distinct batches never queues one)
+        if (jl == 2 && t->plan_calls >= 2 && t->jit_kind[si] != 2 && !t->jit_lsrc[si].empty())
+            jit_prefetch(t->device, t->jit_lsrc[si]);
         scan_fn = fn;
         scan_kind = fn ? t->jit_kind[si] : 0;
         if (!fn && jm == 1) {
@@ -2686,6 +2696,40 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
 
 // Test hook: plan a batch (as gace_debug_buckets) and compile its specialised probe kernel
 // with NVRTC without launching it.  *cubin_bytes = size of the compiled kernel image.
+// Test hook: the generated JitShape source of a batch (structure-keyed, or layout-keyed with
+// layout != 0), without compiling it.  out[cap] receives it NUL-terminated; *len its length.
+extern "C" gace_status gace_debug_jit_source(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
+                                             const int64_t *dhi, int host, const gace_pred *preds,
+                                             uint32_t npreds, const gace_pair *pairs, uint32_t npairs,
+                                             uint64_t hll_mask, double sample_rate, int layout, char *out,
+                                             uint64_t cap, uint64_t *len) {
+    if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "bad arguments");
+    gace_table t;
+    t.ncols = ncols;
+    t.host = host != 0;
+    for (uint32_t c = 0; c < ncols; ++c) {
+        t.dtypes.push_back((int)dtypes[c]);
+        t.dlo.push_back(dlo[c]);
+        t.dhi.push_back(dhi[c]);
+    }
+    gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, sample_rate, hll_mask, GACE_HLL_P);
+    if (st) return st;
+    Plan pl;
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    if (st) return st;
+    bool i64 = false;
+    for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
+    const std::string src = jit_shape_source(pl, sample_rate < 1.0, i64, std::vector<uint8_t>(pl.slots.size(), 0),
+                                             layout != 0);
+    if (len) *len = src.size();
+    if (out && cap) {
+        const size_t n = std::min<size_t>(cap - 1, src.size());
+        memcpy(out, src.data(), n);
+        out[n] = 0;
+    }
+    return GACE_OK;
+}
+
 extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *dtypes, const int64_t *dlo,
                                               const int64_t *dhi, int host, const gace_pred *preds,
                                               uint32_t npreds, const gace_pair *pairs, uint32_t npairs,

@@ -45,7 +45,7 @@ def _full(G, oracle, name, rate=None, seed=None, monkeypatch=None):
     got, kinds = [], []
     t = G.Table(dcols, device=0)
     try:
-        for k in range(2):
+        for k in range(3):
             got.append(t.probe(w.preds, w.pairs, rate, seed, w.hll_cols))
             kinds.append(t.last_timing()["jit"])
             G.jit_sync()
@@ -80,9 +80,9 @@ def _full(G, oracle, name, rate=None, seed=None, monkeypatch=None):
 def test_bench_config_full_size_vs_oracle(G, oracle, monkeypatch, name):
     monkeypatch.delenv("GACE_JIT", raising=False)
     kinds = _full(G, oracle, name, monkeypatch=monkeypatch if name in ("C5", "C3") else None)
-    assert kinds[1] == 2, kinds                 # the layout-specialised kernel bench.py times
-    if len(kinds) > 2:
-        assert kinds[2] == 1, kinds             # structure-specialised (a new batch's kernel)
+    assert kinds[2] == 2, kinds                 # the layout-specialised kernel bench.py times
+    if len(kinds) > 3:
+        assert kinds[3] == 1, kinds             # structure-specialised (a new batch's kernel)
 
 
 def test_c5_full_size_sampled_vs_oracle(G, oracle):

@@ -311,8 +311,7 @@ def test_background_specialisation(G, oracle, monkeypatch):
         for k in range(3):
             _assert_same(t.probe(w.preds, w.pairs, 1.0, 0, w.hll_cols), want)
             kinds.append(t.last_timing()["jit"])
-            if k == 0:
-                G.jit_sync()
+            G.jit_sync()
         assert kinds[0] in (0, 1, 2) and kinds[2] == 2, kinds
         P2 = w.preds.copy()
         P2["a"] += 3

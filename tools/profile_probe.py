@@ -2,8 +2,8 @@
 
     python tools/profile_probe.py [--config C5] [--rows N] [--probes 3] [--rate R]
 
-The first probe runs whatever kernel is compiled (the generic one on a fresh process);
-after gace_jit_sync the remaining probes run the layout-specialised kernel
+The first probe runs whatever kernel is compiled (the generic one on a fresh process), the
+second the structure-specialised one, and from the third on the layout-specialised kernel
 (`gace_jit_probe`), which is what bench.py times: profile it with
 `ncu -k regex:gace_jit_probe -c 1 ...`.
 """
@@ -38,6 +38,6 @@ for k in range(a.probes):
         r = t.probe(w.preds, w.pairs, rate, w.sample_seed, w.hll_cols)
     tm = t.last_timing()
     print(f"probe {k}: kernel {tm['jit']} scan {tm['scan_ms']:.3f} ms total {tm['total_ms']:.3f} ms", flush=True)
-    if k == 0:
-        gace.jit_sync()
+    if k < 2:
+        gace.jit_sync()             # probe 1: structure-keyed kernel, probe 2 on: layout-keyed
 t.detach()
