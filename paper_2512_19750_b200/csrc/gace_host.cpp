@@ -366,8 +366,24 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     for (int64_t t : S.T) toff.push_back((uint64_t)t - (uint64_t)S.base);   // in [1, span]
     auto le = [&](uint64_t x) { return (uint32_t)(std::upper_bound(toff.begin(), toff.end(), x) - toff.begin()); };
     // sub-bucket of bucket b in the packed group, and whether breakpoint T[i] cuts it
-    auto sub_of = [&](uint32_t b) -> uint32_t { return (!S.TBp || b == 0) ? 0 : count_le(*S.TBp, S.T[b - 1]); };
-    auto cuts = [&](uint32_t i) -> bool { return S.TBp && std::binary_search(S.TBp->begin(), S.TBp->end(), S.T[i]); };
+    // (tabulated once: the cell loops below look them up per cell)
+    std::vector<uint32_t> sub_tab(S.T.size() + 1, 0);
+    std::vector<uint8_t> cut_tab(S.T.size(), 0);
+    if (S.TBp) {
+        for (size_t b = 1; b <= S.T.size(); ++b) sub_tab[b] = count_le(*S.TBp, S.T[b - 1]);
+        for (size_t i = 0; i < S.T.size(); ++i) cut_tab[i] = std::binary_search(S.TBp->begin(), S.TBp->end(), S.T[i]);
+    }
+    auto sub_of = [&](uint32_t b) -> uint32_t { return sub_tab[b]; };
+    auto cuts = [&](uint32_t i) -> bool { return cut_tab[i] != 0; };
+    // #{t in toff : t <= x} for non-decreasing x along a cell sweep (amortised O(1))
+    struct Sweep {
+        const std::vector<uint64_t> &t;
+        uint32_t j = 0;
+        uint32_t operator()(uint64_t x) {
+            while (j < t.size() && t[j] <= x) ++j;
+            return j;
+        }
+    };
     S.s1 = s1;
     S.l1.clear();
     S.l2.clear();
@@ -411,11 +427,13 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     };
     const uint64_t ncells = (span >> s1) + 1;
     const uint64_t csize = 1ull << s1;
+    S.l1.reserve(ncells);
+    Sweep at_lo{toff}, at_hi{toff};
     if (S.fmt == FMT1T) {      // one in-cell threshold per cell (gace_plan.h FMT1T)
         auto bs = [&](uint32_t b) { return (b + 1) | (sub_of(b) << S.sb); };
         for (uint64_t k = 0; k < ncells && ok; ++k) {
             const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
-            const uint32_t b0 = le(lo), cnt = le(hi) - b0;       // breakpoints in (lo, hi]
+            const uint32_t b0 = at_lo(lo), cnt = at_hi(hi) - b0;   // breakpoints in (lo, hi]
             if (cnt == 0) {
                 S.l1.push_back(bs(b0) - 1);                        // t = 0: always "crossed"
             } else if (cnt == 1) {
@@ -431,8 +449,8 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     }
     for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
-        const uint32_t b0 = le(lo);
-        if (le(hi) == b0) {                                        // plain cell
+        const uint32_t b0 = at_lo(lo);
+        if (at_hi(hi) == b0) {                                     // plain cell
             S.l1.push_back(b0 | (sub_of(b0) << kSubShift));
         } else {                                                   // boundary cell -> record
             const uint4 e = node(lo, hi, s1);
@@ -587,35 +605,51 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         TB.erase(std::unique(TB.begin(), TB.end()), TB.end());
         return TB;
     };
-    // orientation: prefer making a column the full-resolution side of one group (its
-    // histogram then comes from the grid) and the packed sub-bucket side of one group
+    // orientation: every column should be the full-resolution (A) side of some group -- its
+    // histogram then comes from that grid's row sums -- and the packed sub-bucket (B) side
+    // of at most one group.  Chosen from the group topology only (exhaustively for up to 12
+    // groups, ties to the lowest orientation mask; greedily beyond), never from the grid
+    // sizes: the orientation is part of the specialised kernel's structure, so a bind sweep
+    // that moves the predicate bounds keeps its kernel.
     {
-        std::vector<int> has_hist(pl.slots.size(), 0), has_prim(pl.slots.size(), 0);
-        for (auto &G : pl.groups) {
-            double best = -1e300;
-            for (int o = 0; o < 2; ++o) {
+        const size_t G_ = pl.groups.size(), ns = pl.slots.size();
+        std::vector<std::vector<int64_t>> tb[2];            // tb[o][g]: B-side breakpoints if oriented o
+        for (int o = 0; o < 2; ++o)
+            for (auto &G : pl.groups) tb[o].push_back(side_bps(G, o ? G.s0 : G.s1));
+        auto score_of = [&](uint32_t mask, int upto) {
+            std::vector<int> has_hist(ns, 0), has_prim(ns, 0);
+            int sc = 0;
+            for (int g = 0; g < upto; ++g) {
+                const int o = (mask >> g) & 1;
+                const Group &G = pl.groups[g];
                 const int A = o ? G.s1 : G.s0, B = o ? G.s0 : G.s1;
-                std::vector<int64_t> TB = side_bps(G, B);
-                const double cells = (double)pl.slots[A].nb * (double)(TB.size() + 1);
-                // ties go to the lower slot as the A side -- not to the smaller grid: the
-                // orientation is part of the specialised kernel's structure, so it must not
-                // change when a bind sweep moves the predicate bounds (same template, same kernel)
-                (void)cells;
-                const double score = 4.0 * !has_hist[A] + 2.0 * (!has_prim[B] && TB.size() + 1 <= kSubMax) - 0.5 * o;
-                if (score > best) {
-                    best = score;
-                    G.a = A;
-                    G.b = B;
-                    G.TB.swap(TB);
-                }
+                if (!has_hist[A]) { has_hist[A] = 1; sc += 4; }
+                if (!has_prim[B] && tb[o][g].size() + 1 <= kSubMax) { has_prim[B] = 1; sc += 2; }
             }
+            return sc;
+        };
+        uint32_t best_mask = 0;
+        if (G_ <= 12) {
+            int best = -1;
+            for (uint32_t m = 0; m < (1u << G_); ++m) {
+                const int sc = score_of(m, (int)G_);
+                if (sc > best) { best = sc; best_mask = m; }
+            }
+        } else {
+            for (size_t g = 0; g < G_; ++g)
+                if (score_of(best_mask | (1u << g), (int)g + 1) > score_of(best_mask, (int)g + 1)) best_mask |= 1u << g;
+        }
+        for (size_t g = 0; g < G_; ++g) {
+            Group &G = pl.groups[g];
+            const int o = (best_mask >> g) & 1;
+            G.a = o ? G.s1 : G.s0;
+            G.b = o ? G.s0 : G.s1;
+            G.TB = tb[o][g];
             G.na = pl.slots[G.a].nb;
             // row stride = sub-bucket count rounded up to odd: rows then start in different
             // shared-memory banks, so a warp whose rows share one sub-bucket (a sorted B
             // column) does not serialise on a single bank (the extra column stays zero)
             G.nbs = ((uint32_t)G.TB.size() + 1) | 1u;
-            has_hist[G.a] = 1;
-            if (G.nbs <= kSubMax) has_prim[G.b] = 1;
         }
     }
     // ---- budget: grids (+ the B side's bucket -> sub-bucket map) in increasing size while
@@ -725,7 +759,10 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             const uint32_t mx = t1_max_s1(S, nsub_of(S));     // finer than the target when the fields force it
             if (t1s > mx && mx >= 1 && (span >> mx) + 1 <= 32768) t1s = mx;
         }
-        if (narrow && !S.clamp && S.dtype == GACE_I32 && span < 16384) {
+        // exact cells: small int32 spans; up to 32767 buckets when no sub-bucket is packed
+        // (bucket field bits 0..14: C3's 1025 EQ binds); a clamped span too -- keys outside
+        // it land in an edge cell, so such a column never takes its HLL from the cells
+        if (S.dtype == GACE_I32 && span < 16384 && (narrow || (S.prim_b < 0 && S.nb < 32768))) {
             S.fmt = FMTEX;
             s1[i] = 0;
         } else if (use_t1 && t1s <= t1_max_s1(S, nsub_of(S))) {
@@ -781,13 +818,16 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             if (S.mode == MODE_LUT) used += lut_bytes(S);
         for (auto &S : pl.slots) {
             if (!S.has_hll || S.dtype != GACE_I32 || t->host || getenv("GACE_NO_BITMAP")) continue;
-            if (S.mode == MODE_LUT && S.fmt == FMTEX) continue;
+            if (S.mode == MODE_LUT && S.fmt == FMTEX && !S.clamp) continue;   // (index, rank) in the cells
             const int64_t base = (int64_t)((uint64_t)S.dl & ~31ull);
             const uint64_t words = (((uint64_t)S.dh - (uint64_t)base) >> 5) + 1;
             if (words > 32768) continue;                        // <= 128 KB
             // zeroing and merging the bitmap costs ~words per CTA: worth it when every CTA
-            // scans many rows per bitmap word (C4: 200M rows, 2K words; not C1's 1M rows)
-            if (t->nrows < 32ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
+            // scans several rows per bitmap word (C4: 200M rows, 2K words; C3: 100M rows, 32K
+            // words; not C1's 1M rows).  Rows per rank, not this shard's own count, so every
+            // rank of a multi-GPU table makes the same choice (identical plans).
+            const uint64_t rows = t->has_dist ? t->dist.nrows_total / (uint64_t)t->dist.nranks : t->nrows;
+            if (rows < 8ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
             const size_t bytes = 4 * words;
             if (bytes > 4ull * kHllM && used + bytes - 4ull * kHllM > kSmemBudget) continue;
             used = used + bytes - 4ull * kHllM;
@@ -879,7 +919,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                 img16[k] = (uint16_t)((c & kSpecial) ? 0x8000u | (S.l2_idx + (c & kRecMask)) : idx | (sub << 9));
             } else if (S.fmt == FMTEX) {                   // cell k is the key base + k
                 uint32_t hidx = 0, rank = 0;
-                if (S.has_hll) {
+                if (S.has_hll && !S.clamp && !S.bm) {
                     const uint32_t h = host_fmix32((uint32_t)(int32_t)(S.base + (int64_t)k));
                     hidx = h >> (32 - kHllP);
                     rank = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
@@ -1015,7 +1055,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         // the GPU -- gace_probe launches it the first time a plan needs it -- and kept in the
         // table's d_hceil at byte offset col * 4096)
         Q.hceil_off = kNone;
-        if (S.has_hll && !S.bm && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX) &&
+        if (S.has_hll && !S.bm && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX && !S.clamp) &&
             (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL"))
             Q.hceil_off = (uint32_t)S.col * kHllM;
         Q.hll_out = S.hll_out;
@@ -1027,7 +1067,8 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         Q.fmt = S.fmt;
         // bs layout per format: the plain level-1 word is used as bs directly
         const bool lutm = S.has_preds && S.mode == MODE_LUT;
-        Q.sb = (uint8_t)(!lutm ? 16 : S.fmt == FMT1T ? S.sb : S.fmt == FMT32 ? kSubShift : 9);
+        Q.sb = (uint8_t)(!lutm ? 16 : S.fmt == FMT1T ? S.sb : S.fmt == FMT32 ? kSubShift
+                                                : (S.fmt == FMTEX && S.nb > 512) ? 15 : 9);
         Q.bmask = (1u << Q.sb) - 1u;
         Q.submask = !lutm || S.fmt == FMT1T ? 0xFFFFFFFFu : S.fmt == FMT32 ? kSubMask : 63u;
         Q.sub_mul = 1u << (32 - Q.sb);
@@ -1804,10 +1845,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
         if (!fn) {
             std::vector<uint8_t> cl(pl.slots.size(), 0);
             for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
-            if (t->jit_ssrc[si].empty()) {
-                t->jit_ssrc[si] = jit_shape_source(pl, sample, i64, cl, jl == 1);
-                if (jl == 2) t->jit_lsrc[si] = jit_shape_source(pl, sample, i64, cl, true);
-            }
+            if (t->jit_ssrc[si].empty()) t->jit_ssrc[si] = jit_shape_source(pl, sample, i64, cl, jl == 1);
             if (jl == 2 && !t->jit_lsrc[si].empty() && jit_lookup(t->device, t->jit_lsrc[si], &fn)) {
                 t->jit_kind[si] = 2;                               // repeat of a batch seen before
                 t->jit_lsrc[si].clear();
@@ -1822,9 +1860,13 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
             if (fn && t->jit_kind[si] != 2) t->jit_kind[si] = jl == 1 ? 2 : 1;
         }
         // a batch probed again is worth its own layout-keyed kernel (compiled in the
-        // background; a stream of distinct batches never queues one)
-        if (jl == 2 && t->plan_calls >= 2 && t->jit_kind[si] != 2 && !t->jit_lsrc[si].empty())
+        // background; a stream of distinct batches never generates or queues one)
+        if (jl == 2 && t->plan_calls >= 2 && t->jit_kind[si] == 1 && t->jit_lsrc[si].empty()) {
+            std::vector<uint8_t> cl(pl.slots.size(), 0);
+            for (size_t i = 0; i < pl.slots.size(); ++i) cl[i] = t->clustered[pl.slots[i].col];
+            t->jit_lsrc[si] = jit_shape_source(pl, sample, i64, cl, true);
             jit_prefetch(t->device, t->jit_lsrc[si]);
+        }
         scan_fn = fn;
         scan_kind = fn ? t->jit_kind[si] : 0;
         if (!fn && jm == 1) {
@@ -2629,6 +2671,7 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;
+    t.nrows = getenv("GACE_DEBUG_ROWS") ? strtoull(getenv("GACE_DEBUG_ROWS"), nullptr, 10) : 0;   // row-count heuristics
     for (uint32_t c = 0; c < ncols; ++c) {
         t.dtypes.push_back((int)dtypes[c]);
         t.dlo.push_back(dlo[c]);
@@ -2663,7 +2706,10 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
-            b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base, Q.sb);
+            if (Q.fmt == FMTEX)                    // the kernel's decode: the cell word's bucket field
+                b = M.u32(Q.lut_w + ((uint32_t)x - (uint32_t)Q.base)) & Q.bmask;
+            else
+                b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base, Q.sb);
         } else {
             int64_t x = values[k];
             if (pl.clamp) x = std::min(std::max(x, Q.clamp_lo), Q.clamp_hi);
@@ -2707,6 +2753,7 @@ extern "C" gace_status gace_debug_jit_source(uint32_t ncols, const gace_dtype *d
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;
+    t.nrows = getenv("GACE_DEBUG_ROWS") ? strtoull(getenv("GACE_DEBUG_ROWS"), nullptr, 10) : 0;   // row-count heuristics
     for (uint32_t c = 0; c < ncols; ++c) {
         t.dtypes.push_back((int)dtypes[c]);
         t.dlo.push_back(dlo[c]);
@@ -2738,6 +2785,7 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;
+    t.nrows = getenv("GACE_DEBUG_ROWS") ? strtoull(getenv("GACE_DEBUG_ROWS"), nullptr, 10) : 0;   // row-count heuristics
     for (uint32_t c = 0; c < ncols; ++c) {
         t.dtypes.push_back((int)dtypes[c]);
         t.dlo.push_back(dlo[c]);

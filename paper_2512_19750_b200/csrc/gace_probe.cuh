@@ -156,6 +156,11 @@ __device__ __noinline__ uint32_t hll_bound(uint32_t hll_idx, uint32_t *G, int s,
     return min(__reduce_min_sync(0xFFFFFFFFu, L), 255u) | (complete ? 256u : 0u);
 }
 
+// Bitmaps of at most this many words are pushed into the merged bitmap at the refresh points
+// (so a domain the scan covers completely stops costing work early, C4); larger ones (C3's
+// 2^20-value Zipf domain: 32K words, never complete) only at the CTA's end.
+constexpr uint32_t kBmRefreshWords = 4096;
+
 // Presence-bitmap slot s: this warp ORs its 1/nwarps slice of the CTA's bitmap into the
 // merged bitmap g_bm, counting the bits it sets there for the first time, and reports
 // whether the merged bitmap now holds every value of the column domain.  The registers
@@ -555,7 +560,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
     } else if (Sh::hll(P, s) && !(dbg & 8)) {
         if ((bmfull >> s) & 1u) return;        // registers at their ceilings: nothing can change
         uint32_t *R = sm + Sh::hllw(P, s);
-        if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX) {
+        if (Sh::mode(P, s) == MODE_LUT && Sh::fmt(P, s) == FMTEX && !Sh::sclamp(P, s)) {
             // (index, rank) precomputed per key value in its exact cell.  A CTA needs each
             // value's contribution once: the first thread to apply it clears the rank in the
             // cell (a benign race -- every writer stores the same word), so repeats of the
@@ -754,6 +759,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                         if (hb >> 8) bmfull |= 1u << s;       // registers at their ceilings: column complete
                     }
                     else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
+                             P.slot[s].bm_words <= kBmRefreshWords &&
                              bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
                                      P.slot[s].bm_words, P.g_bmcnt + s, Sh::bmnv(P, s)))
                         bmfull |= 1u << s;
@@ -834,6 +840,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                             if (hb >> 8) bmfull |= 1u << s;       // registers at their ceilings: column complete
                         }
                         else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
+                                 P.slot[s].bm_words <= kBmRefreshWords &&
                                  bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
                                          P.slot[s].bm_words, P.g_bmcnt + s, Sh::bmnv(P, s)))
                             bmfull |= 1u << s;

@@ -34,6 +34,10 @@ def _same(got, want):
 @pytest.mark.parametrize("name,nrows,rate", [("C1", 100_003, 1.0), ("C5", 120_001, 1.0), ("C2", 200_001, 0.01)])
 def test_graph_replay_parity(G, oracle, monkeypatch, jit, name, nrows, rate):
     monkeypatch.setenv("GACE_JIT", jit)
+    # one specialised kernel kind (the layout-keyed one, compiled synchronously): a kernel
+    # that a background compile upgrades mid-sequence changes the graph key, so the counts
+    # of captures below would depend on the compile's timing (results would not)
+    monkeypatch.setenv("GACE_JIT_LAYOUT", "1")
     w = synth.get(name, nrows)
     cols_np = [x.numpy() for x in w.table()]
     want = oracle.probe(cols_np, w.preds, w.pairs, rate=rate, seed=5, hll_cols=w.hll_cols)

@@ -448,3 +448,57 @@ def test_presence_bitmap_hll(G, oracle, monkeypatch, name, nrows, rate):
     for jit in ("0", "1"):
         monkeypatch.setenv("GACE_JIT", jit)
         _check(G, oracle, cols, w.preds, w.pairs, rate, 29, w.hll_cols)
+
+
+def _high_rank_keys(is64: bool, n: int, seed: int):
+    """Keys whose HLL rank exceeds 16 (the shared-memory registers' in-thermometer range:
+    such ranks also go straight to the merged registers), found with the generator's own
+    hashes restated in numpy (fmix32 / mix64(x + gamma))."""
+    g = np.random.default_rng(seed)
+    out = []
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    while len(out) < n:
+        if is64:
+            x = g.integers(-(1 << 62), 1 << 62, size=1 << 21, dtype=np.int64)
+            with np.errstate(over="ignore"):
+                z = x.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+                z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+                z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+                z = z ^ (z >> np.uint64(31))
+                w = (z << np.uint64(12)) & M
+            ok = w < np.uint64(1 << 48)                      # rank >= 17
+        else:
+            x = g.integers(-(1 << 31), 1 << 31, size=1 << 22, dtype=np.int64).astype(np.int32)
+            h = x.astype(np.uint32).astype(np.uint64)
+            h ^= h >> np.uint64(16)
+            h = (h * np.uint64(0x85EBCA6B)) & np.uint64(0xFFFFFFFF)
+            h ^= h >> np.uint64(13)
+            h = (h * np.uint64(0xC2B2AE35)) & np.uint64(0xFFFFFFFF)
+            h ^= h >> np.uint64(16)
+            w = (h << np.uint64(12)) & np.uint64(0xFFFFFFFF)
+            ok = w < np.uint64(1 << 16)
+        out.extend(x[ok].tolist())
+    return np.array(out[:n], dtype=np.int64 if is64 else np.int32)
+
+
+@pytest.mark.parametrize("jit", ["0", "1"])
+def test_hll_ranks_above_16(G, oracle, monkeypatch, jit):
+    """HLL ranks 17..21 (int32) and 17..53 (int64) -- beyond the 16-bit shared-memory
+    thermometers -- mixed into ordinary keys, with and without predicates on the columns,
+    generic and specialised kernels: registers bit-exact against the oracle."""
+    monkeypatch.setenv("GACE_JIT", jit)
+    g = np.random.default_rng(77)
+    n = 300_007
+    hi32 = _high_rank_keys(False, 64, 1)
+    hi64 = _high_rank_keys(True, 64, 2)
+    a = g.integers(0, 1 << 20, size=n).astype(np.int32)
+    b = g.integers(-(1 << 40), 1 << 40, size=n).astype(np.int64)
+    pos = g.choice(n, size=2000, replace=False)
+    a[pos] = hi32[g.integers(0, len(hi32), size=2000)]
+    b[pos] = hi64[g.integers(0, len(hi64), size=2000)]
+    P = np.array([(0, 5, 0, 1000, 500_000), (1, 1, 0, 0, 0)], dtype=synth.PRED_DTYPE)
+    Q = np.array([(0, 1)], dtype=synth.PAIR_DTYPE)
+    for preds, pairs in ((P, Q), (P[:0], None)):
+        for rate in (1.0, 0.6):
+            _check(G, oracle, [a, b], preds, pairs, rate, 13, [0, 1])
+            _check(G, oracle, [a], preds[preds["col"] == 0], None, rate, 13, [0])

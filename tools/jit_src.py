@@ -17,6 +17,7 @@ os.environ["GACE_JIT_SRC"] = out
 from paper_2512_19750_b200 import gace  # noqa: E402
 
 w = synth.get(name, rows)
+os.environ.setdefault("GACE_DEBUG_ROWS", str(w.nrows))
 dt = [0 if c.dtype == "i32" else 1 for c in w.columns]
 gace.debug_jit_compile(dt, [c.lo for c in w.columns], [c.hi for c in w.columns], False, w.preds, w.pairs,
                        w.hll_cols, w.rate)
