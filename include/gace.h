@@ -329,7 +329,9 @@ typedef struct {
                                (precompiled) kernel, 1 specialised for the plan's
                                structure, 2 specialised for its structure and layout,
                                -1 specialisation failed, generic kernel used            */
-    int32_t pad;
+    int32_t merge;          /* cross-GPU merge of that call: 0 none (one rank, no NCCL),
+                               1 grouped ncclAllReduce sum + max, 2 fused peer-memory
+                               kernel over an NCCL symmetric window (NVLink loads)      */
     double jit_compile_ms;  /* NVRTC compile time spent in that call (0 when cached)   */
 } gace_timing;
 

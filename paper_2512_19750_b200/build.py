@@ -18,8 +18,22 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["gace_kernels.cu", "gace_sets.cu", "gace_host.cpp", "gace_jit.cpp"]
-HEADERS = ["gace_plan.h", "gace_kernels.h", "gace_probe.cuh", "gace_jit.h", "gace_sets.h"]
+SOURCES = ["gace_kernels.cu", "gace_sets.cu", "gace_merge.cu", "gace_host.cpp", "gace_jit.cpp"]
+HEADERS = ["gace_plan.h", "gace_kernels.h", "gace_probe.cuh", "gace_jit.h", "gace_sets.h", "gace_merge.h"]
+
+
+def _nccl_include() -> str | None:
+    """NCCL >= 2.28 headers with the device API (nccl_device.h), for the fused merge kernel
+    (gace_merge.cu).  The library itself is loaded at run time (dlopen), never linked."""
+    try:
+        import nvidia.nccl
+        for d in list(getattr(nvidia.nccl, "__path__", [])):
+            inc = os.path.join(d, "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except ImportError:
+        pass
+    return None
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -55,6 +69,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s] + hdrs + [inc]):
             cmd = [NVCC] + ARCH + COMMON + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
+            if src == "gace_merge.cu":
+                ninc = _nccl_include()
+                cmd[-4:-4] = ["-I", ninc, "-DGACE_NCCL_DEVICE=1"] if ninc else ["-DGACE_NCCL_DEVICE=0"]
             if src.endswith(".cpp"):
                 cmd = [NVCC] + COMMON + ["-I", OBJ, "-x", "c++", "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)

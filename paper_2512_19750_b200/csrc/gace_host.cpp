@@ -34,6 +34,7 @@
 #include "../../include/gace.h"
 #include "gace_jit.h"
 #include "gace_kernels.h"
+#include "gace_merge.h"
 #include "gace_plan.h"
 #include "gace_sets.h"
 
@@ -146,6 +147,9 @@ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 }  // namespace
 
 constexpr uint32_t kMagic = 0x47414345u;   // "GACE"
+// per-rank symmetric window of the fused merge: the largest packed result,
+// [1 + 4096 + 4096 u64 | 8 HLL columns x 4096 registers], rounded up
+constexpr size_t kMergeBytes = 128 * 1024;
 
 // what a captured probe graph bakes in: plan, sampling, seed, ablation bits, scratch buffers
 struct GraphKey {
@@ -187,6 +191,7 @@ struct gace_table {
     void *comm = nullptr;
     bool own_comm = false;
     bool comm_dead = false;            // aborted after an asynchronous NCCL error / timeout
+    MergeState *merge = nullptr;       // fused merge over a symmetric window (gace_merge.cu), or none
     DevBuf d_coll;                     // small collective scratch (attach domains, plan agreement)
     int sms = 148;
     DevBuf d_plan, d_accb[2], d_pre, d_part, d_out, d_nsamp, d_mask, d_stage[2];
@@ -1296,6 +1301,13 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
                     t->dhi[c] = dom[ncols + c];
                 }
             }
+            // the fused merge (NCCL device API, NVLink peer loads; gace_merge.cu) when every
+            // rank is load/store reachable; else the grouped all-reduce (GACE_NCCL_FUSED=0 forces it)
+            const char *fz = getenv("GACE_NCCL_FUSED");
+            if (!(fz && !atoi(fz)) && merge_available()) {
+                std::string why;
+                if (!merge_create(t->comm, dist->nranks, kMergeBytes, &t->merge, &why)) t->merge = nullptr;
+            }
         }
     }
     *out = t;
@@ -1668,6 +1680,8 @@ gace_status gace_table_detach(gace_table *t) {
     cudaSetDevice(t->device);
     if (t->stream) cudaStreamSynchronize(t->stream);
     if (t->copy_stream) cudaStreamSynchronize(t->copy_stream);
+    if (t->merge && !t->comm_dead) merge_destroy(t->merge);
+    t->merge = nullptr;
     if (t->own_comm && t->comm && !t->comm_dead) {
         Nccl *n = nccl();
         if (n) n->CommDestroy(t->comm);
@@ -1812,6 +1826,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // seed and scratch buffers captures the enqueue below (memsets, scan, finalize, D2H and
     // the stage events as external records); later identical calls launch the graph.
     uint64_t nl = 0;                 // our kernel launches enqueued by this call
+    int merge_kind = 0;              // 0 one rank, 1 grouped all-reduce, 2 fused peer-memory kernel
     uint64_t launches = 0;
     double jit_ms = 0;
     int jit_used = 0;
@@ -2013,7 +2028,12 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // buffer (mapped under UVA, same address), so no D2H copy is queued; with several ranks
     // the result stays on the device for the NCCL merge and is copied back after it
     const bool zero_copy = !t->use_nccl && !getenv("GACE_NO_ZERO_COPY");
-    char *out_base = zero_copy ? t->h_out.as<char>() : t->d_out.as<char>();
+    // fused merge: the finalize writes into this rank's symmetric window, the merge kernel
+    // reads every rank's window into d_out
+    size_t win_bytes = 0;
+    char *win = t->merge ? static_cast<char *>(merge_buffer(t->merge, &win_bytes)) : nullptr;
+    const bool fused = win && out_bytes <= win_bytes;
+    char *out_base = fused ? win : zero_copy ? t->h_out.as<char>() : t->d_out.as<char>();
     F.out = reinterpret_cast<unsigned long long *>(out_base);
     F.out_regs = reinterpret_cast<uint8_t *>(out_base + align16(8 * out_words));
     F.g_bm = P.g_bm;
@@ -2033,7 +2053,13 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     nl += (F.njobs + F.hll_blocks ? 2 : 1) + (F.nbm ? 1 : 0);
     CUDA_TRY(rec(t->ev[3], s));
 
-    if (t->use_nccl) {
+    if (fused) {
+        CUDA_TRY(merge_launch(t->merge, (uint32_t)out_words, (uint32_t)align16(8 * out_words), pl.hll_bytes,
+                              t->d_out.p, s));
+        ++nl;
+        merge_kind = 2;
+    } else if (t->use_nccl) {
+        merge_kind = 1;
         Nccl *n = nccl();
         if (!n) return fail(GACE_ENCCL, "libnccl.so.2 not loadable");
         n->GroupStart();
@@ -2093,6 +2119,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     }
     T.scan_launches = launches;
     T.jit = jit_used;
+    T.merge = merge_kind;
     T.jit_compile_ms = jit_ms;
     T.bytes_scanned = t->nrows * bytes_per_row;
     return GACE_OK;

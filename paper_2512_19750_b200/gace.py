@@ -70,7 +70,7 @@ class _Timing(ctypes.Structure):
     _fields_ = [("plan_upload_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
                 ("finalize_ms", ctypes.c_double), ("merge_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("scan_launches", ctypes.c_uint64),
-                ("bytes_scanned", ctypes.c_uint64), ("jit", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("bytes_scanned", ctypes.c_uint64), ("jit", ctypes.c_int32), ("merge", ctypes.c_int32),
                 ("jit_compile_ms", ctypes.c_double)]
 
 

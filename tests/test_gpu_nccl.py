@@ -53,6 +53,7 @@ def test_nccl_merge_matches_oracle(G, oracle, monkeypatch, name, nrows, rate, fo
             np.testing.assert_array_equal(got.regs, r)
         tm = t.last_timing()
         assert tm["merge_ms"] > 0 and tm["d2h_ms"] > 0      # the merge and the copy after it ran
+        assert tm["merge"] in (1, 2), tm                    # all-reduce, or the fused window kernel
     finally:
         t.detach()
 
@@ -115,3 +116,34 @@ def test_nccl_domain_agreement_empty_shard(G, oracle):
         assert got.n_sampled == 0 and not got.counts.any() and not got.joints.any() and not got.regs.any()
     finally:
         t.detach()
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_nccl_merge_kinds(G, oracle, monkeypatch, fused):
+    """Both merge implementations on one rank: the grouped ncclAllReduce (GACE_NCCL_FUSED=0)
+    and the fused kernel over the NCCL symmetric window (LSA barrier, peer loads: SURVEY.md
+    §8(f) NEXT-2b) -- the latter whenever the loaded libnccl has the device API (2.28+)."""
+    monkeypatch.setenv("GACE_NCCL_FUSED", fused)
+    w = synth.get("C5", 100_003)
+    cols = [x.numpy() for x in w.table()]
+    t = _nccl_table(G, [torch.from_numpy(c).cuda() for c in cols])
+    try:
+        for rate in (1.0, 0.3):
+            got = t.probe(w.preds, w.pairs, rate, 8, w.hll_cols)
+            n, c, j, r = oracle.probe(cols, w.preds, w.pairs, rate=rate, seed=8, hll_cols=w.hll_cols)
+            assert got.n_sampled == n
+            np.testing.assert_array_equal(got.counts, c)
+            np.testing.assert_array_equal(got.joints, j)
+            np.testing.assert_array_equal(got.regs, r)
+            kind = t.last_timing()["merge"]
+            if fused == "0":
+                assert kind == 1
+            else:
+                assert kind in (1, 2)
+    finally:
+        t.detach()
+    if fused == "1":
+        import ctypes
+        h = ctypes.CDLL("libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+        if hasattr(h, "ncclDevCommCreate"):             # device API present: the fused kernel ran
+            assert kind == 2
