@@ -1841,7 +1841,9 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     ++t->plan_calls;
     // rows per launch: keep every CTA's u32 bins below 2^31
     // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
-    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19), 1ull << 33);
+    // (sampled launches: <= 2^31 rows, so the compacted row ids fit 32 bits)
+    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19),
+                                                 sample_rate < 1.0 ? (1ull << 31) : (1ull << 33));
     const uint64_t big_launch = t->host ? std::min<uint64_t>(t->nrows, 1ull << 24) : std::min(t->nrows, max_rows);
     void *scan_fn = nullptr;
     int scan_kind = 0;
@@ -1939,6 +1941,8 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
+    // sparse samples: kept rows compacted per warp (gace_probe.cuh s_queue); GACE_COMPACT=0/1 overrides
+    P.compact = getenv("GACE_COMPACT") ? (uint32_t)(atoi(getenv("GACE_COMPACT")) != 0) : (sample_rate < 0.125 ? 1u : 0u);
     if (ab_env) P.dbg = (uint32_t)strtoul(ab_env, nullptr, 0);   // design experiments only
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
 

@@ -260,6 +260,7 @@ struct ProbeParams {
     uint32_t clamp;                        // clamp keys into each slot's [clamp_lo, clamp_hi]
     uint32_t c1, c4, c_hll;                // 1, 4, 2^p: multipliers the compiler cannot see, so that
                                            // u * 4 + base etc. stay IMADs (FMA pipe) instead of LEA/SHF
+    uint32_t compact;                      // sampled launch: queue kept rows per warp (rate < 1/8)
     uint32_t dbg;                          // ablation bits (env GACE_ABLATE; 0 in production):
                                            // 1 no HLL raise, 2 no histogram adds, 4 no grid adds, 8 no HLL
 };

@@ -700,12 +700,10 @@ __device__ __forceinline__ void quad_work(const ProbeParams &P, int4 (&r)[Sh::NC
     pair_work<Sh>(P, keep, bs);
 }
 
-// One row past the last full unit (scalar loads; out of line: cold code).
+// Row r of the launch alone (scalar loads of its keys, replicated over a quad whose rows
+// 1..3 are masked off): the ragged tail, and the compacted rows of a sparse sample.
 template <class Sh>
-__device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
-    const uint32_t keep = (!Sh::SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
-    if (!keep) return 0;
-    int4 rj[Sh::NC][Sh::I64 ? 2 : 1];
+__device__ __forceinline__ void load_row(const ProbeParams &P, uint64_t r, int4 (&rj)[Sh::NC][Sh::I64 ? 2 : 1]) {
 #pragma unroll
     for (int s = 0; s < Sh::NC; ++s) {
         if (!Sh::active(P, s)) continue;
@@ -719,9 +717,26 @@ __device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
             rj[s][Sh::I64 ? 1 : 0] = make_int4(lo, hi, lo, hi);
         }
     }
+}
+
+// One row past the last full unit (out of line: cold code).
+template <class Sh>
+__device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
+    const uint32_t keep = (!Sh::SAMPLE || keep_row(P, P.row0 + r)) ? 1u : 0u;
+    if (!keep) return 0;
+    int4 rj[Sh::NC][Sh::I64 ? 2 : 1];
+    load_row<Sh>(P, r, rj);
     quad_work<Sh>(P, rj, 1u, s_wlim[kThreads / 32], 0u);
     return 1;
 }
+
+// Sparse samples (rate < 1/8): each warp hashes the sample bits of its row quads, queues the
+// kept rows' indices in shared memory, and works on them 32 at a time -- every lane one kept
+// row -- instead of running the per-quad work for the few lanes whose quad kept a row (at rate
+// 0.01, 72 % of the warps had a kept row somewhere, so almost every warp paid the whole quad
+// work at 1/32 of its lanes).  Only kept rows' keys are read.
+constexpr uint32_t kQueue = 64;                       // entries per warp (ring)
+__shared__ uint32_t s_queue[kThreads / 32][kQueue];
 
 template <class Sh>
 __device__ __forceinline__ void probe_body(const ProbeParams &P) {
@@ -791,13 +806,65 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     // sample bits of a row quad (all four rows when the probe is not sampled)
     auto quad_keep = [&](uint32_t uu) -> uint32_t {
         if (!Sh::SAMPLE) return 0xFu;
-        const uint64_t g0 = P.row0 + (uint64_t)uu * 4;
+        // SplitMix64 states of consecutive rows differ by gamma: one 64-bit multiply per quad
+        uint64_t z = P.seed + (P.row0 + (uint64_t)uu * 4 + 1) * GACE_GAMMA;
         uint32_t kk = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) kk |= (keep_row(P, g0 + k) ? 1u : 0u) << k;
+        for (int k = 0; k < 4; ++k, z += GACE_GAMMA) kk |= (mix64(z) < P.thr ? 1u : 0u) << k;
         return kk;
     };
-    if (U == 1 && NC <= 4) {
+    if (Sh::SAMPLE && P.compact) {
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t *q = s_queue[threadIdx.x >> 5];
+        uint32_t qh = 0, qt = 0;                       // ring head / tail (warp-uniform)
+        // kept rows of the queue head, one per lane (all 32 lanes, or the last partial batch)
+        auto work = [&](uint32_t nb) {
+            if (lane < nb) {
+                int4 rj[NC][Sh::I64 ? 2 : 1];
+                load_row<Sh>(P, q[(qh + lane) % kQueue], rj);
+                quad_work<Sh>(P, rj, 1u, wlim, bmfull);
+            }
+            qh += nb;
+            __syncwarp();
+        };
+        // row quads below the tail (nunits units of U quads); warp-uniform trip count: every
+        // lane iterates until the warp's first quad is past the end (lanes past it hash nothing)
+        const uint32_t nq = nunits * U;
+        for (uint32_t ub = u - lane; ub < nq; ub += stride) {
+            const uint32_t uu = ub + lane;
+            if (it == next_refresh) {
+                next_refresh = it + min(it, 32u);
+#pragma unroll
+                for (int s = 0; s < NC; ++s)
+                    if (Sh::active(P, s) && Sh::hll(P, s) && !Sh::hllbm(P, s) && !((bmfull >> s) & 1u)) {
+                        const uint32_t hc = P.slot[s].hceil_off;
+                        const uint32_t hb = hll_bound(Sh::hllw(P, s), P.g_hll_glob + Sh::hllout(P, s) * kHllM, s,
+                                                      hc != kNone ? P.g_hceil + hc : nullptr);
+                        const uint32_t L = min(hb & 255u, 31u);
+                        if (lane == 0) wlim[s] = (0xFFFFFFFFu >> L) & 0xFFFFFFFEu;
+                        if (hb >> 8) bmfull |= 1u << s;
+                    } else if (Sh::active(P, s) && Sh::hll(P, s) && Sh::hllbm(P, s) && !((bmfull >> s) & 1u) &&
+                               P.slot[s].bm_words <= kBmRefreshWords &&
+                               bm_push(smem32() + Sh::bmaddr(P, s) / 4, P.g_bm + P.slot[s].bm_goff,
+                                       P.slot[s].bm_words, P.g_bmcnt + s, Sh::bmnv(P, s)))
+                        bmfull |= 1u << s;
+                __syncwarp();
+            }
+            ++it;
+            const uint32_t keep = uu < nq ? quad_keep(uu) : 0u;
+            kept += __popc(keep);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {              // row k of every lane's quad: <= 32 new entries
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, (keep >> k) & 1u);
+                if (!b) continue;
+                if ((b >> lane) & 1u) q[(qt + __popc(b & ((1u << lane) - 1u))) % kQueue] = uu * 4 + k;
+                qt += __popc(b);
+                __syncwarp();
+                if (qt - qh >= 32) work(32);
+            }
+        }
+        if (qt != qh) work(qt - qh);                  // the last partial batch
+    } else if (U == 1 && NC <= 4) {
         // column-streamed loop; a sampled probe loads only quads with a kept row (at rate
         // 0.01 that is 4 % of the quads, so most key bytes are never read)
         int4 r[NC][Sh::I64 ? 2 : 1];

@@ -502,3 +502,18 @@ def test_hll_ranks_above_16(G, oracle, monkeypatch, jit):
         for rate in (1.0, 0.6):
             _check(G, oracle, [a, b], preds, pairs, rate, 13, [0, 1])
             _check(G, oracle, [a], preds[preds["col"] == 0], None, rate, 13, [0])
+
+
+@pytest.mark.parametrize("compact", ["0", "1"])
+@pytest.mark.parametrize("jit", ["0", "1"])
+@pytest.mark.parametrize("name,nrows,rate", [("C5", 300_001, 0.01), ("C1", 200_003, 0.3), ("C5_i64", 150_007, 0.05),
+                                             ("C4", 200_001, 0.002), ("C3", 250_002, 0.1)])
+def test_sample_compaction(G, oracle, monkeypatch, compact, jit, name, nrows, rate):
+    """Sampled probes with the kept rows compacted per warp (GACE_COMPACT=1: rows queued in
+    shared memory, worked on 32 at a time) and without (per-quad work), on generic and
+    specialised kernels, at rates either side of the 1/8 default switch."""
+    monkeypatch.setenv("GACE_COMPACT", compact)
+    monkeypatch.setenv("GACE_JIT", jit)
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, 31, w.hll_cols)
