@@ -80,3 +80,74 @@ def test_shard_ranges_cover():
             assert rs[0][0] == 0 and rs[-1][1] == N
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(e - s for s, e in rs) - min(e - s for s, e in rs) <= 1
+
+
+def _plan_worker(rank, world, port, q):
+    """Each rank plans the same batch for its own shard of C5 through the product's planner
+    (host-only hook gace_debug_jit_source: the specialised kernel's layout-keyed source, i.e.
+    every table offset, shift and constant of the plan), once over its shard's own value
+    domains and once over the domains all-reduced (min / max) across the ranks -- what
+    gace_table_attach does over NCCL for a multi-rank table -- and gets the NCCL unique id
+    through the product's dist_info (rank 0 creates it, the process group broadcasts it)."""
+    import ctypes
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_2512_19750_b200 import dist as gdist
+        from paper_2512_19750_b200 import gace
+        L = gace.lib()
+        vp, u32, u64, i32, dbl = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+        L.gace_debug_jit_source.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, dbl, i32, vp, u64,
+                                            ctypes.POINTER(u64)]
+        w = synth.get("C5", 40_000)
+        r0, r1 = gdist.shard_range(rank, world, w.nrows)
+        t = [x.numpy() for x in w.table(r0, r1)]
+        lo = torch.tensor([int(x.min()) for x in t], dtype=torch.int64)
+        hi = torch.tensor([int(x.max()) for x in t], dtype=torch.int64)
+
+        def src(dlo, dhi):
+            dt = np.zeros(len(t), dtype=np.int32)
+            dl = np.ascontiguousarray(dlo.numpy(), dtype=np.int64)
+            dh = np.ascontiguousarray(dhi.numpy(), dtype=np.int64)
+            P = gace.as_preds(w.preds)
+            Q = gace.as_pairs(w.pairs)
+            buf = ctypes.create_string_buffer(1 << 17)
+            n = ctypes.c_uint64()
+            rc = L.gace_debug_jit_source(len(t), dt.ctypes.data, dl.ctypes.data, dh.ctypes.data, 0, P.ctypes.data,
+                                         len(P), Q.ctypes.data, len(Q), w.hll_mask, 1.0, 1, buf, 1 << 17,
+                                         ctypes.byref(n))
+            assert rc == 0
+            return buf.value.decode()
+
+        own = src(lo, hi)
+        glo, ghi = lo.clone(), hi.clone()
+        dist.all_reduce(glo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(ghi, op=dist.ReduceOp.MAX)
+        agreed = src(glo, ghi)
+        info = gdist.dist_info(w.nrows)
+        out = [None] * world
+        dist.all_gather_object(out, (own, agreed, info.unique_id, info.row_offset, info.nranks))
+        if rank == 0:
+            whole = [x.numpy() for x in w.table()]
+            q.put((out, src(torch.tensor([int(x.min()) for x in whole]), torch.tensor([int(x.max()) for x in whole]))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_plans_agree():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out, whole = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (own0, agreed0, uid0, off0, n0), (own1, agreed1, uid1, off1, n1) = out
+    assert own0 != own1                    # shard-local domains: the ranks would plan differently
+    assert agreed0 == agreed1 == whole     # agreed domains: identical plans, the whole table's plan
+    assert uid0 == uid1 and len(uid0) == 128 and n0 == n1 == 2
+    assert (off0, off1) == (0, 20_000)
