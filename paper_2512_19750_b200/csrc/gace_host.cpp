@@ -518,7 +518,7 @@ struct Plan {
     ProbeParams P{};
 };
 
-constexpr size_t kSmemBudget = kMaxSmem - 2048;   // keep 2 KB for static shared memory
+constexpr size_t kSmemBudget = kMaxSmem - kStaticSmem;   // gace_plan.h kStaticSmem
 
 // Plan summary on stderr (env GACE_PLAN_DUMP; design inspection only).
 void dump_plan(const Plan &pl) {

@@ -291,7 +291,7 @@ static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lock(mu);
         if (dev >= 64 || !((configured >> dev) & 1ull)) {
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 2048);
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - kStaticSmem);
             if (e != cudaSuccess) return e;
             if (dev < 64) configured |= 1ull << dev;
         }

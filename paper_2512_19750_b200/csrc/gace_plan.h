@@ -36,6 +36,9 @@ constexpr int kMaxGroups = 28;         // unordered slot pairs
 constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
 constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM, <= 64 registers)
+// static shared memory of the probe kernels (skip-bound slices and limits, the sparse-sample
+// row queues: gace_probe.cuh); the plan's dynamic shared memory gets the rest of the 227 KB
+constexpr int kStaticSmem = 12 * 1024;
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
 constexpr uint32_t kSpecial = 0x80000000u;  // entry is a nested block or a list
 constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list

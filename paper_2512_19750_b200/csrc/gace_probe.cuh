@@ -737,6 +737,8 @@ __device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
 // work at 1/32 of its lanes).  Only kept rows' keys are read.
 constexpr uint32_t kQueue = 64;                       // entries per warp (ring)
 __shared__ uint32_t s_queue[kThreads / 32][kQueue];
+static_assert(sizeof(uint32_t) * (kThreads / 32) * kQueue + 2 * kMaxSlots * (kThreads / 32) +
+                  4 * (kThreads / 32 + 1) * kMaxSlots <= kStaticSmem, "static shared memory over kStaticSmem");
 
 template <class Sh>
 __device__ __forceinline__ void probe_body(const ProbeParams &P) {
