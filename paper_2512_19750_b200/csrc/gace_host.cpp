@@ -827,12 +827,13 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             const int64_t base = (int64_t)((uint64_t)S.dl & ~31ull);
             const uint64_t words = (((uint64_t)S.dh - (uint64_t)base) >> 5) + 1;
             if (words > 32768) continue;                        // <= 128 KB
-            // zeroing and merging the bitmap costs ~words per CTA: worth it when every CTA
-            // scans several rows per bitmap word (C4: 200M rows, 2K words; C3: 100M rows, 32K
-            // words; not C1's 1M rows).  Rows per rank, not this shard's own count, so every
-            // rank of a multi-GPU table makes the same choice (identical plans).
+            // zeroing and merging the bitmap costs ~words per CTA (and the finalize hashes every
+            // present value on one CTA): worth it when every CTA scans many rows per bitmap word
+            // (C4: 200M rows, 2K words; not C1's 1M rows, nor C3's 100M rows over 32K words --
+            // measured there: scan unchanged, finalize +0.15 ms).  Rows per rank, not this
+            // shard's own count, so every rank of a multi-GPU table makes the same choice.
             const uint64_t rows = t->has_dist ? t->dist.nrows_total / (uint64_t)t->dist.nranks : t->nrows;
-            if (rows < 8ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
+            if (rows < 32ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
             const size_t bytes = 4 * words;
             if (bytes > 4ull * kHllM && used + bytes - 4ull * kHllM > kSmemBudget) continue;
             used = used + bytes - 4ull * kHllM;

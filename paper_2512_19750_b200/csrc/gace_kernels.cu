@@ -292,7 +292,10 @@ static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
         std::lock_guard<std::mutex> lock(mu);
         if (dev >= 64 || !((configured >> dev) & 1ull)) {
             e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - kStaticSmem);
-            if (e != cudaSuccess) return e;
+            if (e != cudaSuccess) {
+                (void)cudaGetLastError();    // reported here; must not surface at the next launch
+                return e;
+            }
             if (dev < 64) configured |= 1ull << dev;
         }
     }

@@ -27,6 +27,12 @@
 #ifndef GACE_L2_PREFETCH
 #define GACE_L2_PREFETCH 1
 #endif
+// GACE_CHECK=1 (specialised kernels: GACE_JIT_DEFS=GACE_CHECK=1): every shared-memory access
+// through the helpers below is bounds-checked against the launch's dynamic shared memory and
+// traps when outside it -- our own memcheck, since compute-sanitizer is closed on the B200 pool.
+#ifndef GACE_CHECK
+#define GACE_CHECK 0
+#endif
 
 namespace gace {
 
@@ -62,11 +68,20 @@ __device__ __forceinline__ int4 ld_stream(const void *p) {
 
 extern __shared__ uint4 g_smem[];
 
+__device__ __forceinline__ void smem_check(uint32_t off, uint32_t bytes) {
+    if (GACE_CHECK) {
+        uint32_t dyn;
+        asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        if (off > dyn || bytes > dyn - off) __trap();
+    }
+}
+
 __device__ __forceinline__ uint32_t *smem32() { return reinterpret_cast<uint32_t *>(g_smem); }
 
 // u32 in shared memory at byte address a (bucket counters, maps and grids are addressed
 // in bytes so the hot loop never scales an index).
 __device__ __forceinline__ uint32_t *at(uint32_t a) {
+    smem_check(a, 4);
     return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(g_smem) + a);
 }
 
@@ -77,16 +92,19 @@ __device__ __forceinline__ uint32_t *at(uint32_t a) {
 // uniform register instead of re-deriving it from SR_CgaCtaId at every use; C5 scan -3 %)
 __device__ __forceinline__ uint32_t sbase() { uint32_t v; asm("mov.u32 %0, _ZN4gace6g_smemE;" : "=r"(v)); return v; }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t off) {
+    smem_check(off, 4);
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase() + off));
     return v;
 }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t off) {
+    smem_check(off, 2);
     unsigned short v;
     asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(sbase() + off));
     return v;
 }
 __device__ __forceinline__ void red_add1(uint32_t off) {
+    smem_check(off, 4);
     asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(sbase() + off) : "memory");
 }
 
@@ -96,6 +114,7 @@ __device__ __forceinline__ uint32_t saddr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void red_max_if(bool pred, const uint32_t *addr, uint32_t v) {
+    if (pred) smem_check(saddr(addr) - sbase(), 4);
     asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.max.u32 [%1], %2;\n}"
                  :: "r"((uint32_t)pred), "r"(saddr(addr)), "r"(v) : "memory");
 }
@@ -194,9 +213,12 @@ __device__ __noinline__ uint32_t search_bucket(const int64_t *bps, uint32_t n, i
 }
 
 struct SmemTables {
-    __device__ __forceinline__ uint4 u4(uint32_t i) const { return g_smem[i]; }
-    __device__ __forceinline__ uint32_t u32(uint32_t i) const { return smem32()[i]; }
-    __device__ __forceinline__ uint32_t u16(uint32_t i) const { return reinterpret_cast<const uint16_t *>(g_smem)[i]; }
+    __device__ __forceinline__ uint4 u4(uint32_t i) const { smem_check(16 * i, 16); return g_smem[i]; }
+    __device__ __forceinline__ uint32_t u32(uint32_t i) const { smem_check(4 * i, 4); return smem32()[i]; }
+    __device__ __forceinline__ uint32_t u16(uint32_t i) const {
+        smem_check(2 * i, 2);
+        return reinterpret_cast<const uint16_t *>(g_smem)[i];
+    }
 };
 
 // Full walk through nested cells and lists (out of line: rare special entries only).
@@ -351,6 +373,7 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
 // thresholds), or the full walk for nested / list records (sub-bucket via the map).
 template <class Sh>
 __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s, uint32_t rec, uint32_t u) {
+    smem_check(16 * rec, 16);
     const uint4 r = g_smem[rec];
     if (!(r.x & kSpecial)) {
         const uint32_t c1 = u > r.y, c2 = u > r.z, c3 = u > r.w;
@@ -432,6 +455,7 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
             for (int k = 0; k < 4; ++k) {
                 if (k >= nk || !(e[k] & sp)) continue;
                 if (Sh::fold(P, s)) u[k] = offset_of<Sh>(P, s, v[k]);
+                smem_check(16 * (e[k] & Sh::t1dmask(P, s)), 16);
                 const uint4 r = g_smem[e[k] & Sh::t1dmask(P, s)];
                 if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
                     const uint32_t c1 = u[k] > r.y, c2 = u[k] > r.z, c3 = u[k] > r.w;

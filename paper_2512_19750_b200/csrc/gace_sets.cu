@@ -288,7 +288,10 @@ template <int W, int NCM, bool EXACT, bool I64, bool SAMPLE>
 cudaError_t launch_t(const SetsParams &P, int grid, size_t smem, cudaStream_t s) {
     auto k = P.fold ? sets_kernel<W, NCM, EXACT, I64, SAMPLE, W == 1> : sets_kernel<W, NCM, EXACT, I64, SAMPLE, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();        // reported here; must not surface at the next launch
+        return e;
+    }
     k<<<grid, kSetsThreads, smem, s>>>(P);
     return cudaGetLastError();
 }
