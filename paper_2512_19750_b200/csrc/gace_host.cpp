@@ -320,8 +320,18 @@ void add_breakpoints(const Interval &I, int64_t dl, int64_t dh, std::vector<int6
     if (I.hi < dh) T.push_back(I.hi + 1);
 }
 
+// #{t in T : t <= x} over sorted T -- branch-free halving (the planner calls it per predicate
+// bound and per bucket: branchy searches mispredicted at ~100 ns per call on C3's 1024 binds)
 uint32_t count_le(const std::vector<int64_t> &T, int64_t x) {
-    return (uint32_t)(std::upper_bound(T.begin(), T.end(), x) - T.begin());
+    const int64_t *base = T.data();
+    size_t len = T.size();
+    if (!len) return 0;
+    while (len > 1) {
+        const size_t half = len >> 1;
+        base = base[half - 1] <= x ? base + half : base;
+        len -= half;
+    }
+    return (uint32_t)(base - T.data()) + (*base <= x ? 1u : 0u);
 }
 
 struct SlotPlan {
@@ -549,8 +559,20 @@ bool slot_foldable(const SlotParams &Q) {
     return Q.fmt == FMT1T && Q.s1 >= 1 && ((uint64_t)Q.base & ((1ull << Q.s1) - 1)) == 0 && Q.base >= 0;
 }
 
+// sparse = the probe's sample rate is below 1/8: only the few kept rows are looked up, so the
+// level-1 tables are planned ~8x coarser (the lookup resolution barely matters there, while a
+// new batch's planning, plan upload and per-CTA table load all scale with the table size)
 gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
-                      uint32_t nq, uint64_t hll_mask, Plan &pl) {
+                      uint32_t nq, uint64_t hll_mask, Plan &pl, bool sparse = false) {
+    // design inspection: GACE_PLAN_PROFILE=1 prints the planner's phase times (stderr)
+    static const bool prof = getenv("GACE_PLAN_PROFILE") != nullptr;
+    auto tp0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char *name) {
+        if (!prof) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "plan %-12s %8.1f us\n", name, std::chrono::duration<double, std::micro>(now - tp0).count());
+        tp0 = std::chrono::steady_clock::now();     // (the print is not part of the next phase)
+    };
     // ---- slots: probed columns in ascending order
     std::vector<bool> probed(t->ncols, false);
     for (uint32_t p = 0; p < np; ++p) probed[preds[p].col] = true;
@@ -586,6 +608,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         S.T.erase(std::unique(S.T.begin(), S.T.end()), S.T.end());
         S.nb = (uint32_t)S.T.size() + 1;
     }
+    phase("intervals");
     // ---- cross-column pairs -> groups (one per unordered column pair)
     for (uint32_t q = 0; q < nq; ++q) {
         const int si = pl.pslot[pairs[q].i], sj = pl.pslot[pairs[q].j];
@@ -634,7 +657,9 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             return sc;
         };
         uint32_t best_mask = 0;
-        if (G_ <= 12) {
+        if (const char *om = getenv("GACE_ORIENT_MASK")) {        // design experiments: force one
+            best_mask = (uint32_t)strtoul(om, nullptr, 0);
+        } else if (G_ <= 12) {
             int best = -1;
             for (uint32_t m = 0; m < (1u << G_); ++m) {
                 const int sc = score_of(m, (int)G_);
@@ -657,6 +682,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             G.nbs = ((uint32_t)G.TB.size() + 1) | 1u;
         }
     }
+    phase("groups");
     // ---- budget: grids (+ the B side's bucket -> sub-bucket map) in increasing size while
     // they fit with 4 KB per predicate column kept for its lookup table; the rest per row
     size_t fixed = 256;
@@ -699,6 +725,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         }
     }
 
+    phase("budget");
     // ---- lookup tables within the remaining budget
     const size_t lut_budget = kSmemBudget - fixed;
     for (auto &S : pl.slots) {
@@ -758,7 +785,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         uint32_t t1s = 0;                    // FMT1T level-1 shift: ~128 cells per breakpoint, <= 32K cells
         {
             uint64_t target = 64;
-            while (target < 32768 && target < 128ull * S.T.size()) target <<= 1;
+            while (target < (sparse ? 4096u : 32768u) && target < (sparse ? 16ull : 128ull) * S.T.size()) target <<= 1;
             while (t1s < 31 && (span >> t1s) + 1 > target) ++t1s;
             t1s = std::max<uint32_t>(t1s, 1);
             const uint32_t mx = t1_max_s1(S, nsub_of(S));     // finer than the target when the fields force it
@@ -778,7 +805,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             S.fmt = narrow ? FMT16 : FMT32;
             const uint64_t cap = S.fmt == FMT16 ? 16384 : 8192;
             uint64_t target = 64;
-            while (target < cap && target < 32ull * S.T.size()) target <<= 1;
+            while (target < (sparse ? cap / 8 : cap) && target < (sparse ? 4ull : 32ull) * S.T.size()) target <<= 1;
             uint32_t sh = 0;
             while (sh < 31 && (span >> sh) + 1 > target) ++sh;
             s1[i] = sh;
@@ -813,6 +840,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (!build_lut(S, span_of(S), s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
     }
 
+    phase("luts");
     // ---- HLL mode per column: a presence bitmap (one bit per value of a small int32 domain;
     // the finalize hashes each present value once) instead of hashing every key, when it
     // fits where the u32 registers were budgeted (exact: registers depend only on the set
@@ -843,6 +871,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         }
     }
 
+    phase("hll");
     // ---- layout: image [per slot: L1 | nested | lists][maps] | acc [own hists][grids][direct] |
     //      presence bitmaps | hll registers
     uint32_t w = 0;    // u32 cursor
@@ -903,6 +932,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     if (pl.smem_bytes > kSmemBudget)
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
 
+    phase("layout");
     // ---- fill the image (absolute shared-memory indices)
     pl.image.assign((size_t)image_words * 4, 0);
     uint4 *img4 = reinterpret_cast<uint4 *>(pl.image.data());
@@ -944,6 +974,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         for (uint32_t r = 0; r < B.nb; ++r) img32[G.map_w + r] = r == 0 ? 0 : count_le(G.TB, B.T[r - 1]);
     }
 
+    phase("image");
     // ---- finalize plan
     uint32_t pre = 0;
     for (auto &S : pl.slots) {
@@ -972,16 +1003,56 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         hi = count_le(T, pl.iv[p].hi);
     };
     auto negated = [&](uint32_t p) -> uint32_t { return (preds[p].flags & GACE_PRED_NEGATE) ? 1 : 0; };
+    // bucket intervals of the predicates on their own columns: every clipped interval end is a
+    // breakpoint of the column (lo, or hi + 1), so its bucket is that breakpoint's position --
+    // found in an open-addressing index of each column's breakpoints (O(1), not a search)
+    struct BpIndex {
+        std::vector<int64_t> key;
+        std::vector<uint32_t> pos;
+        uint64_t mask = 0;
+        void build(const std::vector<int64_t> &T) {
+            size_t cap = 16;
+            while (cap < 2 * T.size()) cap <<= 1;
+            key.assign(cap, 0);
+            pos.assign(cap, kNone);
+            mask = cap - 1;
+            for (size_t i = 0; i < T.size(); ++i) {
+                uint64_t h = ((uint64_t)T[i] * 0x9E3779B97F4A7C15ull) >> 20;
+                while (pos[h & mask] != kNone) ++h;
+                key[h & mask] = T[i];
+                pos[h & mask] = (uint32_t)i;
+            }
+        }
+        uint32_t find(int64_t x) const {            // index of x in T, or kNone
+            for (uint64_t h = ((uint64_t)x * 0x9E3779B97F4A7C15ull) >> 20;; ++h) {
+                if (pos[h & mask] == kNone) return kNone;
+                if (key[h & mask] == x) return pos[h & mask];
+            }
+        }
+    };
+    std::vector<BpIndex> bpx(pl.slots.size());
+    for (size_t i = 0; i < pl.slots.size(); ++i) bpx[i].build(pl.slots[i].T);
+    auto bucket_iv_fast = [&](uint32_t p, int sl, uint32_t &lo, uint32_t &hi) {
+        const Interval &I = pl.iv[p];
+        const SlotPlan &S = pl.slots[sl];
+        if (I.empty) { lo = 1; hi = 0; return; }
+        const uint32_t a = I.lo > S.dl ? bpx[sl].find(I.lo) : kNone;
+        const uint32_t b = I.hi < S.dh ? bpx[sl].find(I.hi + 1) : kNone;
+        lo = I.lo > S.dl ? (a != kNone ? a + 1 : count_le(S.T, I.lo)) : 0u;
+        hi = I.hi < S.dh ? (b != kNone ? b : count_le(S.T, I.hi)) : (uint32_t)S.T.size();
+    };
+    phase("fin-jobs");
     pl.fpreds.resize(np);
     for (uint32_t p = 0; p < np; ++p) {
         const SlotPlan &S = pl.slots[pl.pslot[p]];
         FinPred F{};
         F.pre = S.pre;
         F.stride = S.pre_stride;
-        bucket_iv(p, S.T, F.lo, F.hi);
+        bucket_iv_fast(p, pl.pslot[p], F.lo, F.hi);
         F.neg = negated(p);
         pl.fpreds[p] = F;
     }
+    phase("fin-preds");
     pl.fpairs.resize(nq);
     struct DEnt { uint32_t g, q; DirectPair D; };
     std::vector<DEnt> dlist;
@@ -1037,6 +1108,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         pl.direct.push_back(E.D);
     }
 
+    phase("finalize");
     // ---- kernel parameters (pointers filled in at launch)
     ProbeParams &P = pl.P;
     memset(&P, 0, sizeof(P));
@@ -1133,6 +1205,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     P.hll_off = pl.hll_off;
     P.hll_bytes = pl.hll_bytes;
     P.smem_bytes = pl.smem_bytes;
+    phase("params");
     if (getenv("GACE_PLAN_DUMP")) dump_plan(pl);
     return GACE_OK;
 }
@@ -1754,14 +1827,16 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     }
     t->dirty = true;                                             // (a completed call synchronised)
     t->timing_kind = 0;
+    const bool sparse_plan = sample_rate < 0.125;          // make_plan's sparse hint (part of the key)
     std::string key;
-    key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 8);
+    key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 9);
+    key.push_back(sparse_plan ? 's' : 'd');
     key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
     if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
     if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
     if (!t->plan || key != t->plan_key) {
         auto fresh = std::make_shared<Plan>();
-        st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh), key);
+        st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh, sparse_plan), key);
         if (st) return st;
         const Plan &q = *fresh;
         // the cached plan is replaced below: until then (and on any failure) no plan is
