@@ -444,6 +444,16 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     const uint64_t csize = 1ull << s1;
     S.l1.reserve(ncells);
     Sweep at_lo{toff}, at_hi{toff};
+    // a record of <= 3 breakpoints (the common boundary cell), from the sweep's own indices:
+    // node()'s first case without its searches
+    auto direct = [&](uint32_t b0, uint32_t cnt) -> uint4 {
+        uint32_t t[3] = {kNoThr, kNoThr, kNoThr}, flags = 0;
+        for (uint32_t i = 0; i < cnt; ++i) {
+            t[i] = (uint32_t)(toff[b0 + i] - 1);                   // u > t  <=>  u >= breakpoint
+            if (cuts(b0 + i)) flags |= 1u << (kIncShift + i);
+        }
+        return make_uint4(b0 | (sub_of(b0) << kSubShift) | flags, t[0], t[1], t[2]);
+    };
     if (S.fmt == FMT1T) {      // one in-cell threshold per cell (gace_plan.h FMT1T)
         auto bs = [&](uint32_t b) { return (b + 1) | (sub_of(b) << S.sb); };
         for (uint64_t k = 0; k < ncells && ok; ++k) {
@@ -455,7 +465,7 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
                 const uint32_t t = (uint32_t)(toff[b0] - lo);      // in [1, 2^s1)
                 S.l1.push_back((t << (32 - s1)) | (cuts(b0) ? 1u << (30 - s1) : 0u) | bs(b0));
             } else {
-                const uint4 e = node(lo, hi, s1);
+                const uint4 e = cnt <= 3 ? direct(b0, cnt) : node(lo, hi, s1);
                 S.l1.push_back(t1_special(s1) | (uint32_t)S.l2.size());   // slot-relative record
                 S.l2.push_back(e);
             }
@@ -464,11 +474,11 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     }
     for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
-        const uint32_t b0 = at_lo(lo);
-        if (at_hi(hi) == b0) {                                     // plain cell
+        const uint32_t b0 = at_lo(lo), cnt = at_hi(hi) - b0;
+        if (cnt == 0) {                                            // plain cell
             S.l1.push_back(b0 | (sub_of(b0) << kSubShift));
         } else {                                                   // boundary cell -> record
-            const uint4 e = node(lo, hi, s1);
+            const uint4 e = cnt <= 3 ? direct(b0, cnt) : node(lo, hi, s1);
             S.l1.push_back(kSpecial | (uint32_t)S.l2.size());
             S.l2.push_back(e);
         }
@@ -1876,7 +1886,14 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const Plan &pl = *static_cast<const Plan *>(t->plan.get());
     const size_t o_img = t->o_img, o_dir = t->o_dir, o_job = t->o_job, o_fp = t->o_fp, o_fq = t->o_fq, o_bps = t->o_bps;
 
-    const int grid = t->sms;
+    // persistent grid: one CTA per SM; a small table gets fewer CTAs (GACE_ROWS_PER_CTA: at
+    // least that many rows each), since every CTA pays a fixed cost -- zeroing its shared
+    // accumulators and registers, loading the plan image, flushing its partials
+    int grid = t->sms;
+    if (const char *rp = getenv("GACE_ROWS_PER_CTA")) {
+        const uint64_t per = strtoull(rp, nullptr, 10);
+        if (per && !t->host) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(t->sms, (t->nrows + per - 1) / per));
+    }
     // + merged HLL bound registers + merged presence bitmaps
     // + n_sampled counter at the end, so one memset clears the whole accumulator
     const size_t nsamp_off = align16(8ull * pl.acc_words + 4ull * pl.hll_bytes + 4ull * pl.bm_gwords + 4ull * kMaxSlots + 16);
