@@ -27,6 +27,9 @@
 #ifndef GACE_L2_PREFETCH
 #define GACE_L2_PREFETCH 1
 #endif
+#ifndef GACE_L2_PREFETCH_U           // the same for the multi-quad units of 1-2 column probes
+#define GACE_L2_PREFETCH_U 0
+#endif
 // GACE_CHECK=1 (specialised kernels: GACE_JIT_DEFS=GACE_CHECK=1): every shared-memory access
 // through the helpers below is bounds-checked against the launch's dynamic shared memory and
 // traps when outside it -- our own memcheck, since compute-sanitizer is closed on the B200 pool.
@@ -962,9 +965,20 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         X = Xn;
     }
 #else
-    // no register prefetch: the 24 warps of the SM keep enough loads in flight, and the
-    // registers go to the lookup / hash work instead
+    // no register prefetch: the 32 warps of the SM keep loads in flight, and the registers go
+    // to the lookup / hash work instead; the units two iterations ahead are pulled into L2
     for (; u < nunits; u += stride) {
+#if GACE_L2_PREFETCH_U
+        if (!Sh::SAMPLE && u + 2 * stride < nunits) {
+#pragma unroll
+            for (int s = 0; s < NC; ++s) {
+                if (!Sh::active(P, s)) continue;
+                const char *a = static_cast<const char *>(P.slot[s].ptr) +
+                                (uint64_t)(u + 2 * stride) * U * (Sh::is32(P, s) ? 16u : 32u);
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(a));
+            }
+        }
+#endif
         Unit<Sh> X;
         load_unit<Sh>(P, u, X);
         body(X, u);
