@@ -12,6 +12,7 @@
 // sub-buckets of only the pair-relevant predicates.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>   // environ
 
 #include <algorithm>
 #include <array>
@@ -43,6 +44,31 @@ using namespace gace;
 namespace {
 
 thread_local std::string g_err;
+
+// Design / test switches (GACE_*) read by the probe path: one pass over the environment at the
+// start of each probe call (refresh_knobs) instead of a getenv per switch -- at C1's size ten
+// getenv scans were a visible part of the per-call host time.  Tests change them between calls.
+struct KnobSnap {
+    std::vector<std::pair<std::string, std::string>> kv;
+};
+thread_local KnobSnap g_knobs;
+thread_local bool g_knobs_valid = false;
+void refresh_knobs() {
+    g_knobs.kv.clear();
+    for (char **e = environ; e && *e; ++e) {
+        const char *v = *e;
+        if (v[0] != 'G' || strncmp(v, "GACE_", 5) != 0) continue;
+        const char *eq = strchr(v, '=');
+        if (eq) g_knobs.kv.emplace_back(std::string(v, eq - v), std::string(eq + 1));
+    }
+    g_knobs_valid = true;
+}
+const char *knob(const char *name) {
+    if (!g_knobs_valid) return getenv(name);
+    for (const auto &p : g_knobs.kv)
+        if (p.first == name) return p.second.c_str();
+    return nullptr;
+}
 std::atomic<uint64_t> g_launches{0};
 
 gace_status fail(gace_status s, const std::string &msg) {
@@ -667,7 +693,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             return sc;
         };
         uint32_t best_mask = 0;
-        if (const char *om = getenv("GACE_ORIENT_MASK")) {        // design experiments: force one
+        if (const char *om = knob("GACE_ORIENT_MASK")) {        // design experiments: force one
             best_mask = (uint32_t)strtoul(om, nullptr, 0);
         } else if (G_ <= 12) {
             int best = -1;
@@ -785,7 +811,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     auto nsub_of = [&](const SlotPlan &S) -> uint32_t {
         return S.prim_b < 0 ? 1u : (uint32_t)pl.groups[S.prim_b].TB.size() + 1;
     };
-    const bool use_t1 = !getenv("GACE_NO_T1");      // design A/B switch (GACE_NO_T1=1: older formats)
+    const bool use_t1 = !knob("GACE_NO_T1");      // design A/B switch (GACE_NO_T1=1: older formats)
     for (size_t i = 0; i < pl.slots.size(); ++i) {
         SlotPlan &S = pl.slots[i];
         if (S.mode != MODE_LUT) continue;
@@ -860,7 +886,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         for (auto &S : pl.slots)
             if (S.mode == MODE_LUT) used += lut_bytes(S);
         for (auto &S : pl.slots) {
-            if (!S.has_hll || S.dtype != GACE_I32 || t->host || getenv("GACE_NO_BITMAP")) continue;
+            if (!S.has_hll || S.dtype != GACE_I32 || t->host || knob("GACE_NO_BITMAP")) continue;
             if (S.mode == MODE_LUT && S.fmt == FMTEX && !S.clamp) continue;   // (index, rank) in the cells
             const int64_t base = (int64_t)((uint64_t)S.dl & ~31ull);
             const uint64_t words = (((uint64_t)S.dh - (uint64_t)base) >> 5) + 1;
@@ -871,7 +897,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             // measured there: scan unchanged, finalize +0.15 ms).  Rows per rank, not this
             // shard's own count, so every rank of a multi-GPU table makes the same choice.
             const uint64_t rows = t->has_dist ? t->dist.nrows_total / (uint64_t)t->dist.nranks : t->nrows;
-            if (rows < 32ull * words * (uint64_t)t->sms && !getenv("GACE_FORCE_BITMAP")) continue;
+            if (rows < 32ull * words * (uint64_t)t->sms && !knob("GACE_FORCE_BITMAP")) continue;
             const size_t bytes = 4 * words;
             if (bytes > 4ull * kHllM && used + bytes - 4ull * kHllM > kSmemBudget) continue;
             used = used + bytes - 4ull * kHllM;
@@ -1144,7 +1170,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         // table's d_hceil at byte offset col * 4096)
         Q.hceil_off = kNone;
         if (S.has_hll && !S.bm && !(S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX && !S.clamp) &&
-            (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !getenv("GACE_NO_CEIL"))
+            (uint64_t)S.dh - (uint64_t)S.dl < (1ull << 25) && !t->host && !knob("GACE_NO_CEIL"))
             Q.hceil_off = (uint32_t)S.col * kHllM;
         Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
@@ -1216,7 +1242,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     P.hll_bytes = pl.hll_bytes;
     P.smem_bytes = pl.smem_bytes;
     phase("params");
-    if (getenv("GACE_PLAN_DUMP")) dump_plan(pl);
+    if (knob("GACE_PLAN_DUMP")) dump_plan(pl);
     return GACE_OK;
 }
 
@@ -1229,14 +1255,17 @@ gace_status check_table(const gace_table *t) {
     return GACE_OK;
 }
 
+// per_item = false: the batch is byte-identical to the table's cached (validated) batch, so
+// the per-predicate / per-pair checks are skipped (repeated probes: no O(P) host work)
 gace_status validate_batch(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
-                           uint32_t nq, double rate, uint64_t hll_mask, uint32_t hll_p) {
+                           uint32_t nq, double rate, uint64_t hll_mask, uint32_t hll_p, bool per_item = true) {
     if (np > GACE_MAX_PREDS) return fail(GACE_EINVAL, "npreds > 4096");
     if (nq > GACE_MAX_PAIRS) return fail(GACE_EINVAL, "npairs > 4096");
     if (np && !preds) return fail(GACE_EINVAL, "preds is NULL");
     if (nq && !pairs) return fail(GACE_EINVAL, "pairs is NULL");
     if (!(rate >= 0.0 && rate <= 1.0)) return fail(GACE_EINVAL, "sample_rate must be in [0, 1]");
     if (t->ncols < 64 && (hll_mask >> t->ncols)) return fail(GACE_EINVAL, "hll_col_mask names a column >= ncols");
+    if (!per_item) return hll_p != GACE_HLL_P ? fail(GACE_EUNSUPPORTED, "hll_p must be 12") : GACE_OK;
     for (uint32_t p = 0; p < np; ++p) {
         if (preds[p].col >= t->ncols) return fail(GACE_EINVAL, "predicate column out of range");
         if (preds[p].op > GACE_BETWEEN) return fail(GACE_EINVAL, "unknown predicate op");
@@ -1252,6 +1281,7 @@ uint64_t threshold_of(double rate) { return rate >= 1.0 ? ~0ull : (uint64_t)std:
 
 gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uint32_t ncols, uint64_t nrows,
                           const gace_dist *dist, int device, void *stream, bool host, gace_table **out) {
+    refresh_knobs();
     if (!out) return fail(GACE_EINVAL, "out is NULL");
     if (!ptrs || !dtypes) return fail(GACE_EINVAL, "column pointers / dtypes are NULL");
     if (ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "ncols must be in [1, 64]");
@@ -1387,7 +1417,7 @@ gace_status attach_common(const void *const *ptrs, const gace_dtype *dtypes, uin
             }
             // the fused merge (NCCL device API, NVLink peer loads; gace_merge.cu) when every
             // rank is load/store reachable; else the grouped all-reduce (GACE_NCCL_FUSED=0 forces it)
-            const char *fz = getenv("GACE_NCCL_FUSED");
+            const char *fz = knob("GACE_NCCL_FUSED");
             if (!(fz && !atoi(fz)) && merge_available()) {
                 std::string why;
                 if (!merge_create(t->comm, dist->nranks, kMergeBytes, &t->merge, &why)) t->merge = nullptr;
@@ -1501,7 +1531,7 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
              gchain([&](uint32_t g) { return u32s(f(P.grp[g])); }) + "; }\n";
     };
     {
-        const char *ab = getenv("GACE_ABLATE");          // design experiments: ablations baked in
+        const char *ab = knob("GACE_ABLATE");          // design experiments: ablations baked in
         o += std::string("  __device__ static constexpr uint32_t dbg(const ProbeParams &) { return ") +
              std::to_string(ab ? (uint32_t)strtoul(ab, nullptr, 0) : 0u) + "u; }\n";
     }
@@ -1556,7 +1586,7 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
 // layout-keyed one only (compiled per batch layout); unset / 2: the structure-keyed one at
 // once and the layout-keyed one compiled in the background, used once it is loaded.
 int jit_layout_mode() {
-    const char *e = getenv("GACE_JIT_LAYOUT");
+    const char *e = knob("GACE_JIT_LAYOUT");
     if (!e) return 2;
     const int v = atoi(e);
     return v < 0 || v > 2 ? 2 : v;
@@ -1566,7 +1596,7 @@ bool jit_layout() { return jit_layout_mode() == 1; }
 // Launches of at least this many rows use a specialised kernel (GACE_JIT_MIN_ROWS, default
 // 2^24: below it the generic kernel's extra instructions cost less than a launch).
 uint64_t jit_min_rows() {
-    const char *e = getenv("GACE_JIT_MIN_ROWS");
+    const char *e = knob("GACE_JIT_MIN_ROWS");
     return e ? strtoull(e, nullptr, 10) : (1ull << 24);
 }
 
@@ -1574,7 +1604,7 @@ uint64_t jit_min_rows() {
 // launches of >= 2^24 rows use a specialised kernel if one is compiled, else the generic
 // kernel while the specialised one compiles in the background (no call waits for NVRTC).
 int jit_mode() {
-    const char *e = getenv("GACE_JIT");
+    const char *e = knob("GACE_JIT");
     if (!e) return 2;
     return atoi(e) ? 1 : 0;
 }
@@ -1821,8 +1851,19 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
                        uint64_t *n_sampled, uint64_t *counts, uint64_t *joint_counts, uint8_t *hll_regs) {
     gace_status st = check_table(t);
     if (st) return st;
+    refresh_knobs();
     std::lock_guard<std::mutex> lock(t->mu);
-    st = validate_batch(t, preds, npreds, pairs, npairs, sample_rate, hll_col_mask, hll_p);
+    if (npreds > GACE_MAX_PREDS || npairs > GACE_MAX_PAIRS) return fail(GACE_EINVAL, "npreds / npairs > 4096");
+    if ((npreds && !preds) || (npairs && !pairs)) return fail(GACE_EINVAL, "preds / pairs is NULL");
+    const bool sparse_plan = sample_rate < 0.125;          // make_plan's sparse hint (part of the key)
+    std::string key;
+    key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 9);
+    key.push_back(sparse_plan ? 's' : 'd');
+    key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
+    if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
+    if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
+    const bool cached = t->plan && key == t->plan_key;
+    st = validate_batch(t, preds, npreds, pairs, npairs, sample_rate, hll_col_mask, hll_p, !cached);
     if (st) return st;
     const int nh = popcount64(hll_col_mask);
     if (!n_sampled) return fail(GACE_EINVAL, "n_sampled is NULL");
@@ -1837,14 +1878,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     }
     t->dirty = true;                                             // (a completed call synchronised)
     t->timing_kind = 0;
-    const bool sparse_plan = sample_rate < 0.125;          // make_plan's sparse hint (part of the key)
-    std::string key;
-    key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 9);
-    key.push_back(sparse_plan ? 's' : 'd');
-    key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
-    if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
-    if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
-    if (!t->plan || key != t->plan_key) {
+    if (!cached) {
         auto fresh = std::make_shared<Plan>();
         st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh, sparse_plan), key);
         if (st) return st;
@@ -1890,7 +1924,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // least that many rows each), since every CTA pays a fixed cost -- zeroing its shared
     // accumulators and registers, loading the plan image, flushing its partials
     int grid = t->sms;
-    if (const char *rp = getenv("GACE_ROWS_PER_CTA")) {
+    if (const char *rp = knob("GACE_ROWS_PER_CTA")) {
         const uint64_t per = strtoull(rp, nullptr, 10);
         if (per && !t->host) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(t->sms, (t->nrows + per - 1) / per));
     }
@@ -1903,7 +1937,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     const size_t out_bytes = align16(8 * out_words) + pl.hll_bytes;
     const bool use_graph = t->graphs && !t->host && t->nrows > 0 && t->stream != nullptr && !t->use_nccl;
     // graphs bake in one accumulator buffer and keep the memset; eager calls alternate
-    const bool dbuf = !use_graph && !getenv("GACE_NO_ACC_DBUF");
+    const bool dbuf = !use_graph && !knob("GACE_NO_ACC_DBUF");
     const int ab = dbuf ? t->acc_next : 0, ob = ab ^ 1;
     DevBuf &acc = t->d_accb[ab];
     const bool need_memset = !(dbuf && t->acc_clean[ab] && acc.cap >= acc_bytes);
@@ -1925,7 +1959,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     int jit_used = 0;
     uint64_t bytes_per_row = 0;
     for (auto &S : pl.slots) bytes_per_row += S.dtype == GACE_I32 ? 4 : 8;
-    const char *ab_env = getenv("GACE_ABLATE");
+    const char *ab_env = knob("GACE_ABLATE");
     // ---- scan kernel for this call's large launches (gace_probe.cuh)
     const bool sample = sample_rate < 1.0;
     bool i64 = false;
@@ -2035,7 +2069,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
     // sparse samples: kept rows compacted per warp (gace_probe.cuh s_queue); GACE_COMPACT=0/1 overrides
-    P.compact = getenv("GACE_COMPACT") ? (uint32_t)(atoi(getenv("GACE_COMPACT")) != 0) : (sample_rate < 0.125 ? 1u : 0u);
+    P.compact = knob("GACE_COMPACT") ? (uint32_t)(atoi(knob("GACE_COMPACT")) != 0) : (sample_rate < 0.125 ? 1u : 0u);
     if (ab_env) P.dbg = (uint32_t)strtoul(ab_env, nullptr, 0);   // design experiments only
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
 
@@ -2124,7 +2158,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // one rank: the finalize kernels write the packed result straight into the pinned host
     // buffer (mapped under UVA, same address), so no D2H copy is queued; with several ranks
     // the result stays on the device for the NCCL merge and is copied back after it
-    const bool zero_copy = !t->use_nccl && !getenv("GACE_NO_ZERO_COPY");
+    const bool zero_copy = !t->use_nccl && !knob("GACE_NO_ZERO_COPY");
     // fused merge: the finalize writes into this rank's symmetric window, the merge kernel
     // reads every rank's window into d_out
     size_t win_bytes = 0;
@@ -2227,6 +2261,7 @@ gace_status gace_probe_sets(gace_table *t, const gace_pred *preds, uint32_t npre
                             uint64_t *n_sampled, uint64_t *set_counts) {
     gace_status st = check_table(t);
     if (st) return st;
+    refresh_knobs();
     std::lock_guard<std::mutex> lock(t->mu);
     st = validate_batch(t, preds, npreds, nullptr, 0, sample_rate, 0, GACE_HLL_P);
     if (st) return st;
@@ -2792,6 +2827,7 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
                                           int64_t *bps, uint32_t cap, uint32_t *nbp) {
     if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS || col >= ncols || (n && (!values || !out)))
         return fail(GACE_EINVAL, "bad arguments");
+    refresh_knobs();
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;
@@ -2874,6 +2910,7 @@ extern "C" gace_status gace_debug_jit_source(uint32_t ncols, const gace_dtype *d
                                              uint64_t hll_mask, double sample_rate, int layout, char *out,
                                              uint64_t cap, uint64_t *len) {
     if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "bad arguments");
+    refresh_knobs();
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;
@@ -2906,6 +2943,7 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
                                               uint32_t npreds, const gace_pair *pairs, uint32_t npairs,
                                               uint64_t hll_mask, double sample_rate, uint64_t *cubin_bytes) {
     if (!dtypes || !dlo || !dhi || ncols == 0 || ncols > GACE_MAX_COLS) return fail(GACE_EINVAL, "bad arguments");
+    refresh_knobs();
     gace_table t;
     t.ncols = ncols;
     t.host = host != 0;

@@ -76,6 +76,9 @@ struct MergeParams {
 };
 
 __global__ void __launch_bounds__(1024) fin_merge_lsa(const __grid_constant__ MergeParams M) {
+    // launched with programmatic stream serialisation: the launch overlaps the finalize's
+    // tail, and this waits for it (its window writes complete and visible) before anything
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), M.dc, ncclTeamTagLsa(), blockIdx.x);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);     // every rank's result is in its window
     const int n = M.dc.lsaSize;
@@ -148,8 +151,16 @@ cudaError_t merge_launch(MergeState *m, uint32_t nwords, uint32_t regs_off, uint
     P.regs_off = regs_off;
     P.regs_words = regs_bytes / 4;
     P.out = static_cast<unsigned long long *>(out);
-    fin_merge_lsa<<<1, 1024, 0, s>>>(P);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fin_merge_lsa, P);
 }
 
 }  // namespace gace
