@@ -1969,8 +1969,12 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     // rows per launch: keep every CTA's u32 bins below 2^31
     // (and unit indices within 32 bits: <= 2^31 units of 4..16 rows)
     // (sampled launches: <= 2^31 rows, so the compacted row ids fit 32 bits)
-    const uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19),
-                                                 sample_rate < 1.0 ? (1ull << 31) : (1ull << 33));
+    uint64_t max_rows = std::min<uint64_t>((uint64_t)grid * kThreads * (1ull << 19),
+                                           sample_rate < 1.0 ? (1ull << 31) : (1ull << 33));
+    if (const char *ml = knob("GACE_MAX_LAUNCH_ROWS")) {     // tests: force chunked launches
+        const uint64_t m = strtoull(ml, nullptr, 10) & ~3ull;
+        if (m) max_rows = std::min(max_rows, m);
+    }
     const uint64_t big_launch = t->host ? std::min<uint64_t>(t->nrows, 1ull << 24) : std::min(t->nrows, max_rows);
     void *scan_fn = nullptr;
     int scan_kind = 0;

@@ -517,3 +517,23 @@ def test_sample_compaction(G, oracle, monkeypatch, compact, jit, name, nrows, ra
     w = synth.get(name, nrows)
     cols = [x.numpy() for x in w.table()]
     _check(G, oracle, cols, w.preds, w.pairs, rate, 31, w.hll_cols)
+
+
+@pytest.mark.parametrize("jit", ["0", "1"])
+@pytest.mark.parametrize("name,nrows,rate", [("C5", 1_000_003, 1.0), ("C1", 700_001, 0.3), ("C5_i64", 500_009, 0.05),
+                                             ("C4", 600_001, 1.0)])
+def test_chunked_launches(G, oracle, monkeypatch, jit, name, nrows, rate):
+    """A table scanned in several launches (GACE_MAX_LAUNCH_ROWS forces ~100K-row launches):
+    each launch's own ragged tail, its row offset into the sample, HLL partials max-merged
+    across launches and counters summed across them (the multi-launch path)."""
+    monkeypatch.setenv("GACE_MAX_LAUNCH_ROWS", "100004")
+    monkeypatch.setenv("GACE_JIT", jit)
+    w = synth.get(name, nrows)
+    cols = [x.numpy() for x in w.table()]
+    _check(G, oracle, cols, w.preds, w.pairs, rate, 17, w.hll_cols)
+    t = G.Table([torch.from_numpy(c).cuda() for c in cols])
+    try:
+        t.probe(w.preds, w.pairs, rate, 17, w.hll_cols)
+        assert t.last_timing()["scan_launches"] == (nrows + 100003) // 100004
+    finally:
+        t.detach()
