@@ -71,9 +71,21 @@ typedef struct {
 
 /* Multi-GPU description: rows are sharded contiguously, one
  * process per GPU.  row_offset = global id of this shard's first row (reading
- * L7: the sample bit uses global row ids, so results are shard-invariant).
+ * L7: the sample bit uses global row ids, so results are shard-invariant);
+ * row_offset + nrows_local <= nrows_total (GACE_EINVAL otherwise).
  * Either nccl_unique_id (128 bytes from ncclGetUniqueId on rank 0, broadcast by
- * the caller) or an existing nccl_comm (ncclComm_t, not destroyed by detach).  */
+ * the caller) or an existing nccl_comm (ncclComm_t, not destroyed by detach).
+ * With either, results are merged over NCCL at any nranks (1 included); with
+ * neither (nranks must then be 1) the table is a plain single-GPU table with an
+ * offset.  An NCCL table's attach is collective: the ranks all-reduce their
+ * shards' per-column minima / maxima so every rank plans over the same global
+ * value domains, and -- when the loaded libnccl has the 2.28 device API and every
+ * rank is NVLink load/store reachable -- register a 128 KB symmetric window per
+ * rank for the fused merge (§IV-B "Reduction"; SURVEY.md §8(f) NEXT-2b;
+ * GACE_NCCL_FUSED=0 keeps the grouped all-reduce).  Its detach is collective too.
+ * Waits on an NCCL table poll ncclCommGetAsyncError: an asynchronous error, or no
+ * progress within GACE_NCCL_TIMEOUT_MS (default 300000), aborts the communicator
+ * and returns GACE_ENCCL (the table cannot merge again; detach it).  */
 typedef struct {
     int rank;
     int nranks;
@@ -125,7 +137,8 @@ gace_status gace_table_attach_host(const void *const *col_host_ptrs, const gace_
                                    uint32_t ncols, uint64_t nrows_local, const gace_dist *dist,
                                    int device, void *cuda_stream, gace_table **out);
 
-/* Free everything the library allocated for t (never the borrowed columns). */
+/* Free everything the library allocated for t (never the borrowed columns; never a
+ * caller-passed communicator).  Collective for a table attached with NCCL. */
 gace_status gace_table_detach(gace_table *t);
 
 /*
@@ -157,7 +170,11 @@ gace_status gace_table_graph_stats(const gace_table *t, uint64_t *captures, uint
  *   hll_regs[popcount(mask)][4096] u8 registers, ascending column order; may be NULL
  *                                  iff mask == 0 (sampled rows only, reading L4)
  * Synchronous: returns once the results are in host memory.  One probe in flight per
- * handle.  Collective over ranks when attached with dist (identical arguments).
+ * handle.  Collective over ranks when attached with NCCL (identical arguments): a batch
+ * new to the table is agreed on first (all-reduce of the ranks' planning status and a
+ * hash of the batch), so a batch no rank can plan fails on every rank (its own status),
+ * and ranks passing different batches all get GACE_EINVAL -- none enters a merge the
+ * others would not join.
  */
 gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds,
                        const gace_pair *pairs, uint32_t npairs, double sample_rate,
