@@ -1464,6 +1464,16 @@ namespace {
 
 // Source of `struct JitShape` for gace_probe.cuh: the plan's structural decisions as
 // constexpr answers (predicate values stay in the kernel parameters).
+// Threads per CTA of a plan's specialised kernel (gace_plan.h kThreads): 768 for plans of 6+
+// probed columns (GACE_JIT_THREADS overrides; 1024 / 768 / 512).
+int jit_threads(const Plan &pl) {
+    if (const char *e = knob("GACE_JIT_THREADS")) {
+        const int v = atoi(e);
+        if (v == 1024 || v == 768 || v == 512) return v;
+    }
+    return pl.P.nslots >= 6 ? 768 : 1024;
+}
+
 // layout = false: the structure only (layout read from the parameters, gace_probe.cuh
 // RtLayout), so every batch with this structure shares one compiled kernel; layout = true:
 // offsets, shifts and masks baked in as immediates too (one kernel per batch layout).
@@ -1476,7 +1486,9 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
         for (int i = 0; i < n; ++i) r += "s == " + std::to_string(i) + " ? " + f(i) + " : ";
         return r + "0";
     };
-    std::string o = "namespace gace {\nstruct JitShape : RtLayout {\n";
+    std::string o;
+    if (jit_threads(pl) != 1024) o += "#define GACE_THREADS " + std::to_string(jit_threads(pl)) + "\n";
+    o += "namespace gace {\nstruct JitShape : RtLayout {\n";
     o += "  static constexpr int NC = " + std::to_string(nc) + ";\n";
     o += "  static constexpr bool SAMPLE = " + std::string(sample ? "true" : "false") + ";\n";
     o += "  static constexpr bool I64 = " + std::string(i64 ? "true" : "false") + ";\n";
@@ -2083,7 +2095,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     auto launch_scan = [&](const ProbeParams &PP, uint64_t n) -> cudaError_t {
         if (scan_fn && (jm == 1 || n >= jit_min_rows())) {
             std::string err;
-            if (jit_launch_fn(scan_fn, PP, grid, s, &err)) {
+            if (jit_launch_fn(scan_fn, PP, grid, jit_threads(pl), s, &err)) {
                 jit_used = scan_kind;
                 return cudaSuccess;
             }

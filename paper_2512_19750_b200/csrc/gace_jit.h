@@ -24,7 +24,7 @@ bool jit_launch(const ProbeParams &P, int device, const std::string &shape_src, 
 // of a kernel obtained that way (tables keep the handle of their cached plan, so repeated
 // probes skip regenerating the shape source and the cache lookup).
 bool jit_get(int device, const std::string &shape_src, void **fn, double *compile_ms, std::string *err);
-bool jit_launch_fn(void *fn, const ProbeParams &P, int grid, cudaStream_t s, std::string *err);
+bool jit_launch_fn(void *fn, const ProbeParams &P, int grid, int threads, cudaStream_t s, std::string *err);
 
 // Non-blocking: the cached kernel for (device, shape) if it is compiled.
 bool jit_lookup(int device, const std::string &shape_src, void **fn);

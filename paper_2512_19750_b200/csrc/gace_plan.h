@@ -35,7 +35,13 @@ constexpr int kMaxSlots = 8;           // GACE_MAX_PROBED_COLS
 constexpr int kMaxGroups = 28;         // unordered slot pairs
 constexpr int kHllP = 12;
 constexpr int kHllM = 1 << kHllP;
-constexpr int kThreads = 1024;         // probe CTA size (one CTA per SM, <= 64 registers)
+#ifndef GACE_THREADS
+#define GACE_THREADS 1024
+#endif
+// probe CTA size (one CTA per SM): 1024 threads of <= 64 registers; a specialised kernel of a
+// plan with many columns is compiled with 768 (<= 80 registers: the column-streamed keys of 8
+// columns spilled at 64)
+constexpr int kThreads = GACE_THREADS;
 // static shared memory of the probe kernels (skip-bound slices and limits, the sparse-sample
 // row queues: gace_probe.cuh); the plan's dynamic shared memory gets the rest of the 227 KB
 constexpr int kStaticSmem = 12 * 1024;
