@@ -26,10 +26,18 @@ variants = {
 for k, (P, Q, H, rate) in variants.items():
     for _ in range(2):
         t.probe(P, Q, rate, 1, H)
-    ms = []
+    gace.jit_sync()
+    ms, read = [], 0
     for _ in range(5):
         t.probe(P, Q, rate, 1, H)
-        ms.append(t.last_timing()["scan_ms"])
-    gb = w.nrows * w.bytes_per_row / (np.median(ms) * 1e-3) / 1e9
-    print(f"{name} {k:28s} scan {np.median(ms):8.3f} ms  ({gb:7.1f} GB/s of probed-column bytes)", flush=True)
+        tm = t.last_timing()
+        ms.append(tm["scan_ms"])
+        read = tm["bytes_scanned"]          # the bytes THIS variant's probe reads (its probed columns)
+    if not read:
+        # a batch that probes no column reads nothing: no bandwidth to report (round 1 divided
+        # the full table's bytes by this empty scan and reported an impossible 16 TB/s)
+        print(f"{name} {k:28s} scan {np.median(ms):8.3f} ms  (reads no column)", flush=True)
+        continue
+    gb = read / (np.median(ms) * 1e-3) / 1e9
+    print(f"{name} {k:28s} scan {np.median(ms):8.3f} ms  ({gb:7.1f} GB/s of the bytes it reads)", flush=True)
 t.detach()
