@@ -1464,14 +1464,19 @@ namespace {
 
 // Source of `struct JitShape` for gace_probe.cuh: the plan's structural decisions as
 // constexpr answers (predicate values stay in the kernel parameters).
-// Threads per CTA of a plan's specialised kernel (gace_plan.h kThreads): 768 for plans of 6+
-// probed columns (GACE_JIT_THREADS overrides; 1024 / 768 / 512).
+// Threads per CTA of a plan's specialised kernel (gace_plan.h kThreads): 768 (<= 80 registers)
+// when the column-streamed keys of one row unit need >= 24 registers (4 per int32 column, 8
+// per int64), 1024 (<= 64) otherwise.  Measured (profiles/r02_threads_sweep.txt): C4's 8
+// columns 1.43 -> 1.29 ms, C5_i64 2.88 -> 2.76 ms at 768; C5's 4 int32 columns 2.06 at 1024,
+// 2.16 at 768.  GACE_JIT_THREADS overrides (1024 / 768 / 512).
 int jit_threads(const Plan &pl) {
     if (const char *e = knob("GACE_JIT_THREADS")) {
         const int v = atoi(e);
         if (v == 1024 || v == 768 || v == 512) return v;
     }
-    return pl.P.nslots >= 6 ? 768 : 1024;
+    uint32_t key_regs = 0;
+    for (uint32_t i = 0; i < pl.P.nslots; ++i) key_regs += pl.P.slot[i].dtype ? 8 : 4;
+    return key_regs >= 24 ? 768 : 1024;
 }
 
 // layout = false: the structure only (layout read from the parameters, gace_probe.cuh

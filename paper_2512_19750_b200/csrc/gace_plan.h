@@ -39,8 +39,8 @@ constexpr int kHllM = 1 << kHllP;
 #define GACE_THREADS 1024
 #endif
 // probe CTA size (one CTA per SM): 1024 threads of <= 64 registers; a specialised kernel of a
-// plan with many columns is compiled with 768 (<= 80 registers: the column-streamed keys of 8
-// columns spilled at 64)
+// plan whose row unit holds many key registers is compiled with 768 (<= 80 registers: the
+// column-streamed keys of 8 columns spilled at 64; gace_host.cpp jit_threads)
 constexpr int kThreads = GACE_THREADS;
 // static shared memory of the probe kernels (skip-bound slices and limits, the sparse-sample
 // row queues: gace_probe.cuh); the plan's dynamic shared memory gets the rest of the 227 KB
