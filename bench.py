@@ -71,15 +71,20 @@ def fresh_batch(w, b: int):
     bind centre moves per query): the same predicates and pairs with every bound shifted,
     so each batch is new to the library (new plan, new lookup tables), its structure is
     the template's.  EQ binds move by 37 values per batch (C3's sliding bind window);
-    range bounds by 0.05 % of the column's domain per batch."""
+    range bounds by 0.05 % of the column's domain per batch, wrapping inside the domain."""
     P = w.preds.copy()
     for c, col in enumerate(w.columns):
         m = P["col"] == c
         if not m.any():
             continue
         step = 37 if np.all(P["op"][m] == 0) else max(1, int((col.hi - col.lo) * 5e-4))
-        P["a"][m] += b * step
-        P["b"][m] += b * step
+        # the bind stays inside the column's value domain (wrapping around it), the range keeps
+        # its width: a real sweep moves the bind centre over the data, not off it
+        span = col.hi - col.lo + 1
+        a = P["a"][m]
+        a2 = col.lo + (a - col.lo + b * step) % span
+        P["b"][m] += a2 - a
+        P["a"][m] = a2
     return P
 
 
