@@ -386,6 +386,7 @@ struct SlotPlan {
     uint32_t pre = 0, pre_stride = 1;  // finalize: bucket-count prefix of this column
     // HLL by presence bitmap (gace_plan.h SlotParams::bm_addr)
     bool bm = false;
+    bool fdirect = false;              // exact cells hold the byte address of the own histogram bin
     int64_t bm_base = 0;
     uint32_t bm_words = 0, bm_w = kNone, bm_goff = 0, hll_out = 0;
 };
@@ -969,6 +970,17 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         return fail(GACE_EUNSUPPORTED, "probe plan exceeds one CTA's shared memory");
 
     phase("layout");
+    // exact cells of a clamped column in no pair group (C3's bind span) hold the byte address
+    // of the key's own histogram bin: the kernel adds to it directly (SlotParams::fdirect)
+    {
+        std::vector<uint8_t> in_group(pl.slots.size(), 0);
+        for (auto &G : pl.groups) in_group[G.s0] = in_group[G.s1] = 1;
+        for (size_t i = 0; i < pl.slots.size(); ++i) {
+            SlotPlan &S = pl.slots[i];
+            S.fdirect = S.has_preds && S.mode == MODE_LUT && S.fmt == FMTEX && S.clamp && !in_group[i] &&
+                        S.hist_grp < 0 && S.prim_b < 0 && S.hist_w != kNone && !knob("GACE_NO_FDIRECT");
+        }
+    }
     // ---- fill the image (absolute shared-memory indices)
     pl.image.assign((size_t)image_words * 4, 0);
     uint4 *img4 = reinterpret_cast<uint4 *>(pl.image.data());
@@ -996,7 +1008,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
                     hidx = h >> (32 - kHllP);
                     rank = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
                 }
-                img32[S.lut_idx + k] = idx | (sub << 9) | (hidx << 15) | (rank << 27);
+                img32[S.lut_idx + k] = S.fdirect ? 4 * (S.hist_w + idx) : idx | (sub << 9) | (hidx << 15) | (rank << 27);
             } else {
                 img32[S.lut_idx + k] = (c & kSpecial) ? kSpecial | (S.l2_idx + (c & kRecMask)) : c;
             }
@@ -1174,6 +1186,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             Q.hceil_off = (uint32_t)S.col * kHllM;
         Q.hll_out = S.hll_out;
         Q.hist_addr = S.hist_w == kNone ? kNone : 4 * S.hist_w;
+        Q.fdirect = S.fdirect ? 1 : 0;
         Q.prim_b = (int8_t)S.prim_b;
         Q.base = S.base;
         Q.s1 = S.s1;
@@ -1515,6 +1528,8 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
          chain([&](int i) { return std::to_string((int)P.slot[i].fmt); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool clust(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(clustered[i] ? "1" : "0"); }, nc) + "; }\n";
+    o += "  __device__ static constexpr bool fdirect(const ProbeParams &, int s) { return " +
+         chain([&](int i) { return std::string(P.slot[i].fdirect ? "1" : "0"); }, nc) + "; }\n";
     o += "  __device__ static constexpr bool ownh(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::string(P.slot[i].mode != MODE_NOPRED && P.slot[i].hist_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
     auto gchain = [&](auto f) {
@@ -2889,7 +2904,9 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
         } else if (Q.dtype == GACE_I32) {
             int32_t x = (int32_t)values[k];
             if (pl.clamp) x = std::min(std::max(x, (int32_t)Q.clamp_lo), (int32_t)Q.clamp_hi);
-            if (Q.fmt == FMTEX)                    // the kernel's decode: the cell word's bucket field
+            if (Q.fmt == FMTEX && Q.fdirect)       // the kernel's decode: a bin address -> its bucket
+                b = (M.u32(Q.lut_w + ((uint32_t)x - (uint32_t)Q.base)) - Q.hist_addr) / 4;
+            else if (Q.fmt == FMTEX)               // the kernel's decode: the cell word's bucket field
                 b = M.u32(Q.lut_w + ((uint32_t)x - (uint32_t)Q.base)) & Q.bmask;
             else
                 b = lut_lookup(M, Q.fmt, Q.lut_w, Q.s1, (uint32_t)x - (uint32_t)Q.base, Q.sb);

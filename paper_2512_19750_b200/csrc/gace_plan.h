@@ -190,7 +190,9 @@ struct SlotParams {
     int8_t prim_b;          // group whose sub-bucket this column's entries pack, or -1
     uint8_t fmt;            // LutFmt of the level-1 table
     uint8_t sb;             // sub-bucket shift inside bs (16, or the FMT1T bucket field width)
-    uint8_t pad[2];
+    uint8_t fdirect;        // exact cells holding the byte address of the key's own histogram bin
+                            // (FMTEX, clamped, in no pair group): the bin add needs no arithmetic
+    uint8_t pad;
     uint32_t bmask;         // (1 << sb) - 1: bucket field of bs
     uint32_t submask;       // sub-bucket field of bs >> sb (FMT16/FMTEX: 63, FMT32: 127)
     uint32_t sub_mul;       // 2^(32 - sb): bs >> sb as a high multiply (FMA pipe)

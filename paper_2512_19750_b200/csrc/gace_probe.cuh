@@ -291,6 +291,7 @@ struct RtShape : RtLayout {
     __device__ static bool ownh(const ProbeParams &P, int s) {
         return P.slot[s].mode != MODE_NOPRED && P.slot[s].hist_addr != kNone;
     }
+    __device__ static bool fdirect(const ProbeParams &P, int s) { return P.slot[s].fdirect != 0; }
     __device__ static constexpr bool gpacked(int) { return false; }
     __device__ static constexpr bool clust(const ProbeParams &, int) { return false; }
     __device__ static int fmt(const ProbeParams &P, int s) { return P.slot[s].fmt; }
@@ -559,7 +560,7 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
         const uint32_t h = Sh::histb(P, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if ((keep >> k) & 1u) red_add1(h + 4 * (bs[k] & Sh::bmask(P, s)));
+            if ((keep >> k) & 1u) red_add1(Sh::fdirect(P, s) ? bs[k] : h + 4 * (bs[k] & Sh::bmask(P, s)));
     }
     // HLL: w = (hash << p) | 2^(p-1), rank = clz(w) + 1; rank > lower bound L  <=>  w <= ~0 >> L.
     // Shifts by constants are written as multiplies (IMAD / IMAD.HI run on the FMA pipe,
