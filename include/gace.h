@@ -367,6 +367,12 @@ gace_status gace_last_timing(const gace_table *t, gace_timing *out);
  */
 gace_status gace_jit_sync(double timeout_ms, uint64_t *compiled, uint64_t *failed, uint64_t *pending);
 
+/* Stop the background compile worker (process exit): queued compiles are dropped, one in
+ * progress finishes first; later batches run on the kernels already compiled or the generic
+ * one (no compile is started again).  Idempotent; always GACE_OK.  The Python binding calls
+ * it from its atexit hook, before the interpreter tears down CUDA state the worker uses. */
+gace_status gace_jit_shutdown(void);
+
 /* Rank 0 of a multi-GPU job: fill id[128] with a fresh ncclUniqueId to broadcast to
  * the other ranks (GACE_ENCCL if libnccl.so.2 cannot be loaded). */
 gace_status gace_nccl_unique_id(void *id128);

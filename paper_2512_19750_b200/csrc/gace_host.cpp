@@ -377,6 +377,8 @@ struct SlotPlan {
     std::vector<uint32_t> l1;          // level-1 cells in FMT32 encoding (boundary: slot-relative record index)
     std::vector<uint4> l2;             // records and nested blocks (slot-relative indices)
     std::vector<uint32_t> lst;         // list thresholds (breakpoint offsets)
+    uint64_t n_l1 = 0, n_l2 = 0, n_lst = 0;   // table sizes at s1 (built, or estimated: lut_estimate)
+    bool built = false;                // l1 / l2 / lst hold the table at s1
     // roles in the pair grids
     int hist_grp = -1;                 // group whose grid row sums give this column's histogram
     int prim_b = -1;                   // group whose sub-bucket the entries pack
@@ -431,6 +433,13 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     S.l2.clear();
     S.lst.clear();
     bool ok = true;
+    auto done = [&]() {
+        S.n_l1 = S.l1.size();
+        S.n_l2 = S.l2.size();
+        S.n_lst = S.lst.size();
+        S.built = true;
+        return ok;
+    };
     std::function<uint4(uint64_t, uint64_t, uint32_t)> node = [&](uint64_t lo, uint64_t hi, uint32_t s) -> uint4 {
         const uint32_t b0 = le(lo), b1 = le(hi), cnt = b1 - b0;   // breakpoints in (lo, hi]
         if (cnt <= 3) {
@@ -497,7 +506,7 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
                 S.l2.push_back(e);
             }
         }
-        return ok;
+        return done();
     }
     for (uint64_t k = 0; k < ncells && ok; ++k) {
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
@@ -510,11 +519,45 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
             S.l2.push_back(e);
         }
     }
-    return ok;
+    return done();
 }
 
 size_t lut_bytes(const SlotPlan &S) {
-    return (S.fmt == FMT16 ? 2 : 4) * S.l1.size() + 16 * S.l2.size() + 4 * S.lst.size() + 48;
+    return (S.fmt == FMT16 ? 2 : 4) * S.n_l1 + 16 * S.n_l2 + 4 * S.n_lst + 48;
+}
+
+// The sizes build_lut would produce at level-1 shift s1, without building (the planner sizes
+// candidate resolutions with this and builds each table once): every cell is one level-1
+// entry; a cell holding breakpoints (FMT1T: >= 2) adds one record.  A breakpoint exactly at a
+// cell start bounds that cell and lies inside none.  exact = false when some cell holds more
+// than 3 (nested blocks or lists): then the table has to be built to be sized.
+struct LutEst {
+    uint64_t l1 = 0, l2 = 0;
+    bool exact = false;
+};
+LutEst lut_estimate(const SlotPlan &S, uint64_t span, uint32_t s1) {
+    LutEst E;
+    E.l1 = (span >> s1) + 1;
+    const uint32_t need = S.fmt == FMT1T ? 2u : 1u;
+    const uint64_t m = (1ull << s1) - 1;
+    uint64_t cur = UINT64_MAX;
+    uint32_t cnt = 0;
+    for (int64_t t : S.T) {
+        const uint64_t o = (uint64_t)t - (uint64_t)S.base;
+        if (o > span || (o & m) == 0) continue;
+        const uint64_t k = o >> s1;
+        if (k != cur) {
+            if (cnt > 3) return E;
+            E.l2 += cnt >= need ? 1 : 0;
+            cur = k;
+            cnt = 0;
+        }
+        ++cnt;
+    }
+    if (cnt > 3) return E;
+    E.l2 += cnt >= need ? 1 : 0;
+    E.exact = true;
+    return E;
 }
 
 // FMT1T field budget: bucket + 1 in sb bits, the packed sub-bucket above it, and record
@@ -565,7 +608,9 @@ struct Plan {
     ProbeParams P{};
 };
 
-constexpr size_t kSmemBudget = kMaxSmem - kStaticSmem;   // gace_plan.h kStaticSmem
+// dynamic shared memory a plan may use: the 227 KB less the kernel's static reservation
+// (gace_plan.h static_smem_reserve: a full scan's kernels carry no row queue)
+constexpr size_t smem_budget(bool full) { return (size_t)(kMaxSmem - static_smem_reserve(!full)); }
 
 // Plan summary on stderr (env GACE_PLAN_DUMP; design inspection only).
 void dump_plan(const Plan &pl) {
@@ -600,7 +645,8 @@ bool slot_foldable(const SlotParams &Q) {
 // level-1 tables are planned ~8x coarser (the lookup resolution barely matters there, while a
 // new batch's planning, plan upload and per-CTA table load all scale with the table size)
 gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, const gace_pair *pairs,
-                      uint32_t nq, uint64_t hll_mask, Plan &pl, bool sparse = false) {
+                      uint32_t nq, uint64_t hll_mask, Plan &pl, bool sparse = false, bool full = false) {
+    const size_t kSmemBudget = smem_budget(full);
     // design inspection: GACE_PLAN_PROFILE=1 prints the planner's phase times (stderr)
     static const bool prof = getenv("GACE_PLAN_PROFILE") != nullptr;
     auto tp0 = std::chrono::steady_clock::now();
@@ -805,6 +851,23 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         S.l1.clear();
         S.l2.clear();
         S.lst.clear();
+        S.n_l1 = S.n_l2 = S.n_lst = 0;
+        S.built = false;
+    };
+    // S at level-1 shift s: sized by lut_estimate (built at the end), or built when the
+    // estimate cannot size it; false = the table cannot be built
+    auto size_lut = [&](SlotPlan &S, uint32_t s) -> bool {
+        const LutEst E = lut_estimate(S, span_of(S), s);
+        if (!E.exact || knob("GACE_NO_LUT_ESTIMATE")) return build_lut(S, span_of(S), s);
+        S.s1 = s;
+        S.l1.clear();
+        S.l2.clear();
+        S.lst.clear();
+        S.n_l1 = E.l1;
+        S.n_l2 = E.l2;
+        S.n_lst = 0;
+        S.built = false;
+        return true;
     };
     // level-1 formats: exact cells (one per key value, HLL info folded in) for small int32
     // domains; 16-bit cells when buckets <= 512 and packed sub-buckets <= 64; else 32-bit
@@ -847,8 +910,15 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             while (sh < 31 && (span >> sh) + 1 > target) ++sh;
             s1[i] = sh;
         }
-        if (!build_lut(S, span_of(S), s1[i]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
+        if (!size_lut(S, s1[i]) || (S.fmt == FMT16 && S.n_l2 > kRecMask16)) to_search(S);
     }
+    const std::vector<uint32_t> s1_target = s1;
+    auto lut_total = [&]() {
+        size_t tot = 0;
+        for (auto &S : pl.slots)
+            if (S.mode == MODE_LUT) tot += lut_bytes(S);
+        return tot;
+    };
     for (int iter = 0; iter < 256; ++iter) {
         size_t tot = 0;
         int worst = -1;
@@ -867,14 +937,56 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
             S.fmt = small_subs(S) && S.nb <= 512 ? FMT16 : FMT32;                  // thresholds no longer fit
         // a coarser level 1 roughly halves it; when nested blocks / lists dominate (dense
         // breakpoints) that column falls back to a binary search in global memory
-        if (s1[worst] >= 31 || S.l1.size() <= 64 || 16 * S.l2.size() + 4 * S.lst.size() > 4 * S.l1.size()) {
+        if (s1[worst] >= 31 || S.n_l1 <= 64 || 16 * S.n_l2 + 4 * S.n_lst > 4 * S.n_l1) {
             to_search(S);
             continue;
         }
         ++s1[worst];
         if (S.fmt == FMT1T) t1_rebase(S, s1[worst]);
         else if (!S.clamp && S.mode == MODE_LUT) S.base = S.dl;          // left FMT1T: plain domain cover
-        if (!build_lut(S, span_of(S), s1[worst]) || (S.fmt == FMT16 && S.l2.size() > kRecMask16)) to_search(S);
+        if (!size_lut(S, s1[worst]) || (S.fmt == FMT16 && S.n_l2 > kRecMask16)) to_search(S);
+    }
+    // refine again where the halving steps above left room: the table whose keys most often
+    // land in a boundary cell (a record walk, and for the warp a divergent branch; keys taken
+    // as uniform over the span) first, never finer than its target, same format
+    for (int iter = 0; iter < 64 && !knob("GACE_NO_REFINE"); ++iter) {
+        std::vector<std::pair<double, int>> cand;
+        for (size_t i = 0; i < pl.slots.size(); ++i) {
+            const SlotPlan &S = pl.slots[i];
+            if (S.mode != MODE_LUT || S.fmt == FMTEX || s1[i] <= s1_target[i] || !S.n_l1) continue;
+            // a clustered (sorted) column passes each boundary cell once per run, not per key
+            if ((size_t)S.col < t->clustered.size() && t->clustered[S.col]) continue;
+            // boundary cells (records) per cell
+            if (S.n_l2) cand.push_back({-(double)S.n_l2 / (double)S.n_l1, (int)i});
+        }
+        std::sort(cand.begin(), cand.end());
+        bool done = false;
+        for (auto &c : cand) {
+            const int i = c.second;
+            SlotPlan keep = pl.slots[i];
+            SlotPlan &S = pl.slots[i];
+            --s1[i];
+            if (S.fmt == FMT1T) t1_rebase(S, s1[i]);
+            if (size_lut(S, s1[i]) && !(S.fmt == FMT16 && S.n_l2 > kRecMask16) && S.mode == MODE_LUT &&
+                lut_total() <= lut_budget) {
+                done = true;
+                break;
+            }
+            S = keep;
+            ++s1[i];
+        }
+        if (!done) break;
+    }
+    // the tables sized by estimate: built once, at their final shift
+    for (auto &S : pl.slots) {
+        if (S.mode != MODE_LUT || S.built) continue;
+        const uint64_t n1 = S.n_l1, n2 = S.n_l2;
+        if (!build_lut(S, span_of(S), S.s1) || (S.fmt == FMT16 && S.n_l2 > kRecMask16)) {
+            to_search(S);
+            continue;
+        }
+        if (S.n_l1 != n1 || S.n_l2 != n2 || S.n_lst)
+            return fail(GACE_EUNSUPPORTED, "internal: lookup-table size estimate differs from the built table");
     }
 
     phase("luts");
@@ -1890,9 +2002,10 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     if (npreds > GACE_MAX_PREDS || npairs > GACE_MAX_PAIRS) return fail(GACE_EINVAL, "npreds / npairs > 4096");
     if ((npreds && !preds) || (npairs && !pairs)) return fail(GACE_EINVAL, "preds / pairs is NULL");
     const bool sparse_plan = sample_rate < 0.125;          // make_plan's sparse hint (part of the key)
+    const bool full_plan = sample_rate >= 1.0;             // full scan: the larger smem budget (idem)
     std::string key;
     key.reserve(24 * (size_t)npreds + 8 * (size_t)npairs + 9);
-    key.push_back(sparse_plan ? 's' : 'd');
+    key.push_back(sparse_plan ? 's' : full_plan ? 'f' : 'd');
     key.append(reinterpret_cast<const char *>(&hll_col_mask), 8);
     if (npreds) key.append(reinterpret_cast<const char *>(preds), sizeof(gace_pred) * npreds);
     if (npairs) key.append(reinterpret_cast<const char *>(pairs), sizeof(gace_pair) * npairs);
@@ -1914,7 +2027,7 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     t->timing_kind = 0;
     if (!cached) {
         auto fresh = std::make_shared<Plan>();
-        st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh, sparse_plan), key);
+        st = agree_plan(t, make_plan(t, preds, npreds, pairs, npairs, hll_col_mask, *fresh, sparse_plan, full_plan), key);
         if (st) return st;
         const Plan &q = *fresh;
         // the cached plan is replaced below: until then (and on any failure) no plan is
@@ -2625,6 +2738,11 @@ gace_status gace_jit_sync(double timeout_ms, uint64_t *compiled, uint64_t *faile
     return ok ? GACE_OK : fail(GACE_EUNSUPPORTED, "background kernel compiles still running at the timeout");
 }
 
+gace_status gace_jit_shutdown(void) {
+    jit_bg_shutdown();
+    return GACE_OK;
+}
+
 gace_status gace_last_timing(const gace_table *t, gace_timing *out) {
     gace_status st = check_table(t);
     if (st) return st;
@@ -2878,7 +2996,7 @@ extern "C" gace_status gace_debug_buckets(uint32_t ncols, const gace_dtype *dtyp
     gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, 1.0, hll_mask, GACE_HLL_P);
     if (st) return st;
     Plan pl;
-    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl, false, true);    // the plan a full scan uses
     if (st) return st;
     const int s = pl.col2slot[col];
     if (s < 0 || !pl.slots[s].has_preds) return fail(GACE_EINVAL, "column has no predicates");
@@ -2963,7 +3081,7 @@ extern "C" gace_status gace_debug_jit_source(uint32_t ncols, const gace_dtype *d
     gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, sample_rate, hll_mask, GACE_HLL_P);
     if (st) return st;
     Plan pl;
-    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl, sample_rate < 0.125, sample_rate >= 1.0);   // as gace_probe
     if (st) return st;
     bool i64 = false;
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
@@ -2995,18 +3113,20 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
     }
     gace_status st = validate_batch(&t, preds, npreds, pairs, npairs, sample_rate, hll_mask, GACE_HLL_P);
     if (st) return st;
+    // GACE_DEBUG_CLUSTERED = bit mask of columns taken as clustered (planner and kernel path)
+    const unsigned long clm = getenv("GACE_DEBUG_CLUSTERED") ? strtoul(getenv("GACE_DEBUG_CLUSTERED"), nullptr, 0) : 0ul;
+    t.clustered.assign(ncols, 0);
+    for (uint32_t c = 0; c < ncols; ++c) t.clustered[c] = (clm >> c) & 1ul;
     Plan pl;
-    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl);
+    st = make_plan(&t, preds, npreds, pairs, npairs, hll_mask, pl, sample_rate < 0.125, sample_rate >= 1.0);   // as gace_probe
     if (st) return st;
     if (pl.P.nslots == 0) return fail(GACE_EINVAL, "no probed columns");
     bool i64 = false;
     for (auto &S : pl.slots) i64 |= S.dtype == GACE_I64;
     std::string err;
     size_t n = 0;
-    // GACE_DEBUG_CLUSTERED = bit mask of slots compiled with the clustered-column path
-    const unsigned long clm = getenv("GACE_DEBUG_CLUSTERED") ? strtoul(getenv("GACE_DEBUG_CLUSTERED"), nullptr, 0) : 0ul;
     std::vector<uint8_t> cl(pl.slots.size(), 0);
-    for (size_t i = 0; i < cl.size(); ++i) cl[i] = (clm >> i) & 1ul;
+    for (size_t i = 0; i < cl.size(); ++i) cl[i] = t.clustered[pl.slots[i].col];
     if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64, cl, jit_layout()), &n, &err))
         return fail(GACE_EUNSUPPORTED, err);
     if (cubin_bytes) *cubin_bytes = n;

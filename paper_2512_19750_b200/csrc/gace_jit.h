@@ -33,6 +33,7 @@ bool jit_lookup(int device, const std::string &shape_src, void **fn);
 void jit_prefetch(int device, const std::string &shape_src);
 // Wait until no background compile is queued or running (false on timeout).
 bool jit_bg_wait(double timeout_ms);
+void jit_bg_shutdown();     // stop the worker: queued compiles dropped, one in progress finished
 void jit_bg_stats(uint64_t *done, uint64_t *failed, uint64_t *pending);
 
 // NVRTC compile only (no device needed): the test hook gace_debug_jit_compile.

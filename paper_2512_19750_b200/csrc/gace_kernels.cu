@@ -291,7 +291,13 @@ static cudaError_t launch_t(const ProbeParams &P, int grid, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lock(mu);
         if (dev >= 64 || !((configured >> dev) & 1ull)) {
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - kStaticSmem);
+            // the plan was budgeted with static_smem_reserve(SAMPLE): check the compiled kernel
+            cudaFuncAttributes fa{};
+            e = cudaFuncGetAttributes(&fa, k);
+            if (e == cudaSuccess && fa.sharedSizeBytes > (size_t)static_smem_reserve(SAMPLE)) e = cudaErrorInvalidValue;
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxSmem - static_smem_reserve(SAMPLE));
             if (e != cudaSuccess) {
                 (void)cudaGetLastError();    // reported here; must not surface at the next launch
                 return e;

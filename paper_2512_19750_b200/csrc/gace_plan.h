@@ -43,8 +43,14 @@ constexpr int kHllM = 1 << kHllP;
 // column-streamed keys of 8 columns spilled at 64; gace_host.cpp jit_threads)
 constexpr int kThreads = GACE_THREADS;
 // static shared memory of the probe kernels (skip-bound slices and limits, the sparse-sample
-// row queues: gace_probe.cuh); the plan's dynamic shared memory gets the rest of the 227 KB
+// row queues: gace_probe.cuh); the plan's dynamic shared memory gets the rest of the 227 KB.
+// A full scan's kernels carry no row queue (1.5-2.5 KB static), so a plan with sample rate 1
+// gets 9 KB more for its tables (finer level-1 cells, fewer boundary records)
 constexpr int kStaticSmem = 12 * 1024;
+constexpr int kStaticSmemFull = 3 * 1024;
+#ifndef __CUDACC_RTC__     // host side only (NVRTC takes no unannotated functions)
+constexpr int static_smem_reserve(bool sample) { return sample ? kStaticSmem : kStaticSmemFull; }
+#endif
 constexpr uint32_t kNoThr = 0xFFFFFFFFu;
 constexpr uint32_t kSpecial = 0x80000000u;  // entry is a nested block or a list
 constexpr uint32_t kList = 0x40000000u;     // special entry is a short sorted list

@@ -25,7 +25,7 @@
 #define GACE_L2_PF_DIST 2      // L2 prefetch distance in grid-stride iterations
 #endif
 #ifndef GACE_L2_PREFETCH
-#define GACE_L2_PREFETCH 1
+#define GACE_L2_PREFETCH 2
 #endif
 #ifndef GACE_L2_PREFETCH_U           // the same for the multi-quad units of 1-2 column probes
 #define GACE_L2_PREFETCH_U 0
@@ -104,6 +104,12 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t off) {
     smem_check(off, 2);
     unsigned short v;
     asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(sbase() + off));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t off) {     // one LDS.128 (a record)
+    smem_check(off, 16);
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(sbase() + off));
     return v;
 }
 __device__ __forceinline__ void red_add1(uint32_t off) {
@@ -377,8 +383,7 @@ __device__ __forceinline__ uint32_t offset_of(const ProbeParams &P, int s, KeyT<
 // thresholds), or the full walk for nested / list records (sub-bucket via the map).
 template <class Sh>
 __device__ __forceinline__ uint32_t boundary_bucket(const ProbeParams &P, int s, uint32_t rec, uint32_t u) {
-    smem_check(16 * rec, 16);
-    const uint4 r = g_smem[rec];
+    const uint4 r = lds_u4(16 * rec);
     if (!(r.x & kSpecial)) {
         const uint32_t c1 = u > r.y, c2 = u > r.z, c3 = u > r.w;
         uint32_t b = (r.x & kIdxMask) + c1 + c2 + c3;
@@ -459,8 +464,7 @@ __device__ __forceinline__ void bucket_col(const ProbeParams &P, int s, const Ke
             for (int k = 0; k < 4; ++k) {
                 if (k >= nk || !(e[k] & sp)) continue;
                 if (Sh::fold(P, s)) u[k] = offset_of<Sh>(P, s, v[k]);
-                smem_check(16 * (e[k] & Sh::t1dmask(P, s)), 16);
-                const uint4 r = g_smem[e[k] & Sh::t1dmask(P, s)];
+                const uint4 r = lds_u4(16 * (e[k] & Sh::t1dmask(P, s)));
                 if (!(r.x & kSpecial)) {   // direct record, <= 3 thresholds: inline
                     const uint32_t c1 = u[k] > r.y, c2 = u[k] > r.z, c3 = u[k] > r.w;
                     uint32_t b = (r.x & kIdxMask) + 1u + c1 + c2 + c3;
@@ -767,6 +771,8 @@ constexpr uint32_t kQueue = 64;                       // entries per warp (ring)
 __shared__ uint32_t s_queue[kThreads / 32][kQueue];
 static_assert(sizeof(uint32_t) * (kThreads / 32) * kQueue + 2 * kMaxSlots * (kThreads / 32) +
                   4 * (kThreads / 32 + 1) * kMaxSlots <= kStaticSmem, "static shared memory over kStaticSmem");
+static_assert(2 * kMaxSlots * (kThreads / 32) + 4 * (kThreads / 32 + 1) * kMaxSlots <= kStaticSmemFull,
+              "a full scan's static shared memory over kStaticSmemFull");
 
 template <class Sh>
 __device__ __forceinline__ void probe_body(const ProbeParams &P) {
@@ -906,10 +912,23 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         }
         for (; u < nunits; u += stride) {
 #if GACE_L2_PREFETCH
-            // keys two iterations ahead pulled into L2 (one PREFETCH per column: the warp's 32
-            // lanes cover 512 contiguous bytes), so the register loads of the next iteration
-            // hit L2 (full scans only: a sampled probe must not fetch the rows it skips)
-            if (!Sh::SAMPLE && u + GACE_L2_PF_DIST * stride < nunits) {
+            // keys two iterations ahead pulled into L2, so the register loads of the next
+            // iteration hit L2 (full scans only: a sampled probe must not fetch the rows it skips).
+            // GACE_L2_PREFETCH=2 (int32 columns): one 128-byte line per lane -- lane l takes line
+            // l % 4 of column l / 4 (the warp's 512 bytes of a column are 4 lines), so a single
+            // PREFETCH covers every column.  (cp.async.bulk.prefetch needs a warp-uniform
+            // address: the compiler wraps it in a per-lane loop.)  Otherwise one PREFETCH per
+            // column, each lane its own 16 (32) bytes.
+            if (GACE_L2_PREFETCH == 2 && !Sh::I64 && NC <= 8) {
+                if (!Sh::SAMPLE) {
+                    const uint32_t lane = threadIdx.x & 31u;
+                    const uint32_t upf = u - lane + GACE_L2_PF_DIST * stride + 8u * (lane & 3u);
+                    const int s = (int)(lane >> 2);
+                    if (s < NC && upf < nunits && Sh::active(P, s))
+                        asm volatile("prefetch.global.L2 [%0];" ::
+                                     "l"(static_cast<const char *>(P.slot[s].ptr) + (uint64_t)upf * 16u));
+                }
+            } else if (!Sh::SAMPLE && u + GACE_L2_PF_DIST * stride < nunits) {
 #pragma unroll
                 for (int s = 0; s < NC; ++s) {
                     if (!Sh::active(P, s)) continue;

@@ -10,6 +10,7 @@ Names follow the C-ABI: ``table_attach`` / ``table_attach_host`` ->
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 from dataclasses import dataclass
@@ -36,7 +37,7 @@ EXPORTS = ["gace_table_attach", "gace_table_attach_host", "gace_table_detach", "
            "gace_table_graph_stats", "gace_probe", "gace_probe_sets", "gace_cost_fit", "gace_gate_decide", "gace_estimate_cv", "gace_cache_create", "gace_cache_destroy", "gace_cache_put",
            "gace_cache_lookup", "gace_cache_invalidate", "gace_cache_stats",
            "gace_sample_mask", "gace_derive", "gace_gate", "gace_last_timing", "gace_nccl_unique_id",
-           "gace_jit_sync", "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
+           "gace_jit_sync", "gace_jit_shutdown", "gace_debug_buckets", "gace_debug_jit_compile", "gace_kernel_launches", "gace_last_error"]
 
 
 class GaceError(RuntimeError):
@@ -110,6 +111,7 @@ def lib() -> ctypes.CDLL:
     L.gace_last_timing.argtypes = [vp, ctypes.POINTER(_Timing)]
     L.gace_nccl_unique_id.argtypes = [vp]
     L.gace_jit_sync.argtypes = [dbl, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    L.gace_jit_shutdown.argtypes = []
     L.gace_debug_jit_compile.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, dbl, ctypes.POINTER(u64)]
     L.gace_debug_buckets.argtypes = [u32, vp, vp, vp, i32, vp, u32, vp, u32, u64, u32, vp, u64, vp,
                                      ctypes.POINTER(u32), vp, u32, ctypes.POINTER(u32)]
@@ -121,6 +123,8 @@ def lib() -> ctypes.CDLL:
     L.gace_last_error.restype = ctypes.c_char_p
     L.gace_last_error.argtypes = []
     _lib = L
+    # stop the background compile worker before the interpreter tears down torch / CUDA
+    atexit.register(L.gace_jit_shutdown)
     return L
 
 

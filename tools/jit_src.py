@@ -11,7 +11,7 @@ import synth  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
 out = sys.argv[2] if len(sys.argv) > 2 else f"build/jit_{name}.cu"
 rows = int(sys.argv[3]) if len(sys.argv) > 3 else None     # default: the workload's full size
-# GACE_DEBUG_CLUSTERED=<slot mask> compiles the clustered-column path (C5: l_orderkey = 1)
+# GACE_DEBUG_CLUSTERED=<column mask> plans and compiles those columns as clustered (C5: l_orderkey = 1)
 os.makedirs("build", exist_ok=True)
 os.environ["GACE_JIT_SRC"] = out
 from paper_2512_19750_b200 import gace  # noqa: E402
