@@ -480,6 +480,15 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     const uint64_t csize = 1ull << s1;
     S.l1.reserve(ncells);
     Sweep at_lo{toff}, at_hi{toff};
+    // runs of cells without a breakpoint inside share one plain entry: the sweeps below jump
+    // from one breakpoint-holding cell to the next and fill the run between with std::fill
+    // (planning cost O(cells) memory writes + O(breakpoints) work, not per-cell searches)
+    auto run_end = [&](uint64_t k) -> uint64_t {      // first cell >= k holding a breakpoint in (lo, hi]
+        const uint32_t j = at_lo(k << s1);             // first breakpoint above this cell's start
+        if (j >= toff.size()) return ncells;
+        const uint64_t kn = toff[j] >> s1;             // its cell (at that cell's start: it bounds it)
+        return std::min<uint64_t>(kn, ncells);
+    };
     // a record of <= 3 breakpoints (the common boundary cell), from the sweep's own indices:
     // node()'s first case without its searches
     auto direct = [&](uint32_t b0, uint32_t cnt) -> uint4 {
@@ -493,6 +502,12 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
     if (S.fmt == FMT1T) {      // one in-cell threshold per cell (gace_plan.h FMT1T)
         auto bs = [&](uint32_t b) { return (b + 1) | (sub_of(b) << S.sb); };
         for (uint64_t k = 0; k < ncells && ok; ++k) {
+            const uint64_t ke = run_end(k);
+            if (ke > k) {                                          // plain run [k, ke)
+                S.l1.insert(S.l1.end(), ke - k, bs(at_lo(k << s1)) - 1);
+                k = ke - 1;
+                continue;
+            }
             const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
             const uint32_t b0 = at_lo(lo), cnt = at_hi(hi) - b0;   // breakpoints in (lo, hi]
             if (cnt == 0) {
@@ -509,6 +524,13 @@ bool build_lut(SlotPlan &S, uint64_t span, uint32_t s1) {
         return done();
     }
     for (uint64_t k = 0; k < ncells && ok; ++k) {
+        const uint64_t ke = run_end(k);
+        if (ke > k) {                                              // plain run [k, ke)
+            const uint32_t b0 = at_lo(k << s1);
+            S.l1.insert(S.l1.end(), ke - k, b0 | (sub_of(b0) << kSubShift));
+            k = ke - 1;
+            continue;
+        }
         const uint64_t lo = k << s1, hi = std::min<uint64_t>(lo + csize - 1, span);
         const uint32_t b0 = at_lo(lo), cnt = at_hi(hi) - b0;
         if (cnt == 0) {                                            // plain cell
@@ -913,6 +935,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         if (!size_lut(S, s1[i]) || (S.fmt == FMT16 && S.n_l2 > kRecMask16)) to_search(S);
     }
     const std::vector<uint32_t> s1_target = s1;
+    phase("luts-size");
     auto lut_total = [&]() {
         size_t tot = 0;
         for (auto &S : pl.slots)
@@ -946,6 +969,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         else if (!S.clamp && S.mode == MODE_LUT) S.base = S.dl;          // left FMT1T: plain domain cover
         if (!size_lut(S, s1[worst]) || (S.fmt == FMT16 && S.n_l2 > kRecMask16)) to_search(S);
     }
+    phase("luts-fit");
     // refine again where the halving steps above left room: the table whose keys most often
     // land in a boundary cell (a record walk, and for the warp a divergent branch; keys taken
     // as uniform over the span) first, never finer than its target, same format
@@ -977,6 +1001,7 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
         }
         if (!done) break;
     }
+    phase("luts-refine");
     // the tables sized by estimate: built once, at their final shift
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT || S.built) continue;
@@ -1106,23 +1131,41 @@ gace_status make_plan(const gace_table *t, const gace_pred *preds, uint32_t np, 
     for (auto &S : pl.slots) {
         if (S.mode != MODE_LUT) continue;
         uint16_t *img16 = reinterpret_cast<uint16_t *>(img32 + S.lut_idx);
-        for (size_t k = 0; k < S.l1.size(); ++k) {
-            const uint32_t c = S.l1[k];
-            const uint32_t idx = c & kIdxMask, sub = (c >> kSubShift) & kSubMask;
-            if (S.fmt == FMT1T) {
-                img32[S.lut_idx + k] = (c & t1_special(S.s1)) ? t1_special(S.s1) | (S.l2_idx + (c & t1_dmask(S.s1))) : c;
-            } else if (S.fmt == FMT16) {
-                img16[k] = (uint16_t)((c & kSpecial) ? 0x8000u | (S.l2_idx + (c & kRecMask)) : idx | (sub << 9));
-            } else if (S.fmt == FMTEX) {                   // cell k is the key base + k
+        uint32_t *dst = img32 + S.lut_idx;
+        const uint32_t *src = S.l1.data();
+        const size_t n1 = S.l1.size();
+        // one branch-free loop per format (vectorised; records are rare)
+        if (S.fmt == FMT1T) {
+            const uint32_t sp = t1_special(S.s1), dm = t1_dmask(S.s1), l2i = S.l2_idx;
+            for (size_t k = 0; k < n1; ++k) {
+                const uint32_t c = src[k];
+                dst[k] = (c & sp) ? sp | (l2i + (c & dm)) : c;
+            }
+        } else if (S.fmt == FMT16) {
+            const uint32_t l2i = S.l2_idx;
+            for (size_t k = 0; k < n1; ++k) {
+                const uint32_t c = src[k];
+                img16[k] = (uint16_t)((c & kSpecial) ? 0x8000u | (l2i + (c & kRecMask))
+                                                     : (c & kIdxMask) | (((c >> kSubShift) & kSubMask) << 9));
+            }
+        } else if (S.fmt == FMTEX) {                       // cell k is the key base + k
+            const bool hll_cells = S.has_hll && !S.clamp && !S.bm;
+            for (size_t k = 0; k < n1; ++k) {
+                const uint32_t c = src[k];
+                const uint32_t idx = c & kIdxMask, sub = (c >> kSubShift) & kSubMask;
                 uint32_t hidx = 0, rank = 0;
-                if (S.has_hll && !S.clamp && !S.bm) {
+                if (hll_cells) {
                     const uint32_t h = host_fmix32((uint32_t)(int32_t)(S.base + (int64_t)k));
                     hidx = h >> (32 - kHllP);
                     rank = (uint32_t)__builtin_clz((h << kHllP) | (1u << (kHllP - 1))) + 1;
                 }
-                img32[S.lut_idx + k] = S.fdirect ? 4 * (S.hist_w + idx) : idx | (sub << 9) | (hidx << 15) | (rank << 27);
-            } else {
-                img32[S.lut_idx + k] = (c & kSpecial) ? kSpecial | (S.l2_idx + (c & kRecMask)) : c;
+                dst[k] = S.fdirect ? 4 * (S.hist_w + idx) : idx | (sub << 9) | (hidx << 15) | (rank << 27);
+            }
+        } else {
+            const uint32_t l2i = S.l2_idx;
+            for (size_t k = 0; k < n1; ++k) {
+                const uint32_t c = src[k];
+                dst[k] = (c & kSpecial) ? kSpecial | (l2i + (c & kRecMask)) : c;
             }
         }
         for (size_t k = 0; k < S.l2.size(); ++k) img4[S.l2_idx + k] = fix(S.l2[k], S);
