@@ -537,3 +537,32 @@ def test_chunked_launches(G, oracle, monkeypatch, jit, name, nrows, rate):
         assert t.last_timing()["scan_launches"] == (nrows + 100003) // 100004
     finally:
         t.detach()
+
+
+_EXIT_SCRIPT = r"""
+import sys
+sys.path.insert(0, ".")
+import torch, synth
+from paper_2512_19750_b200 import gace
+w = synth.get(sys.argv[1], 300_000)
+t = gace.Table([w.column(c, device="cuda") for c in range(len(w.columns))])
+r = t.probe(w.preds, w.pairs, float(sys.argv[2]), 1, w.hll_cols)   # queues a background compile
+print("probed", r.n_sampled, flush=True)
+"""
+
+
+@pytest.mark.parametrize("name,rate", [("C1", 1.0), ("C5", 1.0), ("C2", 0.01), ("C4", 1.0)])
+def test_exit_with_compile_in_flight(G, name, rate):
+    """A process that exits right after its first probe -- the background NVRTC compile of
+    the specialised kernel still queued or running -- exits cleanly (gace_jit_shutdown from the
+    binding's atexit hook; without it such exits crashed or hung)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("GACE_JIT", None)                       # the default: background compiles
+    r = subprocess.run([sys.executable, "-c", _EXIT_SCRIPT, name, str(rate)], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=180)
+    assert r.returncode == 0, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
+    assert "probed" in r.stdout

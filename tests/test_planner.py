@@ -147,3 +147,42 @@ def test_specialised_kernel_compiles(G, name, monkeypatch):
         n = gace.debug_jit_compile(dt, [int(x.min()) for x in t], [int(x.max()) for x in t], False,
                                    w.preds, w.pairs, w.hll_cols, rate)
         assert n > 1000
+
+
+def test_table_sizing_by_estimate(G, oracle, monkeypatch, capfd):
+    """The planner sizes candidate table resolutions by estimate and builds each table once
+    (gace_host.cpp lut_estimate): the plan it picks must be the one it picks by building every
+    candidate (GACE_NO_LUT_ESTIMATE=1) -- same formats, shifts, cell and record counts, shared
+    memory -- on batches whose tables have to be coarsened and refined to fit (four wide
+    columns, hundreds of ranges, narrow ones that put two breakpoints in a cell, breakpoints on
+    cell starts, pair grids taking shared memory), and every column still resolves exactly."""
+    g = np.random.default_rng(11)
+    for trial in range(12):
+        spans = [int(10 ** g.uniform(4, 9)) for _ in range(4)]
+        rows = []
+        for c, sp in enumerate(spans):
+            for _ in range(int(g.integers(20, 160))):
+                a = int(g.integers(0, sp))
+                w = int(g.choice([0, 1, 3, 100, sp // 50 + 1]))
+                rows.append((c, 5, 0, a, min(a + w, sp)))
+            for k in range(8):                          # on power-of-two cell starts
+                rows.append((c, 2, 0, (k + 1) << int(g.integers(4, 16)), 0))
+        P = np.array(rows, dtype=synth.PRED_DTYPE)
+        pairs = np.array([(i, j) for i in range(0, len(P), 37) for j in range(5, len(P), 53)
+                          if P["col"][i] != P["col"][j]][:64], dtype=synth.PAIR_DTYPE)
+        dt, lo, hi = [0] * 4, [0] * 4, spans
+        dumps = []
+        for est in (True, False):
+            if est:
+                monkeypatch.delenv("GACE_NO_LUT_ESTIMATE", raising=False)
+            else:
+                monkeypatch.setenv("GACE_NO_LUT_ESTIMATE", "1")
+            monkeypatch.setenv("GACE_PLAN_DUMP", "1")
+            capfd.readouterr()
+            G.debug_buckets(dt, lo, hi, False, P, pairs, [0, 1, 2, 3], 0, [0])
+            dumps.append([l for l in capfd.readouterr().err.splitlines() if l.startswith(("slot", "smem"))])
+            monkeypatch.delenv("GACE_PLAN_DUMP")
+        assert dumps[0] == dumps[1] and dumps[0], dumps
+        for c in range(4):
+            _, _, bps = G.debug_buckets(dt, lo, hi, False, P, pairs, [0, 1, 2, 3], c, [])
+            _check_column(G, oracle, dt, lo, hi, False, P, pairs, [0, 1, 2, 3], c, _values(g, 0, spans[c], bps, 3000))
