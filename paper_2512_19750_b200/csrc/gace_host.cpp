@@ -1668,6 +1668,11 @@ std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::v
     o += "  static constexpr bool STATIC = true;\n";
     o += "  static constexpr int U = NC >= 4 ? 1 : 4 / NC;\n";
     o += "  static constexpr int NG = " + std::to_string(P.ngroups) + ";\n";
+    {   // no HLL column: the skip-bound refresh points are compiled out
+        bool any_hll = false;
+        for (uint32_t i = 0; i < P.nslots; ++i) any_hll |= P.slot[i].has_hll != 0;
+        o += "  static constexpr bool ANY_HLL = " + std::string(any_hll ? "true" : "false") + ";\n";
+    }
     o += "  __device__ static constexpr bool active(const ProbeParams &, int s) { return s < NC; }\n";
     o += "  __device__ static constexpr int mode(const ProbeParams &, int s) { return " +
          chain([&](int i) { return std::to_string((int)P.slot[i].mode); }, nc) + "; }\n";

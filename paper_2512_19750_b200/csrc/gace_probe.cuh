@@ -286,6 +286,7 @@ struct RtShape : RtLayout {
     static constexpr bool SAMPLE = SAMPLE_;
     static constexpr bool I64 = I64_;
     static constexpr bool STATIC = false;
+    static constexpr bool ANY_HLL = true;          // refresh points always present
     static constexpr int U = NC >= 4 ? 1 : 4 / NC;
     static constexpr int NG = 0;
     __device__ static bool active(const ProbeParams &P, int s) { return s < (int)P.nslots; }
@@ -796,7 +797,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
     uint32_t bmfull = 0;       // bit s: slot s's HLL is complete -- merged presence bitmap full, or
                                // merged registers at their ceilings (warp-uniform)
     auto body = [&](const Unit<Sh> &X, uint32_t u) {
-        if (it == next_refresh) {
+        if (Sh::ANY_HLL && it == next_refresh) {
             next_refresh = it + min(it, 32u);
             if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
@@ -868,7 +869,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
         const uint32_t nq = nunits * U;
         for (uint32_t ub = u - lane; ub < nq; ub += stride) {
             const uint32_t uu = ub + lane;
-            if (it == next_refresh) {
+            if (Sh::ANY_HLL && it == next_refresh) {
                 next_refresh = it + min(it, 32u);
 #pragma unroll
                 for (int s = 0; s < NC; ++s)
@@ -887,7 +888,8 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
                 __syncwarp();
             }
             ++it;
-            const uint32_t keep = uu < nq ? quad_keep(uu) : 0u;
+            // hashed past the end too (pure arithmetic), masked: no branch around the hash
+            const uint32_t keep = quad_keep(uu) & (uu < nq ? 0xFu : 0u);
             kept += __popc(keep);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {              // row k of every lane's quad: <= 32 new entries
@@ -942,7 +944,7 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             uint32_t un = u + stride < nunits ? u + stride : kNoUnit;
             const uint32_t keep_n = un != kNoUnit ? quad_keep(un) : 0u;
             if (!keep_n) un = kNoUnit;
-            if (it == next_refresh) {
+            if (Sh::ANY_HLL && it == next_refresh) {
                 next_refresh = it + min(it, 32u);
                 if (__activemask() == 0xFFFFFFFFu) {
 #pragma unroll
