@@ -18,3 +18,20 @@ def oracle():
     from oracle import reference
     reference.build()
     return reference
+
+
+_FULL_SIZE = []
+
+
+def pytest_runtest_logreport(report):
+    # full BASELINE-size parity tests (marked slow): remembered for the summary below
+    if report.when == "call" and "slow" in report.keywords:
+        _FULL_SIZE.append((report.nodeid, report.outcome, report.duration))
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Name the full-size tests in the tail of a quiet run (-q prints only dots)."""
+    if _FULL_SIZE:
+        terminalreporter.write_line("full BASELINE-size tests (oracle parity, shard invariance):")
+        for nodeid, outcome, dur in _FULL_SIZE:
+            terminalreporter.write_line(f"  {outcome:7s} {dur:7.1f} s  {nodeid}")
