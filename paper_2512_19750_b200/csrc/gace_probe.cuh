@@ -890,15 +890,37 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             ++it;
             // hashed past the end too (pure arithmetic), masked: no branch around the hash
             const uint32_t keep = quad_keep(uu) & (uu < nq ? 0xFu : 0u);
-            kept += __popc(keep);
+            const uint32_t c = __popc(keep);
+            kept += c;
+            if (!__ballot_sync(0xFFFFFFFFu, keep)) continue;      // no kept row in the warp's 128
+            // one warp prefix sum of the lanes' kept-row counts places every kept row of the
+            // iteration at once (instead of a ballot per quad row)
+            uint32_t incl = c;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {              // row k of every lane's quad: <= 32 new entries
-                const uint32_t b = __ballot_sync(0xFFFFFFFFu, (keep >> k) & 1u);
-                if (!b) continue;
-                if ((b >> lane) & 1u) q[(qt + __popc(b & ((1u << lane) - 1u))) % kQueue] = uu * 4 + k;
-                qt += __popc(b);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            if (qt - qh + total <= kQueue) {
+                uint32_t pos = qt + incl - c, m = keep;
+                while (m) {
+                    q[pos++ % kQueue] = uu * 4 + (__ffs(m) - 1);
+                    m &= m - 1;
+                }
+                qt += total;
                 __syncwarp();
-                if (qt - qh >= 32) work(32);
+                while (qt - qh >= 32) work(32);
+            } else {                                   // > 64 - pending at once: row by row
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {          // row k of every lane's quad: <= 32 new entries
+                    const uint32_t b = __ballot_sync(0xFFFFFFFFu, (keep >> k) & 1u);
+                    if (!b) continue;
+                    if ((b >> lane) & 1u) q[(qt + __popc(b & ((1u << lane) - 1u))) % kQueue] = uu * 4 + k;
+                    qt += __popc(b);
+                    __syncwarp();
+                    if (qt - qh >= 32) work(32);
+                }
             }
         }
         if (qt != qh) work(qt - qh);                  // the last partial batch
