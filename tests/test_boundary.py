@@ -84,3 +84,15 @@ def test_derive_matches_oracle(G, oracle):
     assert math.isnan(sel[0]) and math.isnan(pcs[0])
     with pytest.raises(G.GaceError):
         G.derive(5, [1], [], [], np.zeros((1, 4096), np.uint8), [0.0])
+
+
+def test_jit_shutdown_idempotent(G):
+    """gace_jit_shutdown (the binding's atexit hook) is callable with no worker started, twice,
+    and leaves a clean exit (run in a child process: it stops background compiles for good)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); from paper_2512_19750_b200 import gace; L = gace.lib(); "
+            "print(L.gace_jit_shutdown(), L.gace_jit_shutdown())")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.split() == ["0", "0"]
