@@ -566,3 +566,36 @@ def test_exit_with_compile_in_flight(G, name, rate):
                        capture_output=True, text=True, timeout=180)
     assert r.returncode == 0, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
     assert "probed" in r.stdout
+
+
+@pytest.mark.parametrize("trial", range(4))
+@pytest.mark.parametrize("force_jit", [False, True])
+def test_budget_bound_refined_tables(G, oracle, monkeypatch, trial, force_jit):
+    """Plans at the full-scan shared-memory budget (224 KB): four wide int32 columns with up to
+    160 ranges each (narrow ones put several breakpoints in a cell, others sit on power-of-two
+    cell starts), 64 cross-column pairs and HLL on every column, so the planner coarsens and
+    then refines the tables (test_planner.py::test_table_sizing_by_estimate).  Exact against the
+    oracle through the generic and the plan-specialised kernel, full scan and sampled."""
+    if force_jit:
+        monkeypatch.setenv("GACE_JIT", "1")
+        monkeypatch.setenv("GACE_JIT_MIN_ROWS", "0")
+    g = np.random.default_rng(100 + trial)
+    n = 300_007
+    spans = [int(10 ** g.uniform(4, 9)) for _ in range(4)]
+    cols = [g.integers(0, sp, size=n, endpoint=True).astype(np.int32) for sp in spans]
+    for c, sp in enumerate(spans):          # exact domain ends, whatever the draw
+        cols[c][c] = 0
+        cols[c][c + 4] = sp
+    rows = []
+    for c, sp in enumerate(spans):
+        for _ in range(int(g.integers(20, 160))):
+            a = int(g.integers(0, sp))
+            w = int(g.choice([0, 1, 3, 100, sp // 50 + 1]))
+            rows.append((c, 5, 0, a, min(a + w, sp)))
+        for k in range(8):
+            rows.append((c, 2, 0, (k + 1) << int(g.integers(4, 16)), 0))
+    P = np.array(rows, dtype=synth.PRED_DTYPE)
+    Q = np.array([(i, j) for i in range(0, len(P), 37) for j in range(5, len(P), 53)
+                  if P["col"][i] != P["col"][j]][:64], dtype=synth.PAIR_DTYPE)
+    for rate in (1.0, 0.3):
+        _check(G, oracle, cols, P, Q, rate=rate, seed=trial, hll_cols=[0, 1, 2, 3])
