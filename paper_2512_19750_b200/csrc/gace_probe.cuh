@@ -122,6 +122,12 @@ __device__ __forceinline__ void red_add1(uint32_t off) {
 __device__ __forceinline__ uint32_t saddr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// by byte offset into the dynamic window (the uniform base folds into the address operand)
+__device__ __forceinline__ void red_max_if_off(bool pred, uint32_t off, uint32_t v) {
+    if (pred) smem_check(off, 4);
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.max.u32 [%1], %2;\n}"
+                 :: "r"((uint32_t)pred), "r"(sbase() + off), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_max_if(bool pred, const uint32_t *addr, uint32_t v) {
     if (pred) smem_check(saddr(addr) - sbase(), 4);
     asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.max.u32 [%1], %2;\n}"
@@ -638,15 +644,17 @@ __device__ __forceinline__ void column_tail(const ProbeParams &P, int s, uint32_
                 // compares): a frequent value whose rank is already in (a skewed column's
                 // head, e.g. fmix32(0) = 0 -> rank 21) never reaches the atomic
                 // rank > cur  <=>  w <= ~0 >> cur (cur <= 21; 31 marks "not a survivor": w >= 2^11)
+                // (registers addressed by byte offset from the dynamic window's uniform base)
+                const uint32_t roff = 4 * Sh::hllw(P, s);
                 uint32_t cur[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    cur[k] = w32[k] <= lim ? R[idx[k]] : 31u;
+                    cur[k] = w32[k] <= lim ? lds_u32(roff + 4 * idx[k]) : 31u;
                     if (same) break;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    red_max_if(w32[k] <= (0xFFFFFFFFu >> cur[k]), R + idx[k], __clz(w32[k]) + 1);
+                    red_max_if_off(w32[k] <= (0xFFFFFFFFu >> cur[k]), roff + 4 * idx[k], __clz(w32[k]) + 1);
                     if (same) break;
                 }
             }
