@@ -26,6 +26,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <charconv>
 #include <chrono>
 #include <mutex>
 #include <string>
@@ -1652,96 +1653,141 @@ int jit_threads(const Plan &pl) {
 // offsets, shifts and masks baked in as immediates too (one kernel per batch layout).
 std::string jit_shape_source(const Plan &pl, bool sample, bool i64, const std::vector<uint8_t> &clustered,
                              bool layout) {
+    // (every piece appended in place: a new batch's structure-keyed source is generated on the
+    // probe's host path, so no temporaries per term)
     const ProbeParams &P = pl.P;
     const int nc = (int)P.nslots;
-    auto chain = [&](auto f, int n) {
-        std::string r;
-        for (int i = 0; i < n; ++i) r += "s == " + std::to_string(i) + " ? " + f(i) + " : ";
-        return r + "0";
-    };
     std::string o;
-    if (jit_threads(pl) != 1024) o += "#define GACE_THREADS " + std::to_string(jit_threads(pl)) + "\n";
+    o.reserve(layout ? 8192 : 4096);
+    char nb[64];
+    auto num = [&](long long v) { o.append(nb, (size_t)(std::to_chars(nb, nb + sizeof nb, v).ptr - nb)); };
+    auto bit = [&](bool v) { o += v ? '1' : '0'; };
+    auto tf = [&](bool v) { o += v ? "true" : "false"; };
+    // "s == 0 ? f(0) : s == 1 ? f(1) : ... 0" (f appends its term)
+    auto chain = [&](auto f, int n) {
+        for (int i = 0; i < n; ++i) {
+            o += "s == ";
+            num(i);
+            o += " ? ";
+            f(i);
+            o += " : ";
+        }
+        o += '0';
+    };
+    auto gchain = [&](auto f) {
+        for (uint32_t g = 0; g < P.ngroups; ++g) {
+            o += "g == ";
+            num(g);
+            o += " ? ";
+            f(g);
+            o += " : ";
+        }
+        o += '0';
+    };
+    // one trait: "  __device__ static constexpr <type> <name>(<args>) { return <chain>; }\n"
+    auto trait = [&](const char *head, auto body) {
+        o += "  __device__ static constexpr ";
+        o += head;
+        o += " { return ";
+        body();
+        o += "; }\n";
+    };
+    const int threads = jit_threads(pl);
+    if (threads != 1024) {
+        o += "#define GACE_THREADS ";
+        num(threads);
+        o += '\n';
+    }
     o += "namespace gace {\nstruct JitShape : RtLayout {\n";
-    o += "  static constexpr int NC = " + std::to_string(nc) + ";\n";
-    o += "  static constexpr bool SAMPLE = " + std::string(sample ? "true" : "false") + ";\n";
-    o += "  static constexpr bool I64 = " + std::string(i64 ? "true" : "false") + ";\n";
-    o += "  static constexpr bool STATIC = true;\n";
+    o += "  static constexpr int NC = ";
+    num(nc);
+    o += ";\n  static constexpr bool SAMPLE = ";
+    tf(sample);
+    o += ";\n  static constexpr bool I64 = ";
+    tf(i64);
+    o += ";\n  static constexpr bool STATIC = true;\n";
     o += "  static constexpr int U = NC >= 4 ? 1 : 4 / NC;\n";
-    o += "  static constexpr int NG = " + std::to_string(P.ngroups) + ";\n";
+    o += "  static constexpr int NG = ";
+    num(P.ngroups);
+    o += ";\n";
     {   // no HLL column: the skip-bound refresh points are compiled out
         bool any_hll = false;
         for (uint32_t i = 0; i < P.nslots; ++i) any_hll |= P.slot[i].has_hll != 0;
-        o += "  static constexpr bool ANY_HLL = " + std::string(any_hll ? "true" : "false") + ";\n";
+        o += "  static constexpr bool ANY_HLL = ";
+        tf(any_hll);
+        o += ";\n";
     }
     o += "  __device__ static constexpr bool active(const ProbeParams &, int s) { return s < NC; }\n";
-    o += "  __device__ static constexpr int mode(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::to_string((int)P.slot[i].mode); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool is32(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].dtype == 0 ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool hll(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].has_hll ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool clamp(const ProbeParams &) { return " +
-         std::string(P.clamp ? "true" : "false") + "; }\n";
-    o += "  __device__ static constexpr bool packs(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].prim_b >= 0 ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr int fmt(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::to_string((int)P.slot[i].fmt); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool clust(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(clustered[i] ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool fdirect(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].fdirect ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool ownh(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].mode != MODE_NOPRED && P.slot[i].hist_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
-    auto gchain = [&](auto f) {
-        std::string r;
-        for (uint32_t g = 0; g < P.ngroups; ++g) r += "g == " + std::to_string(g) + " ? " + f(g) + " : ";
-        return r + "0";
+    auto slot_bits = [&](const char *head, auto pred) {
+        trait(head, [&] { chain([&](int i) { bit(pred(i)); }, nc); });
     };
-    o += "  __device__ static constexpr int ga(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].a); }) + "; }\n";
-    o += "  __device__ static constexpr int gb(int g) { return " + gchain([&](uint32_t g) { return std::to_string((int)P.grp[g].b); }) + "; }\n";
-    o += "  __device__ static constexpr bool gpacked(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].packed ? "1" : "0"); }) + "; }\n";
-    o += "  __device__ static constexpr bool ggrid(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].has_grid ? "1" : "0"); }) + "; }\n";
-    o += "  __device__ static constexpr bool gdirect(int g) { return " + gchain([&](uint32_t g) { return std::string(P.grp[g].dend > P.grp[g].dbeg ? "1" : "0"); }) + "; }\n";
-    // plan layout as immediates (the lookup-table contents stay in shared memory)
-    auto u32s = [](uint32_t v) { return std::to_string(v) + "u"; };
-    auto i64s = [](int64_t v) {
-        char b[40];
-        snprintf(b, sizeof b, "(int64_t)%lldLL", (long long)v);
-        if (v == INT64_MIN) snprintf(b, sizeof b, "(int64_t)(-9223372036854775807LL - 1)");
-        return std::string(b);
-    };
-    auto slot_u32 = [&](const char *name, auto f) {
-        o += std::string("  __device__ static constexpr uint32_t ") + name + "(const ProbeParams &, int s) { return " +
-             chain([&](int i) { return u32s(f(P.slot[i])); }, nc) + "; }\n";
-    };
-    auto slot_i64 = [&](const char *name, auto f) {
-        o += std::string("  __device__ static constexpr int64_t ") + name + "(const ProbeParams &, int s) { return " +
-             chain([&](int i) { return i64s(f(P.slot[i])); }, nc) + "; }\n";
-    };
-    auto grp_u32 = [&](const char *name, auto f) {
-        o += std::string("  __device__ static constexpr uint32_t ") + name + "(const ProbeParams &, int g) { return " +
-             gchain([&](uint32_t g) { return u32s(f(P.grp[g])); }) + "; }\n";
-    };
+    trait("int mode(const ProbeParams &, int s)", [&] { chain([&](int i) { num((int)P.slot[i].mode); }, nc); });
+    slot_bits("bool is32(const ProbeParams &, int s)", [&](int i) { return P.slot[i].dtype == 0; });
+    slot_bits("bool hll(const ProbeParams &, int s)", [&](int i) { return P.slot[i].has_hll != 0; });
+    trait("bool clamp(const ProbeParams &)", [&] { tf(P.clamp != 0); });
+    slot_bits("bool packs(const ProbeParams &, int s)", [&](int i) { return P.slot[i].prim_b >= 0; });
+    trait("int fmt(const ProbeParams &, int s)", [&] { chain([&](int i) { num((int)P.slot[i].fmt); }, nc); });
+    slot_bits("bool clust(const ProbeParams &, int s)", [&](int i) { return clustered[i] != 0; });
+    slot_bits("bool fdirect(const ProbeParams &, int s)", [&](int i) { return P.slot[i].fdirect != 0; });
+    slot_bits("bool ownh(const ProbeParams &, int s)",
+              [&](int i) { return P.slot[i].mode != MODE_NOPRED && P.slot[i].hist_addr != kNone; });
+    trait("int ga(int g)", [&] { gchain([&](uint32_t g) { num((int)P.grp[g].a); }); });
+    trait("int gb(int g)", [&] { gchain([&](uint32_t g) { num((int)P.grp[g].b); }); });
+    trait("bool gpacked(int g)", [&] { gchain([&](uint32_t g) { bit(P.grp[g].packed != 0); }); });
+    trait("bool ggrid(int g)", [&] { gchain([&](uint32_t g) { bit(P.grp[g].has_grid != 0); }); });
+    trait("bool gdirect(int g)", [&] { gchain([&](uint32_t g) { bit(P.grp[g].dend > P.grp[g].dbeg); }); });
     {
         const char *ab = knob("GACE_ABLATE");          // design experiments: ablations baked in
-        o += std::string("  __device__ static constexpr uint32_t dbg(const ProbeParams &) { return ") +
-             std::to_string(ab ? (uint32_t)strtoul(ab, nullptr, 0) : 0u) + "u; }\n";
+        trait("uint32_t dbg(const ProbeParams &)", [&] {
+            num(ab ? (long long)(uint32_t)strtoul(ab, nullptr, 0) : 0ll);
+            o += 'u';
+        });
     }
-    o += "  __device__ static constexpr bool hllbm(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(P.slot[i].bm_addr != kNone ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool fold(const ProbeParams &, int s) { return " +
-         chain([&](int i) { return std::string(slot_foldable(P.slot[i]) ? "1" : "0"); }, nc) + "; }\n";
-    o += "  __device__ static constexpr bool sclamp(const ProbeParams &, int s) { return " +
-         chain([&](int i) {
-             const SlotParams &Q = P.slot[i];
-             const bool c = Q.dtype == 0 ? (Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX)
-                                         : (Q.clamp_lo != INT64_MIN || Q.clamp_hi != INT64_MAX);
-             return std::string(c ? "1" : "0");
-         }, nc) + "; }\n";
+    slot_bits("bool hllbm(const ProbeParams &, int s)", [&](int i) { return P.slot[i].bm_addr != kNone; });
+    slot_bits("bool fold(const ProbeParams &, int s)", [&](int i) { return slot_foldable(P.slot[i]); });
+    slot_bits("bool sclamp(const ProbeParams &, int s)", [&](int i) {
+        const SlotParams &Q = P.slot[i];
+        return Q.dtype == 0 ? (Q.clamp_lo != INT32_MIN || Q.clamp_hi != INT32_MAX)
+                            : (Q.clamp_lo != INT64_MIN || Q.clamp_hi != INT64_MAX);
+    });
     if (!layout) {
         o += "};\n}  // namespace gace\n";
         return o;
     }
+    // plan layout as immediates (the lookup-table contents stay in shared memory)
+    auto u32 = [&](uint32_t v) {
+        num(v);
+        o += 'u';
+    };
+    auto i64v = [&](int64_t v) {
+        if (v == INT64_MIN) o += "(int64_t)(-9223372036854775807LL - 1)";
+        else {
+            o += "(int64_t)";
+            num((long long)v);
+            o += "LL";
+        }
+    };
+    auto slot_u32 = [&](const char *name, auto f) {
+        o += "  __device__ static constexpr uint32_t ";
+        o += name;
+        o += "(const ProbeParams &, int s) { return ";
+        chain([&](int i) { u32(f(P.slot[i])); }, nc);
+        o += "; }\n";
+    };
+    auto slot_i64 = [&](const char *name, auto f) {
+        o += "  __device__ static constexpr int64_t ";
+        o += name;
+        o += "(const ProbeParams &, int s) { return ";
+        chain([&](int i) { i64v(f(P.slot[i])); }, nc);
+        o += "; }\n";
+    };
+    auto grp_u32 = [&](const char *name, auto f) {
+        o += "  __device__ static constexpr uint32_t ";
+        o += name;
+        o += "(const ProbeParams &, int g) { return ";
+        gchain([&](uint32_t g) { u32(f(P.grp[g])); });
+        o += "; }\n";
+    };
     slot_i64("base", [](const SlotParams &Q) { return Q.base; });
     slot_u32("foldb", [&](const SlotParams &Q) { return Q.fold_b; });
     slot_u32("foldz", [&](const SlotParams &Q) { return Q.fold_z; });
@@ -3175,6 +3221,12 @@ extern "C" gace_status gace_debug_jit_compile(uint32_t ncols, const gace_dtype *
     size_t n = 0;
     std::vector<uint8_t> cl(pl.slots.size(), 0);
     for (size_t i = 0; i < cl.size(); ++i) cl[i] = t.clustered[pl.slots[i].col];
+    if (getenv("GACE_PLAN_PROFILE")) {       // design inspection: cost of generating the source
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < 20; ++r) (void)jit_shape_source(pl, sample_rate < 1.0, i64, cl, false);
+        fprintf(stderr, "jit_shape_source (structure-keyed) %.1f us\n",
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / 20);
+    }
     if (!jit_compile_check(jit_shape_source(pl, sample_rate < 1.0, i64, cl, jit_layout()), &n, &err))
         return fail(GACE_EUNSUPPORTED, err);
     if (cubin_bytes) *cubin_bytes = n;
