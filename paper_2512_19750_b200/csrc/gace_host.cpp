@@ -2313,8 +2313,11 @@ gace_status gace_probe(gace_table *t, const gace_pred *preds, uint32_t npreds, c
     P.thr = threshold_of(sample_rate);
     P.seed = seed;
     P.sample_all = sample_rate >= 1.0 ? 1u : 0u;
-    // sparse samples: kept rows compacted per warp (gace_probe.cuh s_queue); GACE_COMPACT=0/1 overrides
-    P.compact = knob("GACE_COMPACT") ? (uint32_t)(atoi(knob("GACE_COMPACT")) != 0) : (sample_rate < 0.125 ? 1u : 0u);
+    // samples below 3/8: kept rows compacted per warp (gace_probe.cuh s_queue); above, the
+    // whole-quad path.  Measured on C5 (tools/compact_sweep.py): compaction 2.64 / 2.32 / 2.02 ms
+    // at rates 0.3 / 0.2 / 0.1 against 3.23 / 3.24 / 3.38 for whole quads, 3.84 against 3.16 at
+    // 0.5.  GACE_COMPACT=0/1 overrides.
+    P.compact = knob("GACE_COMPACT") ? (uint32_t)(atoi(knob("GACE_COMPACT")) != 0) : (sample_rate < 0.375 ? 1u : 0u);
     if (ab_env) P.dbg = (uint32_t)strtoul(ab_env, nullptr, 0);   // design experiments only
     const uint64_t row_offset = t->has_dist ? t->dist.row_offset : 0;
 

@@ -771,7 +771,7 @@ __device__ __noinline__ uint32_t tail_row(const ProbeParams &P, uint64_t r) {
     return 1;
 }
 
-// Sparse samples (rate < 1/8): each warp hashes the sample bits of its row quads, queues the
+// Sparse samples (rate < 3/8, gace_host.cpp P.compact): each warp hashes the sample bits of its row quads, queues the
 // kept rows' indices in shared memory, and works on them 32 at a time -- every lane one kept
 // row -- instead of running the per-quad work for the few lanes whose quad kept a row (at rate
 // 0.01, 72 % of the warps had a kept row somewhere, so almost every warp paid the whole quad
