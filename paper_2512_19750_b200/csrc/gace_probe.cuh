@@ -24,8 +24,13 @@
 #ifndef GACE_L2_PF_DIST
 #define GACE_L2_PF_DIST 2      // L2 prefetch distance in grid-stride iterations
 #endif
+// L2 prefetch of the column-streamed keys two iterations ahead: 0 none; 1 one PREFETCH per
+// column; 2 one per iteration for int32 plans (lane-distributed), per column for int64 plans;
+// 3 (default) none for int32 plans, per column for int64 plans -- measured (tools/variants.sh,
+// GACE_JIT_DEFS=GACE_L2_PREFETCH=n): C5 1.95-1.96 ms without, 1.98 with; C5_i64 2.76 ms with,
+// 3.12 without
 #ifndef GACE_L2_PREFETCH
-#define GACE_L2_PREFETCH 2
+#define GACE_L2_PREFETCH 3
 #endif
 #ifndef GACE_L2_PREFETCH_U           // the same for the multi-quad units of 1-2 column probes
 #define GACE_L2_PREFETCH_U 0
@@ -951,7 +956,10 @@ __device__ __forceinline__ void probe_body(const ProbeParams &P) {
             // PREFETCH covers every column.  (cp.async.bulk.prefetch needs a warp-uniform
             // address: the compiler wraps it in a per-lane loop.)  Otherwise one PREFETCH per
             // column, each lane its own 16 (32) bytes.
-            if (GACE_L2_PREFETCH == 2 && !Sh::I64 && NC <= 8) {
+            if (GACE_L2_PREFETCH == 3 && !Sh::I64) {
+                // int32 plans: no prefetch (the column-streamed register loads keep enough
+                // bytes in flight)
+            } else if (GACE_L2_PREFETCH == 2 && !Sh::I64 && NC <= 8) {
                 if (!Sh::SAMPLE) {
                     const uint32_t lane = threadIdx.x & 31u;
                     const uint32_t upf = u - lane + GACE_L2_PF_DIST * stride + 8u * (lane & 3u);
